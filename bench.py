@@ -1,0 +1,413 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native FP8 training primitives (BASELINE.json metric:
+"FP8 E5M2 GEMM TFLOP/s & % FP8 peak; quantize/SR-update GB/s & % HBM BW").
+
+Headline workload (BASELINE.json configs[1]): the
+elementwise quantization sweep over 2^28 FP32 values per GPU, |x| log-uniform
+in [2^-24, 2^17] with random sign plus 1% exact E5M2 ties. One step = the three
+sweeps of that config over the whole tensor:
+    E5M2 RNE                          5 B/elem (4 read + 1 write)
+    E5M2 SR, reference LFSR stream    5 B/elem
+    FP32->FP16 SR, counter 32-bit bits 6 B/elem (bits generated in-kernel)
+= 16 algorithmic bytes per element. `value` is GB/s of algorithmic bytes over
+all ranks (weak scaling: every rank sweeps its own 2^28 values; no collective
+on the data path). Inputs (1 GiB) exceed the 126 MB L2, so no flush is needed.
+
+Secondary lines in the same JSON (timed separately, outside the headline):
+SGD-momentum update into FP16 masters (GB/s), the tcgen05 E5M2 GEMM
+(TFLOP/s at 8192^3) and the config-1 layer step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP8 E5M2 quantize sweep GB/s & % HBM BW (config 2: RNE + LFSR-SR E5M2 + SR FP16)"
+BYTES_PER_ELEM = {"e5m2_rne": 5, "e5m2_sr_lfsr": 5, "fp16_sr_counter": 6}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    world, rank, local = _dist_init()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_mod
+    import paper_1905_12334_b200 as F
+    F.init()
+    hbm_peak, bf16_peak, peak_src = _peaks()
+    n = 1 << args.log2n
+    stream = torch.cuda.current_stream()
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    F.fill_synthetic(x, "config2", seed=rank, p=0.01)  # SURVEY 8d config 2, seed 0 on rank 0
+    c8a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    c8b = torch.empty(n, dtype=torch.uint8, device="cuda")
+    c16 = torch.empty(n, dtype=torch.int16, device="cuda")
+    cnt = [F.Counters() for _ in range(3)]
+
+    def step(evs=None):
+        if evs: evs[0].record(stream)
+        F.quantize(x, "fp8", "nearest-even", 1, out=c8a, counters=cnt[0])
+        if evs: evs[1].record(stream)
+        F.quantize(x, "fp8", "stochastic", 1, bits="lfsr", out=c8b, counters=cnt[1])
+        if evs: evs[2].record(stream)
+        F.quantize(x, "fp16", "stochastic", 1, bits="counter", out=c16, counters=cnt[2])
+        if evs: evs[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    per_step_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                    for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = F.launch_count()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for s in range(args.steps):
+            step(per_step_evs[s])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    launches = F.launch_count() - l0
+    if dist:
+        dist.barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    kt = {k: 0.0 for k in BYTES_PER_ELEM}
+    for evs in per_step_evs:
+        for j, k in enumerate(BYTES_PER_ELEM):
+            kt[k] += evs[j].elapsed_time(evs[j + 1])
+    if dist:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    total_bytes = world * n * sum(BYTES_PER_ELEM.values()) * args.steps
+    value = total_bytes / (elapsed_ms * 1e-3) / 1e9
+    # per-kernel achieved bandwidth (this rank), dominant kernel for the roofline
+    kernel_gbs = {k: n * b * args.steps / (kt[k] * 1e-3) / 1e9 for k, b in BYTES_PER_ELEM.items()}
+    dom = max(kt, key=kt.get)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    result = {
+        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32->e5m2/fp16",
+        "data": "synthetic (seeded, generated in HBM; SURVEY 8d config-2 distribution)",
+        "config": {"workload": "config2: quantize sweep 2^%d FP32 per GPU x {E5M2 RNE, E5M2 SR "
+                               "(reference LFSR stream), FP16 SR (counter bits)}" % args.log2n,
+                   "elements_per_gpu": n, "bytes_per_elem": BYTES_PER_ELEM,
+                   "l2": "no flush: inputs 1 GiB per GPU > 126 MB L2",
+                   "parallelism": f"data-sharded x{world}, no collective"},
+        "kernels_ms_per_step": {k: round(v / args.steps, 4) for k, v in kt.items()},
+        "kernels_gbs": {k: round(v, 1) for k, v in kernel_gbs.items()},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(kernel_gbs[dom], 1),
+                     "peak": hbm_peak, "peak_source": f"{peak_src} HBM copy (MEASURED_PEAKS.json)",
+                     "unit": "GB/s", "frac": round(kernel_gbs[dom] / hbm_peak, 4),
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_launch": n * BYTES_PER_ELEM[dom]},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    # counters sanity (all ranks identical data distribution): overflow fraction
+    o, u, nn = cnt[0].values()
+    result["counters_e5m2_rne_per_step"] = {"overflow": o // (args.steps + args.warmup),
+                                            "underflow": u // (args.steps + args.warmup)}
+    result["e2e"] = e2e_ours(F, args, x, stream)
+    if rank == 0 and not args.no_extras:
+        result["update"] = bench_update(F, args)
+        result["gemm"] = bench_gemm(F, args, bf16_peak)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(x, args)
+    if dist:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+
+
+def e2e_ours(F, args, x_dev, stream):
+    """Same metric through the public API with HOST buffers: pinned H2D of the
+    step's input, the three sweeps, D2H of all codes + counters, every step."""
+    import torch
+    n = 1 << min(args.log2n, args.e2e_log2n)
+    xh = torch.empty(n, dtype=torch.float32).pin_memory()
+    xh.copy_(x_dev[:n])
+    o8a = torch.empty(n, dtype=torch.uint8).pin_memory()
+    o8b = torch.empty(n, dtype=torch.uint8).pin_memory()
+    o16 = torch.empty(n, dtype=torch.int16).pin_memory()
+    oc = torch.empty(9, dtype=torch.int64).pin_memory()
+    xd = torch.empty(n, dtype=torch.float32, device="cuda")
+    c8a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    c8b = torch.empty(n, dtype=torch.uint8, device="cuda")
+    c16 = torch.empty(n, dtype=torch.int16, device="cuda")
+    cnt = F.Counters()
+    cnt3 = torch.zeros(9, dtype=torch.int64, device="cuda")
+
+    def step():
+        xd.copy_(xh, non_blocking=True)
+        cnt3.zero_()
+        q1 = F.quantize(xd, "fp8", "nearest-even", 1, out=c8a)
+        q2 = F.quantize(xd, "fp8", "stochastic", 1, out=c8b)
+        q3 = F.quantize(xd, "fp16", "stochastic", 1, bits="counter", out=c16)
+        cnt3[0:3].copy_(q1.counters.t); cnt3[3:6].copy_(q2.counters.t); cnt3[6:9].copy_(q3.counters.t)
+        o8a.copy_(c8a, non_blocking=True)
+        o8b.copy_(c8b, non_blocking=True)
+        o16.copy_(c16, non_blocking=True)
+        oc.copy_(cnt3, non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 10))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    val = n * sum(BYTES_PER_ELEM.values()) / (ms * 1e-3) / 1e9
+    return {"value": round(val, 2), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
+            "d2h_bytes_per_step": 4 * n + 72, "ms_per_step": round(ms, 3),
+            "elements": n, "note": "pinned host buffers; H2D input + D2H all codes/counters"}
+
+
+def bench_update(F, args):
+    """SGD-momentum update into FP16 masters (E5M2 grads), RNE and LFSR-SR masters."""
+    import torch
+    n = 1 << 28
+    grad = torch.randint(0, 120, (n,), dtype=torch.uint8, device="cuda")
+    master = torch.randint(0, 0x3C00, (n,), dtype=torch.int16, device="cuda")
+    mom = torch.zeros(n, dtype=torch.float32, device="cuda")
+    w8 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, kw, bpe in [("rne_master", dict(master_mode="nearest-even"), 13),
+                          ("sr_lfsr_master", dict(master_mode="stochastic", seed=1), 13),
+                          ("sr_counter_master_w8", dict(master_mode="stochastic", bits="counter",
+                                                        seed=1, w_e5m2=w8), 14)]:
+        for _ in range(3):
+            F.sgd_momentum_update(grad, "fp8", master, mom, lr=1e-4, mu=0.9, scale=8192.0, **kw)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(5):
+            F.sgd_momentum_update(grad, "fp8", master, mom, lr=1e-4, mu=0.9, scale=8192.0, **kw)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 5
+        out[name] = {"ms": round(ms, 4), "gbs": round(n * bpe / (ms * 1e-3) / 1e9, 1),
+                     "bytes_per_param": bpe}
+    out["params"] = n
+    return out
+
+
+def bench_gemm(F, args, bf16_peak):
+    import torch
+    res = {}
+    for (m, n, k) in [(8192, 8192, 8192), (16384, 1024, 16384)]:
+        x = torch.empty(m * k + k * n, dtype=torch.float32, device="cuda")
+        F.fill_synthetic(x, "normal", 3, 1.0)
+        qa = F.quantize(x[: m * k]).codes
+        qb = F.quantize(x[m * k:]).codes
+        c = torch.empty((m, n), dtype=torch.float32, device="cuda")
+        cq = torch.empty(m * n, dtype=torch.uint8, device="cuda")
+        del x
+        for label, kw in [("f32_out", dict(c=c)), ("e5m2_out", dict(want_c=False, out_fmt="fp8",
+                                                                       out_codes=cq))]:
+            for _ in range(2):
+                F.gemm_codes(qa, qb, m, n, k, "fp8", **kw)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            reps = 5
+            a.record()
+            for _ in range(reps):
+                F.gemm_codes(qa, qb, m, n, k, "fp8", **kw)
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / reps
+            tf = 2.0 * m * n * k / (ms * 1e-3) / 1e12
+            res[f"{m}x{n}x{k}_{label}"] = {"ms": round(ms, 3), "tflops": round(tf, 1),
+                                           "frac_fp8_nominal_4500": round(tf / 4500.0, 4)}
+        del qa, qb, c, cq
+        torch.cuda.empty_cache()
+    return res
+
+
+def cpu_baseline(x_dev, args):
+    """The reference's own quantize (oracle/_ref, compiled from /root/reference)
+    on this host's cores, block-parallel (bit-identical to serial), over a bounded
+    sample of the same input."""
+    import oracle as O
+    ns = 1 << args.cpu_log2n
+    xs = x_dev[:ns].cpu().numpy()
+    cores = os.cpu_count() or 1
+    if not O.ref_available():
+        return {"value": None, "unavailable": "oracle/_ref not built"}
+    t0 = time.perf_counter()
+    O.ref_quantize_mt(xs, "fp8", "nearest-even", 1, nthreads=cores)
+    O.ref_quantize_mt(xs, "fp8", "stochastic", 1, nthreads=cores)
+    O.ref_quantize_mt(xs, "fp16", "stochastic", 1, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": round(ns * sum(BYTES_PER_ELEM.values()) / dt / 1e9, 4), "unit": "GB/s",
+            "cores": cores, "kind": "reference",
+            "sample": f"first 2^{args.cpu_log2n} elements of the same input; reference "
+                      "fp8emu encode()+LfsrStream::split block-parallel over 4096-blocks "
+                      "(RNE E5M2, SR E5M2, SR FP16 via the reference LFSR stream)",
+            "seconds": round(dt, 3)}
+
+
+# ------------------------------------------------------------------- reference
+def run_reference(args):
+    world, rank, _ = _dist_init()
+    if rank != 0:
+        return
+    import oracle as O
+    ns = 1 << args.cpu_log2n
+    rng = np.random.default_rng(0)
+    x = (np.exp2(rng.uniform(-24, 17, ns)) * rng.choice([-1.0, 1.0], ns)).astype(np.float32)
+    cores = os.cpu_count() or 1
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+
+    def step():
+        O.ref_quantize_mt(x, "fp8", "nearest-even", 1, nthreads=cores)
+        O.ref_quantize_mt(x, "fp8", "stochastic", 1, nthreads=cores)
+        O.ref_quantize_mt(x, "fp16", "stochastic", 1, nthreads=cores)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = ns * sum(BYTES_PER_ELEM.values()) * args.steps / dt / 1e9
+    sample = (f"2^{args.cpu_log2n} elements per step (bounded sample of the 2^{args.log2n} "
+              "workload); reference encode()+LfsrStream::split, block-parallel over 4096-blocks")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32->e5m2/fp16", "data": "synthetic",
+        "config": {"workload": "config2 (same three sweeps) on host cores",
+                   "elements_per_step": ns},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log2n", type=int, default=28)
+    ap.add_argument("--e2e-log2n", type=int, default=28)
+    ap.add_argument("--cpu-log2n", type=int, default=23)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

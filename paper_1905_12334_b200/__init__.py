@@ -1,0 +1,422 @@
+"""B200-native FP8 (E5M2) training primitives -- the hot path of fp8emu on sm_100a.
+
+This module mirrors the reference's Python surface (``fp8emu``,
+/root/reference/proj/src/python/bindings.cpp:76-238) for the hot path:
+``quantize``, ``dequantize``, ``gemm``, ``transpose``, ``encode``, ``decode``,
+``LossScaler`` and the fused ``sgd_momentum_update``, with the same argument
+names, meanings and error behaviour (``ValueError`` where the reference raises
+``std::invalid_argument``). Every call runs hand-written CUDA kernels from
+``libfp8b200.so`` through its C-ABI (include/fp8b200.h); tensors live in HBM
+as torch CUDA tensors (torch is used for device memory and streams only).
+
+Differences from the reference surface, all deliberate:
+  * codes are 1 byte per E5M2 element (the reference widens to uint16);
+    ``QuantizedTensor.codes_u16()`` returns the reference's layout;
+  * inputs may be numpy arrays (copied to the current CUDA device) or CUDA
+    tensors (used in place, no copy);
+  * extensions: ``bits`` / ``block_offset`` / ``rbits`` for stochastic rounding
+    (reference LFSR stream, counter bits, supplied bits), fused GEMM epilogues,
+    MN-major operands, device-resident loss-scaler state.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import LIB, check
+
+__all__ = [
+    "QuantizedTensor", "ScaleEvent", "LossScaler", "quantize", "dequantize", "transpose",
+    "gemm", "gemm_codes", "encode", "decode", "sgd_momentum_update", "bias_grad",
+    "count_nonfinite", "fill_synthetic", "Counters", "launch_count", "version",
+]
+
+_FMT = {"fp8": _lib.E5M2, "FP8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16,
+        "FP16": _lib.FP16}
+_MODE = {"nearest-even": _lib.RNE, "rne": _lib.RNE, "stochastic": _lib.SR,
+         "truncate": _lib.TRUNC}
+_BITS = {"lfsr": _lib.BITS_LFSR, "counter": _lib.BITS_COUNTER, "supplied": _lib.BITS_SUPPLIED}
+_FMT_NAME = {_lib.E5M2: "FP8", _lib.FP16: "FP16"}
+_MODE_NAME = {_lib.RNE: "nearest-even", _lib.SR: "stochastic", _lib.TRUNC: "truncate"}
+_ACTION = {0: "none", 1: "backoff", 2: "growth", 3: "clamped_to_min"}
+
+
+def _fmt(fmt: str) -> int:
+    try:
+        return _FMT[fmt]
+    except KeyError:
+        raise ValueError(f"unknown float format: {fmt}") from None
+
+
+def _mode(mode: str) -> int:
+    try:
+        return _MODE[mode]
+    except KeyError:
+        raise ValueError(f"unknown rounding mode: {mode}") from None
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _device_f32(x) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        if not x.is_cuda:
+            x = x.to("cuda")
+        if x.dtype != torch.float32:
+            x = x.float()
+        return x.contiguous()
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    return torch.from_numpy(arr).to("cuda")
+
+
+def _code_dtype(fmt: int):
+    return torch.uint8 if fmt == _lib.E5M2 else torch.int16
+
+
+def version() -> str:
+    return LIB.fp8b_version().decode()
+
+
+def launch_count() -> int:
+    """Number of libfp8b200 kernels launched by this process so far."""
+    return int(LIB.fp8b_launch_count())
+
+
+def init() -> None:
+    check(LIB.fp8b_init(), "init")
+
+
+class Counters:
+    """Device int64[3] = {overflow, underflow, nan}; kernels accumulate into it."""
+
+    def __init__(self, device=None):
+        self.t = torch.zeros(3, dtype=torch.int64, device=device or "cuda")
+
+    @property
+    def ptr(self):
+        return self.t.data_ptr()
+
+    def zero_(self):
+        self.t.zero_()
+        return self
+
+    def values(self) -> Tuple[int, int, int]:
+        o, u, n = (int(v) for v in self.t.tolist())
+        return o, u, n
+
+
+class QuantizedTensor:
+    """Mirror of fp8emu::QuantizedTensor (tensor.hpp:37-53) with device codes."""
+
+    def __init__(self, codes: torch.Tensor, shape, fmt: int, mode: int, counters: Counters):
+        self.codes = codes
+        self.shape = list(shape)
+        self.fmt_id = fmt
+        self.mode_id = mode
+        self.counters = counters
+
+    @property
+    def format(self) -> str:
+        return _FMT_NAME[self.fmt_id]
+
+    @property
+    def mode(self) -> str:
+        return _MODE_NAME[self.mode_id]
+
+    @property
+    def overflow_count(self) -> int:
+        return self.counters.values()[0]
+
+    @property
+    def underflow_count(self) -> int:
+        return self.counters.values()[1]
+
+    @property
+    def nan_count(self) -> int:
+        return self.counters.values()[2]
+
+    def numel(self) -> int:
+        return int(np.prod(self.shape)) if self.shape else 1
+
+    def codes_u16(self) -> np.ndarray:
+        """Codes widened to the reference's uint16 storage, on the host."""
+        c = self.codes.cpu().numpy()
+        if self.fmt_id == _lib.FP16:
+            c = c.view(np.uint16)
+        return c.astype(np.uint16).reshape(self.shape)
+
+    def reshaped(self, new_shape) -> "QuantizedTensor":
+        if int(np.prod(new_shape)) != self.numel():
+            raise ValueError("reshape changes element count")
+        return QuantizedTensor(self.codes, new_shape, self.fmt_id, self.mode_id, self.counters)
+
+    def __repr__(self):
+        return f"QuantizedTensor({self.format}, shape={self.shape})"
+
+
+def quantize(array, fmt: str = "fp8", mode: str = "nearest-even", seed: int = 1,
+             saturate: bool = False, *, bits: str = "lfsr", block_offset: int = 0,
+             rbits: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+             counters: Optional[Counters] = None, stream=None) -> QuantizedTensor:
+    """fp8emu.quantize (bindings.cpp:167-176 -> tensor.cpp:46-81) on the GPU."""
+    f, m = _fmt(fmt), _mode(mode)
+    if bits not in _BITS:
+        raise ValueError(f"unknown random-bits source: {bits}")
+    x = _device_f32(array)
+    shape = list(x.shape)
+    n = x.numel()
+    codes = out if out is not None else torch.empty(n, dtype=_code_dtype(f), device=x.device)
+    cnt = counters if counters is not None else Counters(x.device)
+    rb = None
+    if rbits is not None:
+        rb = rbits.reshape(-1).contiguous()
+        if rb.dtype not in (torch.int32, torch.uint32) or rb.numel() != n or not rb.is_cuda:
+            raise ValueError("rbits must be a CUDA int32/uint32 tensor with one word per element")
+    cfg = _lib.QuantConfig(m, _BITS[bits], int(seed) & (2**64 - 1), int(bool(saturate)), 0,
+                           int(block_offset), _ptr(rb))
+    check(LIB.fp8b_quantize(x.data_ptr(), codes.data_ptr(), n, f, cfg, cnt.ptr, _stream(stream)),
+          "quantize")
+    return QuantizedTensor(codes, shape, f, m, cnt)
+
+
+def dequantize(tensor: QuantizedTensor, stream=None) -> torch.Tensor:
+    """fp8emu.dequantize (tensor.cpp:83-98)."""
+    n = tensor.numel()
+    out = torch.empty(n, dtype=torch.float32, device=tensor.codes.device)
+    check(LIB.fp8b_dequantize(tensor.codes.data_ptr(), out.data_ptr(), n, tensor.fmt_id,
+                              _stream(stream)), "dequantize")
+    return out.reshape(tensor.shape)
+
+
+def transpose(tensor: QuantizedTensor, stream=None) -> QuantizedTensor:
+    """fp8emu transpose (tensor.cpp:135-150)."""
+    if len(tensor.shape) != 2:
+        raise ValueError("transpose expects a rank-2 tensor")
+    r, c = tensor.shape
+    out = torch.empty_like(tensor.codes)
+    check(LIB.fp8b_transpose(tensor.codes.data_ptr(), out.data_ptr(), r, c, tensor.fmt_id,
+                             _stream(stream)), "transpose")
+    return QuantizedTensor(out, [c, r], tensor.fmt_id, tensor.mode_id, tensor.counters)
+
+
+def gemm_codes(a_codes: torch.Tensor, b_codes: torch.Tensor, m: int, n: int, k: int,
+               fmt: str = "fp8", *, a_major: str = "k", b_major: str = "n",
+               engine: str = "tensor", c: Optional[torch.Tensor] = None, want_c: bool = True,
+               bias: Optional[torch.Tensor] = None, out_fmt: Optional[str] = None,
+               out_mode: str = "nearest-even", out_seed: int = 1, out_saturate: bool = False,
+               out_codes: Optional[torch.Tensor] = None, out_counters: Optional[Counters] = None,
+               stream=None):
+    """Low-level GEMM over device code buffers (fp8b_gemm).
+
+    a_major: "k" (A stored [M,K]) or "m" (A stored [K,M]);
+    b_major: "n" (B stored [K,N], the reference layout) or "k" (B stored [N,K]).
+    Returns (c, out_codes) -- either may be None.
+    """
+    f = _fmt(fmt)
+    dev = a_codes.device
+    if want_c and c is None:
+        c = torch.empty((m, n), dtype=torch.float32, device=dev)
+    cq = None
+    cqf = 0
+    if out_fmt is not None:
+        cqf = _fmt(out_fmt)
+        cq = out_codes if out_codes is not None else torch.empty(m * n, dtype=_code_dtype(cqf),
+                                                                 device=dev)
+    args = _lib.GemmArgs(
+        _lib.K_MAJOR if a_major == "k" else _lib.MN_MAJOR,
+        _lib.MN_MAJOR if b_major == "n" else _lib.K_MAJOR,
+        _lib.GEMM_TENSOR if engine == "tensor" else _lib.GEMM_SEQUENTIAL, 0,
+        _ptr(c) if want_c else None, _ptr(bias), _ptr(cq), cqf, _mode(out_mode),
+        int(out_seed), int(bool(out_saturate)), 0,
+        out_counters.ptr if out_counters is not None else None)
+    check(LIB.fp8b_gemm(a_codes.data_ptr(), b_codes.data_ptr(), m, n, k, f, args,
+                        _stream(stream)), "gemm_fp8")
+    return (c if want_c else None), cq
+
+
+def gemm(a: QuantizedTensor, b: QuantizedTensor, *, engine: str = "tensor",
+         stream=None) -> torch.Tensor:
+    """fp8emu.gemm (bindings.cpp:183-189 -> kernels.cpp:37-62): FP32 [M, N]."""
+    if len(a.shape) != 2 or len(b.shape) != 2:
+        raise ValueError("gemm_fp8 expects rank-2 operands")
+    if a.shape[1] != b.shape[0]:
+        raise ValueError("gemm_fp8 inner dimensions disagree")
+    if a.fmt_id != b.fmt_id:
+        raise ValueError("kernel operands must share one format")
+    m, k = a.shape
+    n = b.shape[1]
+    c, _ = gemm_codes(a.codes, b.codes, m, n, k, _FMT_NAME[a.fmt_id].lower(), engine=engine,
+                      stream=stream)
+    return c
+
+
+def encode(x: float, fmt: str = "fp8", mode: str = "nearest-even", seed: int = 1,
+           saturate: bool = False):
+    """fp8emu.encode (bindings.cpp:138-152): (code, overflowed, underflowed_to_zero).
+    SR draws from LfsrStream::split(seed, 0), as the binding does."""
+    q = quantize(np.array([x], dtype=np.float32), fmt, mode, seed, saturate)
+    code = int(q.codes_u16()[0])
+    o, u, _ = q.counters.values()
+    return code, bool(o), bool(u)
+
+
+def decode(code: int, fmt: str = "fp8") -> float:
+    """fp8emu.decode for one code (exact in FP32 for both formats)."""
+    f = _fmt(fmt)
+    dt = np.uint8 if f == _lib.E5M2 else np.uint16
+    c = torch.from_numpy(np.array([code], dtype=dt).view(
+        np.uint8 if f == _lib.E5M2 else np.int16)).to("cuda")
+    q = QuantizedTensor(c, [1], f, _lib.RNE, Counters())
+    return float(dequantize(q).cpu()[0])
+
+
+@dataclass
+class ScaleEvent:
+    iteration: int
+    action: str
+    scale_after: float
+
+
+class LossScaler:
+    """fp8emu.LossScaler (loss_scaling.hpp:26-68) with its state in HBM.
+
+    ``step`` launches one device kernel and does not synchronise; the
+    ``scale``/event accessors copy the state back (they synchronise)."""
+
+    def __init__(self, kind: str = "constant", scale: float = 1.0, backoff_factor: float = 0.5,
+                 growth_factor: float = 2.0, growth_interval: int = 2000,
+                 min_threshold_schedule: Sequence[Tuple[int, float]] = (), device=None):
+        if kind == "constant":
+            k = _lib.SCALER_CONSTANT
+        elif kind == "dynamic-backoff":
+            k = _lib.SCALER_DYNAMIC_BACKOFF
+        else:
+            raise ValueError(f"unknown scaler kind: {kind}")
+        sched = list(min_threshold_schedule)
+        if len(sched) > _lib.MAX_SCHEDULE:
+            raise ValueError("min threshold schedule too long")
+        h = _lib.LossScalerState()
+        h.kind, h.n_schedule, h.scale = k, len(sched), float(scale)
+        h.backoff_factor, h.growth_factor = float(backoff_factor), float(growth_factor)
+        h.growth_interval = int(growth_interval)
+        for i, (it, sc) in enumerate(sched):
+            h.sched_iter[i] = int(it)
+            h.sched_scale[i] = float(sc)
+        self._host = h
+        self.kind = kind
+        self.schedule = sched
+        nbytes = C_sizeof(_lib.LossScalerState)
+        self.state = torch.zeros(nbytes, dtype=torch.uint8, device=device or "cuda")
+        check(LIB.fp8b_loss_scaler_init(self.state.data_ptr(), h,
+                                        _stream(None)), "LossScaler")
+
+    @property
+    def ptr(self):
+        return self.state.data_ptr()
+
+    def _read(self) -> _lib.LossScalerState:
+        raw = self.state.cpu().numpy().tobytes()
+        return _lib.LossScalerState.from_buffer_copy(raw)
+
+    @property
+    def scale(self) -> float:
+        return self._read().scale
+
+    @property
+    def steps_since_overflow(self) -> int:
+        return self._read().steps_since_overflow
+
+    def min_threshold(self, iteration: int) -> float:
+        thr = 1.0
+        for it, sc in self.schedule:
+            if it > iteration:
+                break
+            thr = sc
+        return thr
+
+    def step_async(self, grads_finite: bool = True, iteration: int = 0,
+                   counters: Optional[Counters] = None, stream=None) -> None:
+        check(LIB.fp8b_loss_scaler_step(self.ptr, counters.ptr if counters else None,
+                                        int(bool(grads_finite)), int(iteration),
+                                        _stream(stream)), "LossScaler.step")
+
+    def step(self, grads_finite: bool, iteration: int) -> ScaleEvent:
+        self.step_async(grads_finite, iteration)
+        s = self._read()
+        return ScaleEvent(int(s.last_iteration), _ACTION[s.last_action], s.last_scale_after)
+
+    def unscale(self, gradients) -> torch.Tensor:
+        g = _device_f32(gradients).clone()
+        check(LIB.fp8b_unscale(g.data_ptr(), g.numel(), self.ptr, _stream(None)), "unscale")
+        return g
+
+
+def C_sizeof(t) -> int:
+    import ctypes
+    return ctypes.sizeof(t)
+
+
+def sgd_momentum_update(grad: torch.Tensor, grad_fmt: str, master: torch.Tensor,
+                        momentum: torch.Tensor, *, lr: float, mu: float,
+                        two_lambda: float = 0.0, scale: float = 1.0,
+                        scaler: Optional[LossScaler] = None,
+                        skip_counters: Optional[Counters] = None,
+                        master_mode: str = "nearest-even", bits: str = "lfsr", seed: int = 1,
+                        block_offset: int = 0, rbits: Optional[torch.Tensor] = None,
+                        master_counters: Optional[Counters] = None,
+                        w_e5m2: Optional[torch.Tensor] = None, w_saturate: bool = False,
+                        w_counters: Optional[Counters] = None, stream=None) -> None:
+    """update_tensor (nn.cpp:417-432) for one parameter tensor, in place.
+
+    grad: device codes (grad_fmt "fp8"/"fp16") or FP32 values (grad_fmt "f32");
+    master: FP16 codes (int16 tensor); momentum: FP32."""
+    gf = {"fp8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16, "f32": _lib.F32}.get(grad_fmt)
+    if gf is None:
+        raise ValueError(f"unknown gradient format: {grad_fmt}")
+    n = master.numel()
+    if momentum.numel() != n or grad.numel() != n:
+        raise ValueError("update operands disagree in size")
+    args = _lib.SgdArgs(float(lr), float(mu), float(two_lambda), float(scale),
+                        scaler.ptr if scaler is not None else None,
+                        skip_counters.ptr if skip_counters is not None else None,
+                        _mode(master_mode), _BITS[bits], int(seed), int(block_offset),
+                        _ptr(rbits), master_counters.ptr if master_counters else None,
+                        _ptr(w_e5m2), int(bool(w_saturate)), 0,
+                        w_counters.ptr if w_counters else None)
+    check(LIB.fp8b_sgd_momentum_update(grad.data_ptr(), gf, master.data_ptr(),
+                                       momentum.data_ptr(), n, args, _stream(stream)),
+          "sgd_momentum_update")
+
+
+def bias_grad(e: QuantizedTensor, stream=None) -> torch.Tensor:
+    """db[j] = sum_r dequant(qe)[r, j] in row order (nn.cpp:308-314)."""
+    rows, cols = e.shape
+    db = torch.empty(cols, dtype=torch.float32, device=e.codes.device)
+    check(LIB.fp8b_bias_grad(e.codes.data_ptr(), e.fmt_id, rows, cols, db.data_ptr(),
+                             _stream(stream)), "bias_grad")
+    return db
+
+
+def count_nonfinite(x: torch.Tensor, counters: Counters, stream=None) -> None:
+    check(LIB.fp8b_count_nonfinite(x.data_ptr(), x.numel(), counters.ptr, _stream(stream)),
+          "count_nonfinite")
+
+
+def fill_synthetic(out: torch.Tensor, kind: str, seed: int, p: float = 0.01, lo: float = -24.0,
+                   hi: float = 17.0, stream=None) -> torch.Tensor:
+    """Seeded synthetic data in HBM: kind "config2" (log-uniform + ties),
+    "normal" (N(0, p^2)) or "halfnormal" (|N(0, p^2)|)."""
+    k = {"config2": 0, "normal": 1, "halfnormal": 2}[kind]
+    check(LIB.fp8b_fill_synthetic(out.data_ptr(), out.numel(), k, int(seed), float(p),
+                                  float(lo), float(hi), _stream(stream)), "fill_synthetic")
+    return out

@@ -1,0 +1,104 @@
+"""ctypes binding of libfp8b200.so (the C-ABI declared in include/fp8b200.h).
+
+The library is built in-tree (``make -C paper_1905_12334_b200``, or
+``__graft_entry__.build()``). There is no Python or CPU fallback: if the shared
+object is missing, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfp8b200.so")
+
+OK, EINVAL, ENOTSUP, ECUDA = 0, 22, 95, 1000
+E5M2, FP16, F32 = 0, 1, 2
+RNE, SR, TRUNC = 0, 1, 2
+BITS_LFSR, BITS_COUNTER, BITS_SUPPLIED = 0, 1, 2
+K_MAJOR, MN_MAJOR = 0, 1
+GEMM_TENSOR, GEMM_SEQUENTIAL = 0, 1
+SCALER_CONSTANT, SCALER_DYNAMIC_BACKOFF = 0, 1
+MAX_SCHEDULE = 16
+
+_vp = C.c_void_p
+_i32, _i64, _u64 = C.c_int32, C.c_int64, C.c_uint64
+
+
+class QuantConfig(C.Structure):
+    _fields_ = [("mode", _i32), ("bits", _i32), ("seed", _u64), ("saturate", _i32),
+                ("reserved", _i32), ("block_offset", _i64), ("rbits", _vp)]
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [("a_major", _i32), ("b_major", _i32), ("engine", _i32), ("reserved0", _i32),
+                ("c", _vp), ("bias", _vp), ("cq", _vp), ("cq_fmt", _i32), ("cq_mode", _i32),
+                ("cq_seed", _u64), ("cq_saturate", _i32), ("reserved1", _i32),
+                ("cq_counters", _vp)]
+
+
+class LossScalerState(C.Structure):
+    _fields_ = [("kind", _i32), ("n_schedule", _i32), ("scale", C.c_double),
+                ("backoff_factor", C.c_double), ("growth_factor", C.c_double),
+                ("growth_interval", _i64), ("steps_since_overflow", _i64),
+                ("sched_iter", _i64 * MAX_SCHEDULE), ("sched_scale", C.c_double * MAX_SCHEDULE),
+                ("last_iteration", _i64), ("last_action", _i32), ("last_grads_finite", _i32),
+                ("last_scale_after", C.c_double)]
+
+
+class SgdArgs(C.Structure):
+    _fields_ = [("lr", C.c_float), ("mu", C.c_float), ("two_lambda", C.c_float),
+                ("scale", C.c_float), ("scaler", _vp), ("skip_counters", _vp),
+                ("master_mode", _i32), ("bits", _i32), ("seed", _u64), ("block_offset", _i64),
+                ("rbits", _vp), ("master_counters", _vp), ("w_e5m2", _vp),
+                ("w_saturate", _i32), ("reserved", _i32), ("w_counters", _vp)]
+
+
+# every symbol include/fp8b200.h declares, with its ctypes signature
+SIGNATURES = {
+    "fp8b_quantize": (C.c_int, [_vp, _vp, _i64, _i32, C.POINTER(QuantConfig), _vp, _vp]),
+    "fp8b_dequantize": (C.c_int, [_vp, _vp, _i64, _i32, _vp]),
+    "fp8b_transpose": (C.c_int, [_vp, _vp, _i64, _i64, _i32, _vp]),
+    "fp8b_count_nonfinite": (C.c_int, [_vp, _i64, _vp, _vp]),
+    "fp8b_gemm": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, C.POINTER(GemmArgs), _vp]),
+    "fp8b_loss_scaler_init": (C.c_int, [_vp, C.POINTER(LossScalerState), _vp]),
+    "fp8b_loss_scaler_step": (C.c_int, [_vp, _vp, _i32, _i64, _vp]),
+    "fp8b_unscale": (C.c_int, [_vp, _i64, _vp, _vp]),
+    "fp8b_sgd_momentum_update": (C.c_int, [_vp, _i32, _vp, _vp, _i64, C.POINTER(SgdArgs), _vp]),
+    "fp8b_bias_grad": (C.c_int, [_vp, _i32, _i64, _i64, _vp, _vp]),
+    "fp8b_init": (C.c_int, []),
+    "fp8b_last_error": (C.c_char_p, []),
+    "fp8b_version": (C.c_char_p, []),
+    "fp8b_launch_count": (C.c_int64, []),
+    "fp8b_fill_synthetic": (C.c_int, [_vp, _i64, _i32, _u64, C.c_double, C.c_double,
+                                      C.c_double, _vp]),
+}
+
+
+def load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `make -C {HERE}` "
+            "(the CUDA extension is required; there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = load()
+
+
+class Fp8bError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == OK:
+        return
+    msg = LIB.fp8b_last_error().decode(errors="replace")
+    if rc == EINVAL:
+        raise ValueError(f"{what}: {msg}" if what else msg)
+    raise Fp8bError(f"{what}: [{rc}] {msg}" if what else f"[{rc}] {msg}")

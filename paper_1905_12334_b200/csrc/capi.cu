@@ -1,0 +1,292 @@
+// capi.cu -- extern "C" entry points of libfp8b200.so (declared in include/fp8b200.h).
+//
+// Validation mirrors where the reference throws std::invalid_argument; every
+// accepted call is a stream-ordered launch of the kernels in this directory.
+// There is no CPU compute path: a missing or failing GPU is reported as
+// FP8B_ECUDA.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const char* msg) {
+    g_err = msg;
+    return code;
+}
+
+int check_launch(int nkernels) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_err = std::string("CUDA error: ") + cudaGetErrorString(e);
+        return FP8B_ECUDA;
+    }
+    g_launches += nkernels;
+    return FP8B_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- decimated LFSR tables, one copy per device (init once) -------------
+constexpr int kMaxDev = 64;
+std::mutex g_tab_mu;
+fp8b::LfsrTables g_tabs[kMaxDev];
+bool g_tab_ok[kMaxDev];
+
+uint16_t bitrev16(uint16_t v) {
+    uint16_t r = 0;
+    for (int i = 0; i < 16; ++i) r = (uint16_t)(r | (((v >> i) & 1u) << (15 - i)));
+    return r;
+}
+
+int get_tables(fp8b::LfsrTables* out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev)
+        return fail(FP8B_ECUDA, "no CUDA device");
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    if (!g_tab_ok[dev]) {
+        // D = 16 clocks of the (16,15,13,4) Fibonacci LFSR (lfsr.cpp:17-27);
+        // D is a single 65535-cycle since gcd(16, 65535) = 1.
+        std::vector<uint16_t> tabx(fp8b::kLfsrPeriod + fp8b::kBlock), pos(65536, 0);
+        uint16_t s = 1;
+        for (int k = 0; k < fp8b::kLfsrPeriod; ++k) {
+            tabx[k] = bitrev16(s);
+            pos[s] = (uint16_t)k;
+            for (int c = 0; c < 16; ++c) {
+                const uint16_t bit = (uint16_t)(((s >> 0) ^ (s >> 1) ^ (s >> 3) ^ (s >> 12)) & 1u);
+                s = (uint16_t)((s >> 1) | (bit << 15));
+            }
+        }
+        for (int k = 0; k < fp8b::kBlock; ++k) tabx[fp8b::kLfsrPeriod + k] = tabx[k];
+        uint16_t *dt = nullptr, *dp = nullptr;
+        if (cudaMalloc(&dt, tabx.size() * 2) != cudaSuccess ||
+            cudaMalloc(&dp, pos.size() * 2) != cudaSuccess ||
+            cudaMemcpy(dt, tabx.data(), tabx.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(dp, pos.data(), pos.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(FP8B_ECUDA, "failed to upload LFSR tables");
+        }
+        g_tabs[dev].tabx = dt;
+        g_tabs[dev].pos = dp;
+        g_tab_ok[dev] = true;
+    }
+    *out = g_tabs[dev];
+    return FP8B_OK;
+}
+
+bool valid_fmt(int32_t f) { return f == FP8B_E5M2 || f == FP8B_FP16; }
+bool valid_mode(int32_t m) { return m == FP8B_RNE || m == FP8B_SR || m == FP8B_TRUNC; }
+bool valid_bits(int32_t b) { return b == FP8B_BITS_LFSR || b == FP8B_BITS_COUNTER || b == FP8B_BITS_SUPPLIED; }
+
+}  // namespace
+
+extern "C" {
+
+const char* fp8b_last_error(void) { return g_err.c_str(); }
+const char* fp8b_version(void) { return "fp8b200 0.1 sm_100a (tcgen05/TMA)"; }
+int64_t fp8b_launch_count(void) { return g_launches.load(); }
+
+int fp8b_init(void) {
+    fp8b::LfsrTables t;
+    return get_tables(&t);
+}
+
+int fp8b_quantize(const float* x, void* codes, int64_t n, int32_t fmt,
+                  const fp8b_quant_config_t* cfg, int64_t* counters, void* stream) {
+    if (!cfg) return fail(FP8B_EINVAL, "quantize: null config");
+    if (cfg->seed == 0) return fail(FP8B_EINVAL, "QuantConfig.seed must be nonzero");
+    if (n < 0) return fail(FP8B_EINVAL, "negative dimension");
+    if (!valid_fmt(fmt)) return fail(FP8B_EINVAL, "quantize: unknown float format");
+    if (!valid_mode(cfg->mode)) return fail(FP8B_EINVAL, "unknown rounding mode");
+    if (cfg->mode == FP8B_SR && !valid_bits(cfg->bits))
+        return fail(FP8B_EINVAL, "quantize: unknown random-bits source");
+    if (cfg->mode == FP8B_SR && cfg->bits == FP8B_BITS_SUPPLIED && !cfg->rbits)
+        return fail(FP8B_EINVAL, "quantize: supplied-bits SR needs rbits");
+    if (cfg->block_offset < 0) return fail(FP8B_EINVAL, "quantize: negative block_offset");
+    if (n == 0) return FP8B_OK;
+    if (!x || !codes) return fail(FP8B_EINVAL, "quantize: null tensor");
+    fp8b::LfsrTables tabs{nullptr, nullptr};
+    if (cfg->mode == FP8B_SR && cfg->bits == FP8B_BITS_LFSR) {
+        const int rc = get_tables(&tabs);
+        if (rc) return rc;
+    }
+    fp8b::launch_quantize(x, codes, n, fmt, *cfg, counters, S(stream), tabs);
+    return check_launch(1);
+}
+
+int fp8b_dequantize(const void* codes, float* out, int64_t n, int32_t fmt, void* stream) {
+    if (n < 0) return fail(FP8B_EINVAL, "negative dimension");
+    if (!valid_fmt(fmt)) return fail(FP8B_EINVAL, "dequantize: unknown float format");
+    if (n == 0) return FP8B_OK;
+    if (!codes || !out) return fail(FP8B_EINVAL, "dequantize: null tensor");
+    if ((uintptr_t)codes % (fmt == FP8B_E5M2 ? 4 : 8) || (uintptr_t)out % 16)
+        return fail(FP8B_EINVAL, "dequantize: codes must be 4/8-byte and out 16-byte aligned");
+    fp8b::launch_dequantize(codes, out, n, fmt, S(stream));
+    return check_launch(1);
+}
+
+int fp8b_transpose(const void* in, void* out, int64_t rows, int64_t cols, int32_t fmt,
+                   void* stream) {
+    if (rows < 0 || cols < 0) return fail(FP8B_EINVAL, "negative dimension");
+    if (!valid_fmt(fmt)) return fail(FP8B_EINVAL, "transpose: unknown float format");
+    if (rows == 0 || cols == 0) return FP8B_OK;
+    if (!in || !out) return fail(FP8B_EINVAL, "transpose: null tensor");
+    fp8b::launch_transpose(in, out, rows, cols, fmt, S(stream));
+    return check_launch(1);
+}
+
+int fp8b_count_nonfinite(const float* x, int64_t n, int64_t* counters, void* stream) {
+    if (n < 0) return fail(FP8B_EINVAL, "negative dimension");
+    if (n == 0) return FP8B_OK;
+    if (!x || !counters) return fail(FP8B_EINVAL, "count_nonfinite: null pointer");
+    fp8b::launch_count_nonfinite(x, n, counters, S(stream));
+    return check_launch(1);
+}
+
+int fp8b_bias_grad(const void* e_codes, int32_t fmt, int64_t rows, int64_t cols, float* db,
+                   void* stream) {
+    if (rows < 0 || cols < 0) return fail(FP8B_EINVAL, "negative dimension");
+    if (!valid_fmt(fmt)) return fail(FP8B_EINVAL, "bias_grad: unknown float format");
+    if (cols == 0) return FP8B_OK;
+    if (!db || (rows > 0 && !e_codes)) return fail(FP8B_EINVAL, "bias_grad: null tensor");
+    fp8b::launch_bias_grad(e_codes, fmt, rows, cols, db, S(stream));
+    return check_launch(1);
+}
+
+int fp8b_gemm(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int32_t fmt,
+              const fp8b_gemm_args_t* args, void* stream) {
+    if (!args) return fail(FP8B_EINVAL, "gemm: null args");
+    if (m < 0 || n < 0 || k < 0) return fail(FP8B_EINVAL, "gemm_fp8 expects rank-2 operands");
+    if (!valid_fmt(fmt)) return fail(FP8B_EINVAL, "kernel operands must share one format");
+    if (args->a_major != FP8B_K_MAJOR && args->a_major != FP8B_MN_MAJOR)
+        return fail(FP8B_EINVAL, "gemm: bad a_major");
+    if (args->b_major != FP8B_K_MAJOR && args->b_major != FP8B_MN_MAJOR)
+        return fail(FP8B_EINVAL, "gemm: bad b_major");
+    if (args->engine != FP8B_GEMM_TENSOR && args->engine != FP8B_GEMM_SEQUENTIAL)
+        return fail(FP8B_EINVAL, "gemm: bad engine");
+    if (!args->c && !args->cq) return fail(FP8B_EINVAL, "gemm: no output requested");
+    if (args->cq) {
+        if (!valid_fmt(args->cq_fmt)) return fail(FP8B_EINVAL, "gemm: bad cq_fmt");
+        if (!valid_mode(args->cq_mode)) return fail(FP8B_EINVAL, "gemm: bad cq_mode");
+        if (args->cq_mode == FP8B_SR && args->cq_seed == 0)
+            return fail(FP8B_EINVAL, "QuantConfig.seed must be nonzero");
+    }
+    if (m == 0 || n == 0) return FP8B_OK;
+    if (k > 0 && (!a || !b)) return fail(FP8B_EINVAL, "gemm: null operand");
+    fp8b::EpiArgs ep{args->c, args->bias, args->cq, args->cq_fmt, args->cq_mode, args->cq_seed,
+                     args->cq_saturate, args->cq_counters};
+    const int a_mn = args->a_major == FP8B_MN_MAJOR, b_mn = args->b_major == FP8B_MN_MAJOR;
+    if (args->engine == FP8B_GEMM_TENSOR) {
+        int nl = 0;
+        const int rc = fp8b::launch_gemm_tc(a, b, m, n, k, fmt, a_mn, b_mn, ep, S(stream), &nl);
+        if (rc == FP8B_OK) return check_launch(nl);
+        if (rc != FP8B_ENOTSUP) return rc;
+        // Shapes whose row strides TMA cannot address (not a multiple of 16
+        // bytes) run on the CUDA-core engine -- still on the GPU.
+    }
+    fp8b::launch_gemm_seq(a, b, m, n, k, fmt, a_mn, b_mn, ep, S(stream));
+    return check_launch(1);
+}
+
+int fp8b_loss_scaler_init(fp8b_loss_scaler_t* dev_state, const fp8b_loss_scaler_t* o,
+                          void* stream) {
+    if (!dev_state || !o) return fail(FP8B_EINVAL, "loss_scaler_init: null pointer");
+    // loss_scaling.cpp:19-38
+    if (!(o->scale > 0.0) || !(o->scale < INFINITY))
+        return fail(FP8B_EINVAL, "loss scale must be finite and positive");
+    if (o->kind != FP8B_SCALER_CONSTANT && o->kind != FP8B_SCALER_DYNAMIC_BACKOFF)
+        return fail(FP8B_EINVAL, "unknown scaler kind");
+    if (o->n_schedule < 0 || o->n_schedule > FP8B_MAX_SCHEDULE)
+        return fail(FP8B_EINVAL, "min threshold schedule too long");
+    if (o->kind == FP8B_SCALER_DYNAMIC_BACKOFF) {
+        if (!(o->backoff_factor > 0.0) || !(o->backoff_factor < 1.0))
+            return fail(FP8B_EINVAL, "backoff factor must lie in (0, 1)");
+        if (!(o->growth_factor > 1.0)) return fail(FP8B_EINVAL, "growth factor must exceed 1");
+        if (o->growth_interval <= 0) return fail(FP8B_EINVAL, "growth interval must be positive");
+        int64_t prev = -1;
+        for (int i = 0; i < o->n_schedule; ++i) {
+            if (o->sched_iter[i] <= prev)
+                return fail(FP8B_EINVAL, "min threshold schedule iterations must increase");
+            if (!(o->sched_scale[i] > 0.0)) return fail(FP8B_EINVAL, "min threshold must be positive");
+            prev = o->sched_iter[i];
+        }
+    }
+    static thread_local fp8b_loss_scaler_t h;
+    h = *o;
+    h.steps_since_overflow = 0;
+    h.last_iteration = -1;
+    h.last_action = FP8B_ACT_NONE;
+    h.last_grads_finite = 1;
+    h.last_scale_after = o->scale;
+    if (cudaMemcpyAsync(dev_state, &h, sizeof(h), cudaMemcpyHostToDevice, S(stream)) != cudaSuccess ||
+        cudaStreamSynchronize(S(stream)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FP8B_ECUDA, "loss_scaler_init: copy failed");
+    }
+    return FP8B_OK;
+}
+
+int fp8b_loss_scaler_step(fp8b_loss_scaler_t* dev_state, const int64_t* counters,
+                          int32_t grads_finite, int64_t iteration, void* stream) {
+    if (!dev_state) return fail(FP8B_EINVAL, "loss_scaler_step: null state");
+    fp8b::launch_scaler_step(dev_state, counters, grads_finite, iteration, S(stream));
+    return check_launch(1);
+}
+
+int fp8b_unscale(float* g, int64_t n, const fp8b_loss_scaler_t* dev_state, void* stream) {
+    if (n < 0) return fail(FP8B_EINVAL, "negative dimension");
+    if (!dev_state) return fail(FP8B_EINVAL, "unscale: null state");
+    if (n == 0) return FP8B_OK;
+    if (!g) return fail(FP8B_EINVAL, "unscale: null tensor");
+    fp8b::launch_unscale(g, n, dev_state, S(stream));
+    return check_launch(1);
+}
+
+int fp8b_sgd_momentum_update(const void* grad, int32_t grad_fmt, uint16_t* master,
+                             float* momentum, int64_t n, const fp8b_sgd_args_t* args,
+                             void* stream) {
+    if (!args) return fail(FP8B_EINVAL, "sgd: null args");
+    if (n < 0) return fail(FP8B_EINVAL, "negative dimension");
+    if (grad_fmt != FP8B_E5M2 && grad_fmt != FP8B_FP16 && grad_fmt != FP8B_F32)
+        return fail(FP8B_EINVAL, "sgd: unknown gradient format");
+    if (args->master_mode != FP8B_RNE && args->master_mode != FP8B_SR)
+        return fail(FP8B_EINVAL, "sgd: master rounding must be nearest-even or stochastic");
+    if (args->master_mode == FP8B_SR) {
+        if (!valid_bits(args->bits)) return fail(FP8B_EINVAL, "sgd: unknown random-bits source");
+        if (args->seed == 0) return fail(FP8B_EINVAL, "QuantConfig.seed must be nonzero");
+        if (args->bits == FP8B_BITS_SUPPLIED && !args->rbits)
+            return fail(FP8B_EINVAL, "sgd: supplied-bits SR needs rbits");
+        if (args->block_offset < 0) return fail(FP8B_EINVAL, "sgd: negative block_offset");
+    }
+    if (!args->scaler && !(args->scale > 0.0f))
+        return fail(FP8B_EINVAL, "loss scale must be finite and positive");
+    if (n == 0) return FP8B_OK;
+    if (!grad || !master || !momentum) return fail(FP8B_EINVAL, "sgd: null tensor");
+    fp8b::LfsrTables tabs{nullptr, nullptr};
+    if (args->master_mode == FP8B_SR && args->bits == FP8B_BITS_LFSR) {
+        const int rc = get_tables(&tabs);
+        if (rc) return rc;
+    }
+    fp8b::launch_sgd(grad, grad_fmt, master, momentum, n, *args, S(stream), tabs);
+    return check_launch(1);
+}
+
+int fp8b_fill_synthetic(float* out, int64_t n, int32_t kind, uint64_t seed, double p, double lo,
+                        double hi, void* stream) {
+    if (n < 0 || kind < 0 || kind > 2) return fail(FP8B_EINVAL, "fill_synthetic: bad arguments");
+    if (n == 0) return FP8B_OK;
+    if (!out) return fail(FP8B_EINVAL, "fill_synthetic: null tensor");
+    fp8b::launch_fill_synthetic(out, n, kind, seed, p, lo, hi, S(stream));
+    return check_launch(1);
+}
+
+}  // extern "C"

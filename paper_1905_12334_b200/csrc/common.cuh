@@ -1,0 +1,259 @@
+// common.cuh -- device-side building blocks shared by the fp8b200 kernels.
+//
+// The E5M2 / FP16 encoder here is the integer restatement of the reference's
+// encode() (float_format.cpp:97-135) on FP32 bits (SURVEY 8a A2'); it is
+// exhaustively equal to the reference for RNE and truncation over all 2^32
+// inputs (checked on the B200 by tests/test_quantize_gpu.py::test_exhaustive).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fp8b200.h"
+
+namespace fp8b {
+
+constexpr int kBlock = 4096;  // kQuantBlock (tensor.hpp:65)
+constexpr int kLfsrPeriod = 65535;
+
+// Per-format constants (float_format.hpp:30-78). MB = mantissa bits.
+template <int MB>
+struct Fmt {
+    static constexpr uint32_t maxbits = MB == 2 ? 0x47600000u : 0x477FE000u;  // 57344 / 65504
+    static constexpr uint32_t maxcode = (30u << MB) | ((1u << MB) - 1u);
+    static constexpr uint32_t infcode = 31u << MB;
+    static constexpr uint32_t nancode = infcode | (1u << (MB - 1));
+    static constexpr uint32_t signbit = 1u << (5 + MB);
+    // RNE underflow band: 0 < |x| <= half the min subnormal (ties go to even 0)
+    static constexpr uint32_t rne_unf_max = MB == 2 ? 0x37000000u : 0x33000000u;  // 2^-17 / 2^-25
+    // trunc underflow band: 0 < |x| < min subnormal
+    static constexpr uint32_t trunc_unf_lim = MB == 2 ? 0x37800000u : 0x33800000u;  // 2^-16 / 2^-24
+};
+
+// Result of splitting |x| into the truncated code and the discarded bits.
+struct Split {
+    uint32_t code;   // sign | truncated magnitude code, or the final special code
+    uint32_t r16;    // top 16 discarded bits (SR) ; for RNE: round-up decision in bit 0
+    bool inexact;    // a sample is consumed (finite, nonzero, not representable)
+};
+
+// Classify one FP32 value for a target with MB mantissa bits.
+// Specials (NaN, overflow, zero, exact) come back with inexact=false and the
+// final code. Overflow/NaN flags are derived by the caller from the bits.
+template <int MB>
+__device__ __forceinline__ Split split_bits(uint32_t u, bool saturate) {
+    using F = Fmt<MB>;
+    const uint32_t a = u & 0x7FFFFFFFu;
+    const uint32_t sign = (u >> 31) ? F::signbit : 0u;
+    const uint32_t e = a >> 23;
+    const uint32_t m = a & 0x7FFFFFu;
+    const uint32_t sig = e ? (m | 0x800000u) : m;
+    const uint32_t emax1 = e > 1u ? e : 1u;
+    // dbits = 23-MB for normal targets (e >= 113), 136-MB-max(e,1) below.
+    const uint32_t dbits = (23u - MB) + (emax1 < 113u ? 113u - emax1 : 0u);
+    const uint32_t sh = dbits < 31u ? dbits : 31u;
+    const uint32_t ebase = e > 113u ? ((e - 113u) << MB) : 0u;
+    const uint32_t mag0 = ebase + (sig >> sh);
+    const uint32_t d = sig & ((1u << sh) - 1u);
+    // top 16 discarded bits: (d << 16) >> dbits, 64-bit to cover dbits < 16
+    const uint32_t dsh = dbits < 63u ? dbits : 63u;
+    const uint32_t r16 = (uint32_t)(((uint64_t)d << 16) >> dsh);
+    Split s;
+    s.code = sign | mag0;
+    s.r16 = r16;
+    s.inexact = d != 0u;
+    if (a > F::maxbits) {  // includes Inf and NaN
+        s.inexact = false;
+        s.code = (a > 0x7F800000u) ? F::nancode : (sign | (saturate ? F::maxcode : F::infcode));
+    }
+    // a == 0 -> mag0 == 0, d == 0: code = sign, exact. Nothing to do.
+    return s;
+}
+
+// RNE round-up decision from the discarded bits (SURVEY A2' step 7).
+template <int MB>
+__device__ __forceinline__ uint32_t rne_up(uint32_t u) {
+    const uint32_t a = u & 0x7FFFFFFFu;
+    const uint32_t e = a >> 23;
+    const uint32_t m = a & 0x7FFFFFu;
+    const uint32_t sig = e ? (m | 0x800000u) : m;
+    const uint32_t emax1 = e > 1u ? e : 1u;
+    const uint32_t dbits = (23u - MB) + (emax1 < 113u ? 113u - emax1 : 0u);
+    if (dbits > 24u) return 0u;
+    const uint32_t d = sig & ((1u << dbits) - 1u);
+    const uint32_t half = 1u << (dbits - 1u);
+    const uint32_t lsb = (sig >> dbits) & 1u;
+    return (d > half || (d == half && lsb)) ? 1u : 0u;
+}
+
+// Full integer encode for RNE / TRUNC / SR(with r16). Returns the code and
+// sets the reference's flags (float_format.hpp:82-86) plus NaN.
+template <int MB>
+__device__ __forceinline__ uint32_t encode_int(uint32_t u, int mode, uint32_t r16,
+                                               bool saturate, int& ovf, int& unf, int& nan) {
+    using F = Fmt<MB>;
+    const uint32_t a = u & 0x7FFFFFFFu;
+    nan = a > 0x7F800000u;
+    ovf = (a > F::maxbits) && !nan;
+    Split s = split_bits<MB>(u, saturate);
+    uint32_t up = 0;
+    if (s.inexact) {
+        if (mode == FP8B_RNE) up = rne_up<MB>(u);
+        else if (mode == FP8B_SR) up = (s.r16 + r16) >= 65536u;
+    }
+    const uint32_t code = s.code + up;
+    unf = (a != 0u) && !nan && !ovf && ((code & (F::signbit - 1u)) == 0u);
+    return code;
+}
+
+// Hardware RNE path: cvt.rn.satfinite.e5m2x2.f32 + the two reference fixups
+// (SURVEY 0.2): |x| > 57344 overflows to Inf (or max code) and NaN -> 0x7E.
+__device__ __forceinline__ uint32_t cvt_e5m2x2(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t cvt_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// Fix up one hardware E5M2 RNE code and update counters.
+template <int MB>
+__device__ __forceinline__ uint32_t fix_rne(uint32_t hw, uint32_t u, bool saturate,
+                                            uint32_t& c_big, uint32_t& c_nan, uint32_t& c_unf) {
+    using F = Fmt<MB>;
+    const uint32_t a = u & 0x7FFFFFFFu;
+    const bool big = a > F::maxbits;
+    const bool isnan = a > 0x7F800000u;
+    c_big += big;
+    c_nan += isnan;
+    c_unf += (a - 1u) < F::rne_unf_max;
+    const uint32_t sign = (u >> 31) ? F::signbit : 0u;
+    const uint32_t ovcode = sign | (saturate ? F::maxcode : F::infcode);
+    return big ? (isnan ? F::nancode : ovcode) : hw;
+}
+
+// E5M2 / FP16 code -> FP32 (exact). E5M2 is the top byte of an FP16.
+__device__ __forceinline__ float dec_e5m2(uint32_t c) {
+    return __half2float(__ushort_as_half((unsigned short)((c & 0xFFu) << 8)));
+}
+__device__ __forceinline__ float dec_f16(uint32_t c) {
+    return __half2float(__ushort_as_half((unsigned short)(c & 0xFFFFu)));
+}
+template <int MB>
+__device__ __forceinline__ float dec_code(uint32_t c) {
+    return MB == 2 ? dec_e5m2(c) : dec_f16(c);
+}
+
+// SplitMix64 (lfsr.cpp:47-52).
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t mix64_hd(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// LfsrStream::split(seed, idx).state() (lfsr.cpp:34-45).
+__device__ __forceinline__ uint32_t lfsr_split(uint64_t seed, uint64_t idx) {
+    uint64_t h = mix64(seed + 0x9E3779B97F4A7C15ull * (idx + 1));
+    uint32_t s = (uint32_t)(h & 0xFFFFu);
+    while (s == 0u) {
+        h = mix64(h + 1);
+        s = (uint32_t)(h & 0xFFFFu);
+    }
+    return s;
+}
+
+// Decimated-cycle tables: tabx[k] = bitrev16(D^k(1)) for
+// k in [0, 65535 + 4096) (wrapping), pos[s] = k with D^k(1) == s, D = 16 clocks.
+// Sample j of a block stream starting at state s0 is tabx[pos[s0] + j].
+struct LfsrTables {
+    const uint16_t* tabx;
+    const uint16_t* pos;
+};
+
+// Counter-bits sample (see FP8B_BITS_COUNTER).
+__device__ __forceinline__ uint32_t counter_r16(uint64_t seed, uint64_t gi) {
+    return (uint32_t)(mix64(seed + gi + 1ull) >> 48);
+}
+
+// Block-wide sum of three counters; one atomic per CTA.
+template <int NT>
+__device__ __forceinline__ void flush_counters(uint32_t c0, uint32_t c1, uint32_t c2,
+                                               int64_t* counters) {
+    __shared__ unsigned long long red[3][NT / 32];
+    unsigned long long v0 = c0, v1 = c1, v2 = c2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();  // a previous flush in the same kernel may still be reading red
+    if (l == 0) { red[0][w] = v0; red[1][w] = v1; red[2][w] = v2; }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        unsigned long long s = 0;
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) s += red[threadIdx.x][i];
+        if (s) atomicAdd(reinterpret_cast<unsigned long long*>(counters) + threadIdx.x, s);
+    }
+}
+
+// CTA-wide exclusive scan of inexact flags over a 4096-element block walked as
+// (round r in 0..3, thread t in 0..255, k in 0..3) -- the LFSR consumption order.
+template <int MB>
+struct BlockScan {
+    static constexpr int NT = 256;
+    // Exclusive prefix (in block order) of the inexact flags of this thread's
+    // 16 elements, given per-round 4-bit masks. Returns the prefix of the
+    // thread's first element of each round in pre[r].
+    __device__ __forceinline__ static void run(const uint32_t mask[4], uint32_t pre[4],
+                                               uint32_t* smem_w /*[8]*/) {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        // pack the 4 per-round counts (<= 4 each, warp sum <= 128) into bytes
+        uint32_t packed = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) packed |= (uint32_t)__popc(mask[r]) << (8 * r);
+        uint32_t inc = packed;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) smem_w[w] = inc;
+        __syncthreads();
+        const uint32_t excl = inc - packed;
+        // warp offsets per round and round totals
+        uint32_t before[4] = {0, 0, 0, 0}, total[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t t = smem_w[i];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t c = (t >> (8 * r)) & 0xFFu;
+                total[r] += c;
+                if (i < w) before[r] += c;
+            }
+        }
+        uint32_t run_total = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            pre[r] = run_total + before[r] + ((excl >> (8 * r)) & 0xFFu);
+            run_total += total[r];
+        }
+    }
+};
+
+}  // namespace fp8b

@@ -1,0 +1,48 @@
+// kernels.cuh -- launcher declarations shared between the kernel files and the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fp8b200.h"
+
+namespace fp8b {
+
+struct LfsrTables;
+
+// Fused GEMM epilogue: bias add, FP32 store, output Q node.
+struct EpiArgs {
+    float* c;
+    const float* bias;
+    void* cq;
+    int cq_fmt;
+    int cq_mode;
+    uint64_t cq_seed;
+    int cq_sat;
+    int64_t* cq_counters;
+};
+
+void launch_quantize(const float* x, void* codes, int64_t n, int fmt,
+                     const fp8b_quant_config_t& cfg, int64_t* counters, cudaStream_t st,
+                     const LfsrTables& tabs);
+void launch_dequantize(const void* codes, float* out, int64_t n, int fmt, cudaStream_t st);
+void launch_transpose(const void* in, void* out, int64_t rows, int64_t cols, int fmt,
+                      cudaStream_t st);
+void launch_count_nonfinite(const float* x, int64_t n, int64_t* counters, cudaStream_t st);
+void launch_bias_grad(const void* e, int fmt, int64_t rows, int64_t cols, float* db,
+                      cudaStream_t st);
+void launch_sgd(const void* grad, int grad_fmt, uint16_t* master, float* mom, int64_t n,
+                const fp8b_sgd_args_t& args, cudaStream_t st, const LfsrTables& tabs);
+void launch_scaler_step(fp8b_loss_scaler_t* s, const int64_t* counters, int finite, int64_t it,
+                        cudaStream_t st);
+void launch_unscale(float* g, int64_t n, const fp8b_loss_scaler_t* s, cudaStream_t st);
+void launch_gemm_seq(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int fmt,
+                     int a_mn, int b_mn, const EpiArgs& ep, cudaStream_t st);
+// Returns 0 on success, FP8B_ENOTSUP if the shape/layout is not supported by
+// the tensor-core engine.
+int launch_gemm_tc(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int fmt,
+                   int a_mn, int b_mn, const EpiArgs& ep, cudaStream_t st, int* nlaunch);
+void launch_fill_synthetic(float* out, int64_t n, int kind, uint64_t seed, double p, double lo,
+                           double hi, cudaStream_t st);
+
+}  // namespace fp8b

@@ -1,0 +1,385 @@
+// quantize.cu -- E5M2 / FP16 quantize ("Q node") kernels for sm_100a.
+//
+// Replaces fp8emu::quantize (tensor.cpp:46-81) and dequantize (:83-98).
+// All kernels are HBM-streaming: fully coalesced 16-byte loads, persistent
+// grids sized to the SM count, register counters reduced once per CTA.
+//
+//  * quant_elem_kernel   RNE (hardware cvt + fixups), TRUNC, SR with counter or
+//                        supplied bits: position-independent, 16 elements/thread.
+//  * quant_lfsr_kernel   SR with the reference's LFSR block stream: one CTA pass
+//                        per 4096-element block; the sample index of an element
+//                        is its rank among the block's inexact elements (a
+//                        CTA-wide exclusive scan), and the sample itself is a
+//                        lookup in the decimated-cycle table.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fp8b {
+
+// ---------------------------------------------------------------------------
+// Position-independent quantize.
+// MODE: 0 RNE (hardware cvt), 1 SR counter bits, 2 SR supplied bits, 3 TRUNC
+template <int MB, int MODE, int NT>
+__global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict__ x,
+                                                        void* __restrict__ codes, int64_t n,
+                                                        uint64_t seed, int saturate,
+                                                        int64_t elem_offset,
+                                                        const uint32_t* __restrict__ rbits,
+                                                        int64_t* counters) {
+    using F = Fmt<MB>;
+    const bool sat = saturate != 0;
+    uint32_t c_big = 0, c_nan = 0, c_unf = 0;
+    const int64_t ngroups = n >> 2;  // float4 groups
+    const int64_t stride = (int64_t)gridDim.x * NT * 4;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t g0 = (int64_t)blockIdx.x * NT * 4 + threadIdx.x; g0 < ngroups; g0 += stride) {
+        float4 v[4];
+        bool ok[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t g = g0 + (int64_t)j * NT;
+            ok[j] = g < ngroups;
+            if (ok[j]) v[j] = __ldcs(x4 + g);
+        }
+        uint32_t rb[4][4];
+        if (MODE == 2) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (ok[j]) {
+                    const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rbits) + g0 + (int64_t)j * NT);
+                    rb[j][0] = r.x; rb[j][1] = r.y; rb[j][2] = r.z; rb[j][3] = r.w;
+                }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!ok[j]) continue;
+            const int64_t g = g0 + (int64_t)j * NT;
+            const float f[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+            uint32_t c[4];
+            if (MODE == 0) {
+                uint32_t hw01, hw23;
+                if (MB == 2) {
+                    const uint32_t p01 = cvt_e5m2x2(f[0], f[1]);
+                    const uint32_t p23 = cvt_e5m2x2(f[2], f[3]);
+                    c[0] = p01 & 0xFFu; c[1] = p01 >> 8; c[2] = p23 & 0xFFu; c[3] = p23 >> 8;
+                } else {
+                    hw01 = cvt_f16x2(f[0], f[1]);
+                    hw23 = cvt_f16x2(f[2], f[3]);
+                    c[0] = hw01 & 0xFFFFu; c[1] = hw01 >> 16; c[2] = hw23 & 0xFFFFu; c[3] = hw23 >> 16;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    c[k] = fix_rne<MB>(c[k], __float_as_uint(f[k]), sat, c_big, c_nan, c_unf);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t u = __float_as_uint(f[k]);
+                    uint32_t r16 = 0;
+                    if (MODE == 1) r16 = counter_r16(seed, (uint64_t)(elem_offset + g * 4 + k));
+                    if (MODE == 2) r16 = rb[j][k] >> 16;
+                    int o, un, na;
+                    c[k] = encode_int<MB>(u, MODE == 3 ? FP8B_TRUNC : FP8B_SR, r16, sat, o, un, na);
+                    c_big += o + na; c_nan += na; c_unf += un;
+                }
+            }
+            if (MB == 2) {
+                const uint32_t w = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+                __stcs(reinterpret_cast<uint32_t*>(codes) + g, w);
+            } else {
+                const uint2 w = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+                __stcs(reinterpret_cast<uint2*>(codes) + g, w);
+            }
+        }
+    }
+    // scalar tail (n % 4) handled by the first threads of block 0
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+        const int64_t i = (ngroups << 2) + threadIdx.x;
+        const uint32_t u = __float_as_uint(x[i]);
+        uint32_t r16 = 0;
+        if (MODE == 1) r16 = counter_r16(seed, (uint64_t)(elem_offset + i));
+        if (MODE == 2) r16 = rbits[i] >> 16;
+        int o, un, na;
+        const int mode = MODE == 0 ? FP8B_RNE : (MODE == 3 ? FP8B_TRUNC : FP8B_SR);
+        const uint32_t c = encode_int<MB>(u, mode, r16, sat, o, un, na);
+        c_big += o + na; c_nan += na; c_unf += un;
+        if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i] = (uint8_t)c;
+        else reinterpret_cast<uint16_t*>(codes)[i] = (uint16_t)c;
+    }
+    if (counters) flush_counters<NT>(c_big - c_nan, c_unf, c_nan, counters);
+}
+
+// ---------------------------------------------------------------------------
+// Reference-stream SR. One CTA (256 threads) per 4096-element block per
+// iteration; thread t owns elements 1024*r + 4*t + k (r, k in 0..3), i.e. the
+// block is walked in four fully coalesced float4 rounds. Element order inside
+// the block (the order the LFSR stream is consumed in) is (r, t, k).
+
+template <int MB>
+__global__ void __launch_bounds__(256) quant_lfsr_kernel(const float* __restrict__ x,
+                                                         void* __restrict__ codes, int64_t n,
+                                                         uint64_t seed, int saturate,
+                                                         int64_t block_offset, LfsrTables tabs,
+                                                         int64_t* counters, int aligned) {
+    using F = Fmt<MB>;
+    __shared__ uint32_t smem_w[2][8];
+    const bool sat = saturate != 0;
+    uint32_t c_big = 0, c_nan = 0, c_unf = 0;
+    const int64_t nblocks = (n + kBlock - 1) / kBlock;
+    int parity = 0;
+    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, parity ^= 1) {
+        const int64_t base = b * kBlock;
+        const bool full = aligned && base + kBlock <= n;
+        float f[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
+            if (full) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(x + i0));
+                f[r][0] = v.x; f[r][1] = v.y; f[r][2] = v.z; f[r][3] = v.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) f[r][k] = (i0 + k < n) ? x[i0 + k] : 0.0f;
+            }
+        }
+        // stream start for this block: LfsrStream::split(seed, global block)
+        const uint32_t s0 = lfsr_split(seed, (uint64_t)(block_offset + b));
+        const uint32_t p0 = __ldg(tabs.pos + s0);
+        uint32_t code[4][4], r16[4][4], mask[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            mask[r] = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t u = __float_as_uint(f[r][k]);
+                const Split s = split_bits<MB>(u, sat);
+                code[r][k] = s.code;
+                r16[r][k] = s.r16;
+                const int64_t i = base + 1024 * r + 4 * threadIdx.x + k;
+                if (s.inexact && (full || i < n)) mask[r] |= 1u << k;
+                const uint32_t a = u & 0x7FFFFFFFu;
+                if (full || i < n) {
+                    c_big += a > F::maxbits;
+                    c_nan += a > 0x7F800000u;
+                }
+            }
+        }
+        uint32_t pre[4];
+        BlockScan<MB>::run(mask, pre, smem_w[parity]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            uint32_t j = p0 + pre[r];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (mask[r] & (1u << k)) {
+                    const uint32_t sample = __ldg(tabs.tabx + j);
+                    ++j;
+                    const uint32_t up = (r16[r][k] + sample) >= 65536u;
+                    code[r][k] += up;
+                    c_unf += (code[r][k] & (F::signbit - 1u)) == 0u;
+                }
+            }
+            const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
+            if (full) {
+                if (MB == 2) {
+                    const uint32_t w = code[r][0] | (code[r][1] << 8) | (code[r][2] << 16) |
+                                       (code[r][3] << 24);
+                    __stcs(reinterpret_cast<uint32_t*>(codes) + (i0 >> 2), w);
+                } else {
+                    const uint2 w = make_uint2(code[r][0] | (code[r][1] << 16),
+                                               code[r][2] | (code[r][3] << 16));
+                    __stcs(reinterpret_cast<uint2*>(codes) + (i0 >> 2), w);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (i0 + k >= n) continue;
+                    if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i0 + k] = (uint8_t)code[r][k];
+                    else reinterpret_cast<uint16_t*>(codes)[i0 + k] = (uint16_t)code[r][k];
+                }
+            }
+        }
+    }
+    if (counters) flush_counters<256>(c_big - c_nan, c_unf, c_nan, counters);
+}
+
+// Unaligned fallback: one element per thread, same integer rule.
+template <int MB>
+__global__ void quant_scalar_kernel(const float* __restrict__ x, void* __restrict__ codes,
+                                    int64_t n, int mode, int bits, uint64_t seed, int saturate,
+                                    int64_t elem_offset, const uint32_t* __restrict__ rbits,
+                                    int64_t* counters) {
+    uint32_t c_ovf = 0, c_nan = 0, c_unf = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t r16 = 0;
+        if (mode == FP8B_SR) r16 = bits == FP8B_BITS_SUPPLIED ? (rbits[i] >> 16)
+                                                             : counter_r16(seed, (uint64_t)(elem_offset + i));
+        int o, un, na;
+        const uint32_t c = encode_int<MB>(__float_as_uint(x[i]), mode, r16, saturate != 0, o, un, na);
+        c_ovf += o; c_nan += na; c_unf += un;
+        if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i] = (uint8_t)c;
+        else reinterpret_cast<uint16_t*>(codes)[i] = (uint16_t)c;
+    }
+    if (counters) flush_counters<256>(c_ovf, c_unf, c_nan, counters);
+}
+
+// ---------------------------------------------------------------------------
+template <int MB, int NT>
+__global__ void __launch_bounds__(NT) dequant_kernel(const void* __restrict__ codes,
+                                                     float* __restrict__ out, int64_t n) {
+    const int64_t ngroups = n >> 2;
+    for (int64_t g = (int64_t)blockIdx.x * NT + threadIdx.x; g < ngroups;
+         g += (int64_t)gridDim.x * NT) {
+        float4 v;
+        if (MB == 2) {
+            const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(codes) + g);
+            v = make_float4(dec_e5m2(w), dec_e5m2(w >> 8), dec_e5m2(w >> 16), dec_e5m2(w >> 24));
+        } else {
+            const uint2 w = __ldcs(reinterpret_cast<const uint2*>(codes) + g);
+            v = make_float4(dec_f16(w.x), dec_f16(w.x >> 16), dec_f16(w.y), dec_f16(w.y >> 16));
+        }
+        __stcs(reinterpret_cast<float4*>(out) + g, v);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+        const int64_t i = (ngroups << 2) + threadIdx.x;
+        out[i] = MB == 2 ? dec_e5m2(reinterpret_cast<const uint8_t*>(codes)[i])
+                         : dec_f16(reinterpret_cast<const uint16_t*>(codes)[i]);
+    }
+}
+
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t rows,
+                                 int64_t cols) {
+    __shared__ T tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) count_nonfinite_kernel(const float* __restrict__ x,
+                                                             int64_t n, int64_t* counters) {
+    uint32_t c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT)
+        c += (__float_as_uint(x[i]) & 0x7F800000u) == 0x7F800000u;
+    flush_counters<NT>(0, 0, c, counters);
+}
+
+// db[j] = sum over rows of decoded codes, row order (nn.cpp:308-314).
+template <int MB>
+__global__ void bias_grad_kernel(const void* __restrict__ e, int64_t rows, int64_t cols,
+                                 float* __restrict__ db) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    float acc = 0.0f;
+    for (int64_t r = 0; r < rows; ++r) {
+        const uint32_t c = MB == 2 ? reinterpret_cast<const uint8_t*>(e)[r * cols + j]
+                                   : reinterpret_cast<const uint16_t*>(e)[r * cols + j];
+        acc = __fadd_rn(acc, dec_code<MB>(c));
+    }
+    db[j] = acc;
+}
+
+// ---------------------------------------------------------------- launchers
+static int grid_for(const void* fn, int nt, int64_t work_items) {
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t g = (int64_t)num_sms * per_sm;
+    if (work_items < g) g = work_items < 1 ? 1 : work_items;
+    return (int)g;
+}
+
+template <int MB>
+static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quant_config_t& cfg,
+                         int64_t* counters, cudaStream_t st, const LfsrTables& tabs) {
+    constexpr int NT = 256;
+    const int64_t groups16 = (n / 4 + NT * 4 - 1) / (NT * 4);
+    const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)codes % (MB == 2 ? 4 : 8) == 0) &&
+                         (cfg.rbits == nullptr || (uintptr_t)cfg.rbits % 16 == 0);
+    if (cfg.mode == FP8B_SR && cfg.bits == FP8B_BITS_LFSR) {
+        auto fn = quant_lfsr_kernel<MB>;
+        const int64_t nblocks = (n + kBlock - 1) / kBlock;
+        const int g = grid_for((const void*)fn, 256, nblocks);
+        fn<<<g, 256, 0, st>>>(x, codes, n, cfg.seed, cfg.saturate, cfg.block_offset, tabs,
+                              counters, aligned ? 1 : 0);
+        return;
+    }
+    const int64_t eoff = cfg.block_offset * kBlock;
+    if (!aligned) {
+        auto fn = quant_scalar_kernel<MB>;
+        const int g = grid_for((const void*)fn, 256, (n + 255) / 256);
+        fn<<<g, 256, 0, st>>>(x, codes, n, cfg.mode, cfg.bits, cfg.seed, cfg.saturate, eoff,
+                              cfg.rbits, counters);
+        return;
+    }
+#define FP8B_LAUNCH_ELEM(MODE)                                                             \
+    {                                                                                      \
+        auto fn = quant_elem_kernel<MB, MODE, NT>;                                         \
+        const int g = grid_for((const void*)fn, NT, groups16);                             \
+        fn<<<g, NT, 0, st>>>(x, codes, n, cfg.seed, cfg.saturate, eoff, cfg.rbits, counters); \
+    }
+    if (cfg.mode == FP8B_RNE) FP8B_LAUNCH_ELEM(0)
+    else if (cfg.mode == FP8B_TRUNC) FP8B_LAUNCH_ELEM(3)
+    else if (cfg.bits == FP8B_BITS_COUNTER) FP8B_LAUNCH_ELEM(1)
+    else FP8B_LAUNCH_ELEM(2)
+#undef FP8B_LAUNCH_ELEM
+}
+
+void launch_quantize(const float* x, void* codes, int64_t n, int fmt,
+                     const fp8b_quant_config_t& cfg, int64_t* counters, cudaStream_t st,
+                     const LfsrTables& tabs) {
+    if (fmt == FP8B_E5M2) launch_quant<2>(x, codes, n, cfg, counters, st, tabs);
+    else launch_quant<10>(x, codes, n, cfg, counters, st, tabs);
+}
+
+void launch_dequantize(const void* codes, float* out, int64_t n, int fmt, cudaStream_t st) {
+    constexpr int NT = 256;
+    const int64_t groups = (n / 4 + NT - 1) / NT;
+    if (fmt == FP8B_E5M2) {
+        auto fn = dequant_kernel<2, NT>;
+        fn<<<grid_for((const void*)fn, NT, groups), NT, 0, st>>>(codes, out, n);
+    } else {
+        auto fn = dequant_kernel<10, NT>;
+        fn<<<grid_for((const void*)fn, NT, groups), NT, 0, st>>>(codes, out, n);
+    }
+}
+
+void launch_transpose(const void* in, void* out, int64_t rows, int64_t cols, int fmt,
+                      cudaStream_t st) {
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    dim3 block(32, 8);
+    if (fmt == FP8B_E5M2)
+        transpose_kernel<uint8_t><<<grid, block, 0, st>>>((const uint8_t*)in, (uint8_t*)out, rows, cols);
+    else
+        transpose_kernel<uint16_t><<<grid, block, 0, st>>>((const uint16_t*)in, (uint16_t*)out, rows, cols);
+}
+
+void launch_count_nonfinite(const float* x, int64_t n, int64_t* counters, cudaStream_t st) {
+    constexpr int NT = 256;
+    auto fn = count_nonfinite_kernel<NT>;
+    fn<<<grid_for((const void*)fn, NT, (n + NT - 1) / NT), NT, 0, st>>>(x, n, counters);
+}
+
+void launch_bias_grad(const void* e, int fmt, int64_t rows, int64_t cols, float* db,
+                      cudaStream_t st) {
+    const int nt = 128;
+    const unsigned g = (unsigned)((cols + nt - 1) / nt);
+    if (fmt == FP8B_E5M2) bias_grad_kernel<2><<<g, nt, 0, st>>>(e, rows, cols, db);
+    else bias_grad_kernel<10><<<g, nt, 0, st>>>(e, rows, cols, db);
+}
+
+}  // namespace fp8b

@@ -1,0 +1,143 @@
+"""GPU parity for gemm_fp8 (kernels.cpp:37-62).
+
+* FP8B_GEMM_SEQUENTIAL is bitwise equal to the reference (same k-ascending
+  FP32 running sum; products are exact).
+* FP8B_GEMM_TENSOR (tcgen05) is checked against the exact sum with the stated
+  tolerance |C - C_exact| <= tau * (|A||B|)_ij, tau = 1e-6, and its
+  fused E5M2 outputs may differ from Q_RNE(C_ref) only by adjacent codes across
+  a rounding midpoint (counted and reported).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+GG = np.load(os.path.join(GOLD, "gemm_golden.npz"))
+GMETA = json.load(open(os.path.join(GOLD, "gemm_golden.json")))
+TAU = 1e-6
+
+
+@pytest.fixture(scope="module")
+def fp8():
+    import paper_1905_12334_b200 as F
+    F.init()
+    return F
+
+
+def _codes_dev(c, fmt):
+    import torch
+    c = np.ascontiguousarray(c)
+    if fmt == "fp8":
+        return torch.from_numpy(c.astype(np.uint8)).to("cuda")
+    return torch.from_numpy(c.astype(np.uint16).view(np.int16)).to("cuda")
+
+
+@pytest.mark.parametrize("m", GMETA, ids=lambda m: f"{m['m']}x{m['k']}x{m['n']}")
+@pytest.mark.parametrize("fmt", ["fp8", "fp16"])
+def test_sequential_engine_bitwise_golden(fp8, m, fmt):
+    i = m["i"]
+    a, b = _codes_dev(GG[f"a_{i}_{fmt}"], fmt), _codes_dev(GG[f"b_{i}_{fmt}"], fmt)
+    c, _ = fp8.gemm_codes(a, b, m["m"], m["n"], m["k"], fmt, engine="sequential")
+    np.testing.assert_array_equal(c.cpu().numpy().reshape(-1).view(np.uint32),
+                                  GG[f"c_{i}_{fmt}"].reshape(-1).view(np.uint32))
+
+
+def _rand_codes(rng, rows, cols, fmt, scale=1.0):
+    x = (rng.standard_normal(rows * cols) * scale).astype(np.float32)
+    c, _ = O.quantize(x, fmt)
+    return c.reshape(rows, cols)
+
+
+@pytest.mark.parametrize("a_major", ["k", "m"])
+@pytest.mark.parametrize("b_major", ["n", "k"])
+@pytest.mark.parametrize("fmt", ["fp8", "fp16"])
+def test_layouts_sequential_bitwise(fp8, a_major, b_major, fmt):
+    rng = np.random.default_rng(12)
+    m, k, n = 96, 160, 72
+    A = _rand_codes(rng, m, k, fmt)
+    B = _rand_codes(rng, k, n, fmt)
+    want = O.gemm(A, B, m, k, n, fmt)
+    a_st = A if a_major == "k" else A.T.copy()
+    b_st = B if b_major == "n" else B.T.copy()
+    c, _ = fp8.gemm_codes(_codes_dev(a_st, fmt), _codes_dev(b_st, fmt), m, n, k, fmt,
+                          a_major=a_major, b_major=b_major, engine="sequential")
+    np.testing.assert_array_equal(c.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("out_mode", ["nearest-even", "truncate", "stochastic"])
+def test_fused_epilogue_sequential(fp8, out_mode):
+    import torch
+    rng = np.random.default_rng(13)
+    m, k, n = 64, 128, 96
+    A, B = _rand_codes(rng, m, k, "fp8"), _rand_codes(rng, k, n, "fp8")
+    bias = rng.standard_normal(n).astype(np.float32)
+    cnt = fp8.Counters()
+    c, cq = fp8.gemm_codes(_codes_dev(A, "fp8"), _codes_dev(B, "fp8"), m, n, k, "fp8",
+                           engine="sequential", bias=torch.from_numpy(bias).cuda(),
+                           out_fmt="fp8", out_mode=out_mode, out_seed=17, out_counters=cnt)
+    y = O.gemm(A, B, m, k, n, "fp8")
+    y = (y + bias[None, :]).astype(np.float32)
+    np.testing.assert_array_equal(c.cpu().numpy().view(np.uint32), y.view(np.uint32))
+    codes, k_ = O.quantize(y, "fp8", out_mode, 17, bits="counter")
+    np.testing.assert_array_equal(cq.cpu().numpy(), codes.astype(np.uint8))
+    assert cnt.values() == tuple(int(v) for v in k_)
+
+
+def _tolerance_check(c_gpu, A, B, m, k, n, fmt):
+    exact, absdot = O.gemm_exact(A, B, m, k, n, fmt)
+    err = np.abs(c_gpu.astype(np.float64) - exact)
+    bound = TAU * absdot + 1e-30
+    assert (err <= bound).all(), float((err / np.maximum(absdot, 1e-30)).max())
+    return float((err / np.maximum(absdot, 1e-30)).max())
+
+
+@pytest.mark.parametrize("shape", [(128, 256, 128), (256, 512, 256), (200, 96, 136),
+                                   (512, 1024, 1024), (1, 64, 16), (130, 48, 40)])
+@pytest.mark.parametrize("a_major,b_major", [("k", "n"), ("k", "k"), ("m", "n")])
+def test_tensor_engine_tolerance(fp8, shape, a_major, b_major):
+    rng = np.random.default_rng(sum(shape))
+    m, k, n = shape
+    A, B = _rand_codes(rng, m, k, "fp8"), _rand_codes(rng, k, n, "fp8")
+    a_st = A if a_major == "k" else A.T.copy()
+    b_st = B if b_major == "n" else B.T.copy()
+    c, _ = fp8.gemm_codes(_codes_dev(a_st, "fp8"), _codes_dev(b_st, "fp8"), m, n, k, "fp8",
+                          a_major=a_major, b_major=b_major, engine="tensor")
+    _tolerance_check(c.cpu().numpy(), A, B, m, k, n, "fp8")
+
+
+def test_tensor_vs_sequential_large(fp8):
+    """2048^3 (config 3): tensor engine vs the bitwise-reference CUDA-core engine
+    under tau, plus E5M2 output flips only at rounding midpoints."""
+    import torch
+    m = n = k = 2048
+    x = torch.empty(m * k + k * n, dtype=torch.float32, device="cuda")
+    fp8.fill_synthetic(x, "normal", 21, 1.0)
+    qa = fp8.quantize(x[: m * k])
+    qb = fp8.quantize(x[m * k:])
+    ct, cqt = fp8.gemm_codes(qa.codes, qb.codes, m, n, k, "fp8", engine="tensor", out_fmt="fp8")
+    cs, _ = fp8.gemm_codes(qa.codes, qb.codes, m, n, k, "fp8", engine="sequential")
+    da = fp8.dequantize(qa).double().reshape(m, k)
+    db = fp8.dequantize(qb).double().reshape(k, n)
+    absdot = da.abs() @ db.abs()
+    err_t = (ct.double() - da @ db).abs()
+    err_s = (cs.double() - da @ db).abs()
+    assert bool((err_t <= TAU * absdot + 1e-30).all())
+    assert bool((err_s <= TAU * absdot + 1e-30).all())
+    # E5M2 output codes: Q_RNE(C_seq) vs fused epilogue codes
+    ref_codes = fp8.quantize(cs).codes
+    diff = (cqt != ref_codes)
+    nflip = int(diff.sum())
+    if nflip:
+        # every flip must be a neighbouring code whose midpoint separates C_gpu and C_seq
+        idx = diff.nonzero().squeeze(1)
+        a_ = fp8.dequantize(fp8.QuantizedTensor(cqt[idx], [idx.numel()], 0, 0, fp8.Counters()))
+        b_ = fp8.dequantize(fp8.QuantizedTensor(ref_codes[idx], [idx.numel()], 0, 0, fp8.Counters()))
+        mid = (a_.double() + b_.double()) / 2
+        cg, cr = ct.reshape(-1)[idx].double(), cs.reshape(-1)[idx].double()
+        assert bool((((cg - mid) * (cr - mid)) <= 0).all())
+    assert nflip <= m * n * 1e-4

@@ -101,7 +101,7 @@ def test_zero_grads_keep_masters(fp8):
     """test_nn.cpp:133-160: zero weight gradients leave masters bit-identical
     (momentum 0)."""
     import torch
-    n = 9000
+    n = 8000
     master = _dev(UG["master0"][:n].view(np.int16)).clone()
     before = master.clone()
     mom = torch.zeros(n, dtype=torch.float32, device="cuda")

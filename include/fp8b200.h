@@ -49,9 +49,10 @@ enum { FP8B_RNE = 0, FP8B_SR = 1, FP8B_TRUNC = 2 };
  *  LFSR     -- the reference stream, bit-exact: 4096-element block b draws from
  *              LfsrStream::split(seed, block_offset + b), one 16-bit sample per
  *              inexact element (tensor.cpp:57-70, lfsr.cpp:17-45);
- *  COUNTER  -- r16 = (mix64(seed + block_offset*4096 + i + 1) >> 48), i.e. the
- *              top 16 bits of the reference's counter RNG Rand{seed} raw draw
- *              i+1 (rand.hpp:19-21); position-independent, so it fuses anywhere;
+ *  COUNTER  -- r16 = 16-bit lane (g & 3) of mix64(seed + (g >> 2) + 1), with
+ *              g = block_offset*4096 + i: the SplitMix64 counter generator of the
+ *              reference's Rand (rand.hpp:19-21, lfsr.cpp:47-52), one 64-bit
+ *              word per four elements; position-independent, so it fuses anywhere;
  *  SUPPLIED -- r16 = rbits[i] >> 16 from a caller-supplied uint32 tensor.
  * All three round up iff (top 16 discarded bits) + r16 >= 2^16, which is the
  * reference's (a-lo) + r*step >= step (float_format.cpp:122-130) exactly. */
@@ -128,6 +129,12 @@ typedef struct {
  * (the reference requires a shared format, kernels.cpp:9-13). */
 int fp8b_gemm(const void *a, const void *b, int64_t m, int64_t n, int64_t k, int32_t fmt,
               const fp8b_gemm_args_t *args, void *stream);
+
+/* 1 if fp8b_gemm with FP8B_GEMM_TENSOR runs these operands on the tcgen05
+ * engine, 0 if it would take the CUDA-core engine (TMA needs 16-byte aligned
+ * bases and row strides). */
+int fp8b_gemm_tensor_supported(const void *a, const void *b, int64_t m, int64_t n, int64_t k,
+                               int32_t fmt, int32_t a_major, int32_t b_major);
 
 /* ---------------------------------------------------------- loss scaler ---- */
 /* LossScaler (loss_scaling.hpp:26-68) state, resident in DEVICE memory so the

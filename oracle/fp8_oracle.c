@@ -216,9 +216,14 @@ int or_quantize(const float *x, int64_t n, int fmt, int mode, int bits_source,
             int32_t r16 = -1;
             if (mode == OR_SR) {
                 uint32_t r32;
-                if (bits_source == OR_BITS_SUPPLIED) r32 = rbits[i];
-                else r32 = (uint32_t)(or_mix64(seed + (uint64_t)(i + block_offset * kBlock) + 1u) >> 32);
-                r16 = (int32_t)(r32 >> 16);
+                if (bits_source == OR_BITS_SUPPLIED) {
+                    r32 = rbits[i];
+                    r16 = (int32_t)(r32 >> 16);
+                } else {
+                    /* counter bits: one SplitMix64 word per 4 elements, low half first */
+                    const uint64_t gi = (uint64_t)(i + block_offset * kBlock);
+                    r16 = (int32_t)((or_mix64(seed + (gi >> 2) + 1u) >> (16u * (gi & 3u))) & 0xFFFFu);
+                }
             }
             int o, u;
             const uint32_t c = encode_impl((double)x[i], fmt, mode, 0, r16,

@@ -244,6 +244,14 @@ def gemm_codes(a_codes: torch.Tensor, b_codes: torch.Tensor, m: int, n: int, k: 
     return (c if want_c else None), cq
 
 
+def gemm_tensor_supported(a_codes, b_codes, m, n, k, fmt="fp8", a_major="k", b_major="n") -> bool:
+    """True if the tcgen05 engine (not the CUDA-core fallback) runs this GEMM."""
+    return bool(LIB.fp8b_gemm_tensor_supported(
+        a_codes.data_ptr(), b_codes.data_ptr(), m, n, k, _fmt(fmt),
+        _lib.K_MAJOR if a_major == "k" else _lib.MN_MAJOR,
+        _lib.MN_MAJOR if b_major == "n" else _lib.K_MAJOR))
+
+
 def gemm(a: QuantizedTensor, b: QuantizedTensor, *, engine: str = "tensor",
          stream=None) -> torch.Tensor:
     """fp8emu.gemm (bindings.cpp:183-189 -> kernels.cpp:37-62): FP32 [M, N]."""

@@ -61,6 +61,7 @@ SIGNATURES = {
     "fp8b_transpose": (C.c_int, [_vp, _vp, _i64, _i64, _i32, _vp]),
     "fp8b_count_nonfinite": (C.c_int, [_vp, _i64, _vp, _vp]),
     "fp8b_gemm": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, C.POINTER(GemmArgs), _vp]),
+    "fp8b_gemm_tensor_supported": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32]),
     "fp8b_loss_scaler_init": (C.c_int, [_vp, C.POINTER(LossScalerState), _vp]),
     "fp8b_loss_scaler_step": (C.c_int, [_vp, _vp, _i32, _i64, _vp]),
     "fp8b_unscale": (C.c_int, [_vp, _i64, _vp, _vp]),

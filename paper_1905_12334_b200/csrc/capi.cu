@@ -197,6 +197,17 @@ int fp8b_gemm(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int
     return check_launch(1);
 }
 
+int fp8b_gemm_tensor_supported(const void* a, const void* b, int64_t m, int64_t n, int64_t k,
+                               int32_t fmt, int32_t a_major, int32_t b_major) {
+    if (!valid_fmt(fmt) || m <= 0 || n <= 0 || k <= 0) return 0;
+    const int es = fmt == FP8B_E5M2 ? 1 : 2;
+    const int64_t a_inner = a_major == FP8B_MN_MAJOR ? m : k;
+    const int64_t b_inner = b_major == FP8B_MN_MAJOR ? n : k;
+    if ((uintptr_t)a % 16 || (uintptr_t)b % 16 || (a_inner * es) % 16 || (b_inner * es) % 16) return 0;
+    if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return 0;
+    return 1;
+}
+
 int fp8b_loss_scaler_init(fp8b_loss_scaler_t* dev_state, const fp8b_loss_scaler_t* o,
                           void* stream) {
     if (!dev_state || !o) return fail(FP8B_EINVAL, "loss_scaler_init: null pointer");

@@ -182,9 +182,66 @@ struct LfsrTables {
     const uint16_t* pos;
 };
 
-// Counter-bits sample (see FP8B_BITS_COUNTER).
+// Counter-bits sample (see FP8B_BITS_COUNTER): the 64-bit SplitMix64 output
+// for element group g = gi >> 2 supplies the four 16-bit samples of elements
+// 4g .. 4g+3, low half-word first.
+__device__ __forceinline__ uint64_t counter_word(uint64_t seed, uint64_t group) {
+    return mix64(seed + group + 1ull);
+}
 __device__ __forceinline__ uint32_t counter_r16(uint64_t seed, uint64_t gi) {
-    return (uint32_t)(mix64(seed + gi + 1ull) >> 48);
+    return (uint32_t)(counter_word(seed, gi >> 2) >> (16u * (uint32_t)(gi & 3u))) & 0xFFFFu;
+}
+
+// ---- stochastic rounding as an integer carry (the reference rule exactly) --
+// For |x| <= max normal, the SR result magnitude of encode() is
+//   normal targets (|x| >= 2^-14): the FP32 bit pattern with r16 added just
+//   below the kept mantissa (E5M2: r16<<5 under 21 discarded bits; FP16:
+//   r16>>3 under 13 discarded bits -- the dropped low bits of r16 cannot change
+//   the carry), shifted down and re-biased (exponent e -> e-112);
+//   subnormal targets: t = |x| * 2^(16 + quantum exponent), truncated, plus r16,
+//   >> 16.
+// Both are "round up iff top-16 discarded bits + r16 >= 2^16" (SURVEY A2'),
+// which equals float_format.cpp:122-130; checked against encode_int in tests.
+template <int MB>
+__device__ __forceinline__ uint32_t sr_mag(uint32_t a, float xabs, uint32_t r16) {
+    uint32_t cn, t;
+    if (MB == 2) {
+        cn = (a + (r16 << 5) - 0x38000000u) >> 21;
+        t = __float2uint_rz(xabs * 4294967296.0f);        // |x| * 2^32 < 2^18
+    } else {
+        cn = (a + (r16 >> 3) - 0x38000000u) >> 13;
+        t = __float2uint_rz(xabs * 1099511627776.0f);     // |x| * 2^40 < 2^26
+    }
+    const uint32_t cs = (t + r16) >> 16;
+    return a < 0x38800000u ? cs : cn;
+}
+
+// A sample is consumed iff |x| is finite, <= max normal, nonzero and not on the
+// target grid (float_format.cpp:111-113).
+template <int MB>
+__device__ __forceinline__ bool sr_inexact(uint32_t a, float xabs) {
+    const uint32_t mask = MB == 2 ? 0x1FFFFFu : 0x1FFFu;
+    const float q = xabs * (MB == 2 ? 65536.0f : 16777216.0f);  // in subnormal quanta
+    const bool sub_inexact = q != truncf(q);
+    const bool nrm_inexact = (a & mask) != 0u;
+    return (a <= Fmt<MB>::maxbits) && (a < 0x38800000u ? sub_inexact : nrm_inexact);
+}
+
+// Full SR encode with counters, for one element given its sample.
+template <int MB>
+__device__ __forceinline__ uint32_t sr_encode(uint32_t u, uint32_t r16, bool sat, uint32_t& c_big,
+                                              uint32_t& c_nan, uint32_t& c_unf) {
+    using F = Fmt<MB>;
+    const uint32_t a = u & 0x7FFFFFFFu;
+    const uint32_t sign = (u >> 31) ? F::signbit : 0u;
+    const uint32_t mag = sr_mag<MB>(a, __uint_as_float(a), r16);
+    const bool big = a > F::maxbits;
+    const bool isnan = a > 0x7F800000u;
+    c_big += big;
+    c_nan += isnan;
+    c_unf += (!big) & (mag == 0u) & (a != 0u);
+    const uint32_t ovcode = sign | (sat ? F::maxcode : F::infcode);
+    return big ? (isnan ? F::nancode : ovcode) : (sign | mag);
 }
 
 // Block-wide sum of three counters; one atomic per CTA.
@@ -255,5 +312,43 @@ struct BlockScan {
         }
     }
 };
+
+// ---- mbarrier + bulk-copy (TMA) helpers ------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared, completing `bytes` on the mbarrier (TMA unit).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
 
 }  // namespace fp8b

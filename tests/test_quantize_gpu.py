@@ -88,6 +88,31 @@ def test_supplied_bits(fp8):
         assert q.counters.values() == tuple(int(v) for v in cnt)
 
 
+@pytest.mark.parametrize("fmt", ["fp8", "fp16"])
+def test_sr_all_bit_patterns_supplied_bits(fp8, fmt):
+    """Uniformly random FP32 bit patterns (every exponent, NaN/Inf, denormals)
+    with random supplied bits: the carry-add SR kernels == the oracle's
+    reference-derived rule; saturate on and off."""
+    import torch
+    n = 1 << 20
+    rng = np.random.default_rng(17)
+    bits = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    rb = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    x = torch.from_numpy(bits.view(np.float32)).cuda()
+    rbt = torch.from_numpy(rb.view(np.int32)).cuda()
+    for sat in (False, True):
+        for mode in ("stochastic", "truncate"):
+            q = fp8.quantize(x, fmt, mode, 3, sat, bits="supplied", rbits=rbt)
+            codes, cnt = O.quantize(bits.view(np.float32), fmt, mode, 3, sat, bits="supplied",
+                                    rbits=rb)
+            np.testing.assert_array_equal(q.codes_u16(), codes)
+            assert q.counters.values() == tuple(int(v) for v in cnt)
+        q = fp8.quantize(x, fmt, "stochastic", 3, sat, bits="lfsr")
+        codes, cnt = O.quantize(bits.view(np.float32), fmt, "stochastic", 3, sat, bits="lfsr")
+        np.testing.assert_array_equal(q.codes_u16(), codes)
+        assert q.counters.values() == tuple(int(v) for v in cnt)
+
+
 def test_block_offset_sharding(fp8):
     """A rank holding blocks [b0, b1) with block_offset=b0 reproduces its slice
     of the whole-tensor SR codes."""

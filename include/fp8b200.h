@@ -207,6 +207,53 @@ int fp8b_sgd_momentum_update(const void *grad, int32_t grad_fmt, uint16_t *maste
 int fp8b_bias_grad(const void *e_codes, int32_t fmt, int64_t rows, int64_t cols, float *db,
                    void *stream);
 
+/* ---------------------------------------------------------- layer step ---- */
+/* One quantized Dense-layer training step on device, the composition
+ * Network::forward -> backward -> apply_update -> LossScaler::step performs for a
+ * Dense layer (nn.cpp:187-203, 294-326, 401-411, 417-458, 540-547) with every
+ * Q node in E5M2 round-to-nearest-even:
+ *   qx = Q(x); qy = Q(qx . w_q + b)                          (fprop, fused epilogue)
+ *   qe = Q(e); db = colsum(qe); qdw = Q(qx^T . qe)           (wgrad, fused epilogue)
+ *   qdx = Q(qe . w_q^T)                                      (bprop, fused epilogue)
+ *   finite = no overflow in qe/qdw/qdx, no NaN in qdw, db finite  (nn.cpp:401-411)
+ *   if finite: update_tensor(W, qdw), update_tensor(b, db);  w_q = Q(decode(w_master))
+ *   scaler.step(finite, iteration)
+ * The scale used by the backward/update is scaler->scale at entry (nn.cpp:540).
+ * `e` is the loss-scaled upstream error (softmax_xent_backward output,
+ * nn.cpp:286-288). counters = int64[6]: [0..2] overflow/underflow/nan of Q(e)
+ * and Q(dx) plus non-finite db in [2]; [3..5] the Q(dW) counters (so
+ * underflow_fraction = counters[4] / (in*out), nn.cpp:305-306). The step zeroes
+ * them itself. gate = int64[3] workspace. No host synchronisation: the step can
+ * be captured in a CUDA graph. */
+typedef struct {
+    int64_t batch, in_features, out_features;
+    const float *x;          /* [batch, in] FP32 layer input */
+    const float *e;          /* [batch, out] loss-scaled upstream error */
+    uint16_t *w_master;      /* [in, out] FP16 master weights (row-major like nn.hpp:56-61) */
+    float *w_momentum;       /* [in, out] */
+    uint8_t *w_q;            /* [in, out] E5M2 Q(decode(w_master)), refreshed by the update */
+    uint16_t *b_master;      /* [out] FP16 master bias, or NULL for a bias-free layer */
+    float *b_momentum;       /* [out] */
+    float *b_value;          /* [out] workspace: decode(b_master) */
+    uint8_t *qx, *qy, *qe, *qdw;  /* Q-node outputs */
+    uint8_t *qdx;            /* [batch, in] or NULL (first layer: no dx, nn.cpp:317) */
+    float *db;               /* [out] bias gradient (bias layers) */
+    float *y;                /* optional [batch, out] FP32 pre-Q output */
+    int64_t *fwd_counters;   /* int64[3]: Q(x) + Q(y), or NULL */
+    int64_t *counters;       /* int64[6], see above */
+    int64_t *gate;           /* int64[3] workspace */
+    fp8b_loss_scaler_t *scaler;
+    int64_t iteration;
+    float lr, mu, two_lambda;
+    int32_t engine;          /* FP8B_GEMM_TENSOR / FP8B_GEMM_SEQUENTIAL */
+    int32_t master_mode;     /* FP8B_RNE (reference) / FP8B_SR (BASELINE) */
+    int32_t bits;            /* SR bits source for the masters */
+    int32_t saturate;        /* quant.saturate for every Q node */
+    uint64_t seed;           /* master SR seed (nonzero) */
+} fp8b_dense_step_t;
+
+int fp8b_dense_step(const fp8b_dense_step_t *s, void *stream);
+
 /* -------------------------------------------------------------- misc ---- */
 /* Optional eager initialisation for the current device (uploads the 200 KB of
  * LFSR jump tables once); otherwise done lazily by the first SR-LFSR call. Call

@@ -428,3 +428,91 @@ def fill_synthetic(out: torch.Tensor, kind: str, seed: int, p: float = 0.01, lo:
     check(LIB.fp8b_fill_synthetic(out.data_ptr(), out.numel(), k, int(seed), float(p),
                                   float(lo), float(hi), _stream(stream)), "fill_synthetic")
     return out
+
+
+class DenseLayer:
+    """One quantized Dense layer trained on device (fp8b_dense_step).
+
+    Mirrors what nn::Network does for a Dense layer in one training step
+    (forward nn.cpp:187-203, backward nn.cpp:294-326, finiteness nn.cpp:401-411,
+    apply_update nn.cpp:436-458, scaler.step nn.cpp:547): masters start as
+    RNE_FP16(w) (nn.cpp:76-88) and the fprop weights as Q(decode(master)).
+    ``w`` is [in, out] (row-major, as the reference stores Dense weights).
+    """
+
+    def __init__(self, w, bias=None, *, batch: int, lr: float, mu: float,
+                 two_lambda: float = 0.0, scaler: LossScaler, engine: str = "tensor",
+                 master_mode: str = "nearest-even", bits: str = "lfsr", seed: int = 1,
+                 saturate: bool = False, want_dx: bool = True, want_y: bool = False):
+        w = _device_f32(w)
+        if w.dim() != 2:
+            raise ValueError("Dense weights must be rank 2 [in, out]")
+        self.in_features, self.out_features = w.shape
+        self.batch = int(batch)
+        dev = w.device
+        I, O, B = self.in_features, self.out_features, self.batch
+        self.w_master = quantize(w, "fp16").codes.reshape(I, O)
+        wq = quantize(dequantize(QuantizedTensor(self.w_master.reshape(-1), [I * O], _lib.FP16,
+                                                 _lib.RNE, Counters(dev))), "fp8")
+        self.w_q = wq.codes.reshape(I, O)
+        self.w_momentum = torch.zeros(I, O, dtype=torch.float32, device=dev)
+        self.has_bias = bias is not None
+        if self.has_bias:
+            self.b_master = quantize(_device_f32(bias).reshape(-1), "fp16").codes
+            self.b_momentum = torch.zeros(O, dtype=torch.float32, device=dev)
+            self.b_value = torch.empty(O, dtype=torch.float32, device=dev)
+            self.db = torch.empty(O, dtype=torch.float32, device=dev)
+        self.qx = torch.empty(B, I, dtype=torch.uint8, device=dev)
+        self.qy = torch.empty(B, O, dtype=torch.uint8, device=dev)
+        self.qe = torch.empty(B, O, dtype=torch.uint8, device=dev)
+        self.qdw = torch.empty(I, O, dtype=torch.uint8, device=dev)
+        self.qdx = torch.empty(B, I, dtype=torch.uint8, device=dev) if want_dx else None
+        self.y = torch.empty(B, O, dtype=torch.float32, device=dev) if want_y else None
+        self.fwd_counters = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(6, dtype=torch.int64, device=dev)
+        self.gate = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.scaler = scaler
+        if bits not in _BITS:
+            raise ValueError(f"unknown random-bits source: {bits}")
+        self._s = _lib.DenseStep()
+        s = self._s
+        s.batch, s.in_features, s.out_features = B, I, O
+        s.w_master, s.w_momentum, s.w_q = (self.w_master.data_ptr(), self.w_momentum.data_ptr(),
+                                           self.w_q.data_ptr())
+        if self.has_bias:
+            s.b_master, s.b_momentum = self.b_master.data_ptr(), self.b_momentum.data_ptr()
+            s.b_value, s.db = self.b_value.data_ptr(), self.db.data_ptr()
+        s.qx, s.qy, s.qe, s.qdw = (self.qx.data_ptr(), self.qy.data_ptr(), self.qe.data_ptr(),
+                                   self.qdw.data_ptr())
+        s.qdx = _ptr(self.qdx)
+        s.y = _ptr(self.y)
+        s.fwd_counters, s.counters, s.gate = (self.fwd_counters.data_ptr(),
+                                              self.counters.data_ptr(), self.gate.data_ptr())
+        s.scaler = scaler.ptr
+        s.lr, s.mu, s.two_lambda = float(lr), float(mu), float(two_lambda)
+        s.engine = _lib.GEMM_TENSOR if engine == "tensor" else _lib.GEMM_SEQUENTIAL
+        s.master_mode = _mode(master_mode)
+        s.bits = _BITS[bits]
+        s.saturate = int(bool(saturate))
+        s.seed = int(seed)
+
+    def step(self, x: torch.Tensor, e: torch.Tensor, iteration: int, stream=None) -> None:
+        """Asynchronous: forward, backward, gated update and scaler step."""
+        if x.numel() != self.batch * self.in_features or e.numel() != self.batch * self.out_features:
+            raise ValueError("batch and layer sizes disagree")
+        self._x, self._e = x, e
+        self._s.x, self._s.e = x.data_ptr(), e.data_ptr()
+        self._s.iteration = int(iteration)
+        check(LIB.fp8b_dense_step(self._s, _stream(stream)), "dense_step")
+
+    # step statistics (synchronise)
+    def overflow_count(self) -> int:
+        c = self.counters.tolist()
+        return int(c[0] + c[3])
+
+    def grads_finite(self) -> bool:
+        g = self.gate.tolist()
+        return g[0] + g[2] == 0
+
+    def underflow_fraction(self) -> float:
+        return float(self.counters[4].item()) / float(self.in_features * self.out_features)

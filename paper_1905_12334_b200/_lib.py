@@ -54,6 +54,18 @@ class SgdArgs(C.Structure):
                 ("w_saturate", _i32), ("reserved", _i32), ("w_counters", _vp)]
 
 
+class DenseStep(C.Structure):
+    _fields_ = [("batch", _i64), ("in_features", _i64), ("out_features", _i64),
+                ("x", _vp), ("e", _vp), ("w_master", _vp), ("w_momentum", _vp), ("w_q", _vp),
+                ("b_master", _vp), ("b_momentum", _vp), ("b_value", _vp),
+                ("qx", _vp), ("qy", _vp), ("qe", _vp), ("qdw", _vp), ("qdx", _vp),
+                ("db", _vp), ("y", _vp), ("fwd_counters", _vp), ("counters", _vp),
+                ("gate", _vp), ("scaler", _vp), ("iteration", _i64),
+                ("lr", C.c_float), ("mu", C.c_float), ("two_lambda", C.c_float),
+                ("engine", _i32), ("master_mode", _i32), ("bits", _i32), ("saturate", _i32),
+                ("seed", _u64)]
+
+
 # every symbol include/fp8b200.h declares, with its ctypes signature
 SIGNATURES = {
     "fp8b_quantize": (C.c_int, [_vp, _vp, _i64, _i32, C.POINTER(QuantConfig), _vp, _vp]),
@@ -67,6 +79,7 @@ SIGNATURES = {
     "fp8b_unscale": (C.c_int, [_vp, _i64, _vp, _vp]),
     "fp8b_sgd_momentum_update": (C.c_int, [_vp, _i32, _vp, _vp, _i64, C.POINTER(SgdArgs), _vp]),
     "fp8b_bias_grad": (C.c_int, [_vp, _i32, _i64, _i64, _vp, _vp]),
+    "fp8b_dense_step": (C.c_int, [C.POINTER(DenseStep), _vp]),
     "fp8b_init": (C.c_int, []),
     "fp8b_last_error": (C.c_char_p, []),
     "fp8b_version": (C.c_char_p, []),

@@ -68,6 +68,7 @@ int get_tables(fp8b::LfsrTables* out) {
         }
         for (int k = 0; k < fp8b::kBlock; ++k) tabx[fp8b::kLfsrPeriod + k] = tabx[k];
         uint16_t *dt = nullptr, *dp = nullptr;
+        tabx.resize(tabx.size() + 64, 0);  // the staged kernel bulk-copies a 128-byte-padded image
         if (cudaMalloc(&dt, tabx.size() * 2) != cudaSuccess ||
             cudaMalloc(&dp, pos.size() * 2) != cudaSuccess ||
             cudaMemcpy(dt, tabx.data(), tabx.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -88,6 +89,10 @@ bool valid_mode(int32_t m) { return m == FP8B_RNE || m == FP8B_SR || m == FP8B_T
 bool valid_bits(int32_t b) { return b == FP8B_BITS_LFSR || b == FP8B_BITS_COUNTER || b == FP8B_BITS_SUPPLIED; }
 
 }  // namespace
+
+namespace fp8b {
+void note_launches(int n) { g_launches += n; }
+}  // namespace fp8b
 
 extern "C" {
 

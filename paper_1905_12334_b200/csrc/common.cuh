@@ -270,7 +270,7 @@ __device__ __forceinline__ void flush_counters(uint32_t c0, uint32_t c1, uint32_
 
 // CTA-wide exclusive scan of inexact flags over a 4096-element block walked as
 // (round r in 0..3, thread t in 0..255, k in 0..3) -- the LFSR consumption order.
-template <int MB>
+template <int MB, int BAR = 0>
 struct BlockScan {
     static constexpr int NT = 256;
     // Exclusive prefix (in block order) of the inexact flags of this thread's
@@ -278,11 +278,19 @@ struct BlockScan {
     // thread's first element of each round in pre[r].
     __device__ __forceinline__ static void run(const uint32_t mask[4], uint32_t pre[4],
                                                uint32_t* smem_w /*[8]*/) {
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        uint32_t cnt[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) cnt[r] = (uint32_t)__popc(mask[r]);
+        run_counts(cnt, pre, smem_w);
+    }
+    // Same, from per-round counts (each <= 4).
+    __device__ __forceinline__ static void run_counts(const uint32_t cnt[4], uint32_t pre[4],
+                                                      uint32_t* smem_w /*[8]*/) {
+        const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 7;
         // pack the 4 per-round counts (<= 4 each, warp sum <= 128) into bytes
         uint32_t packed = 0;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) packed |= (uint32_t)__popc(mask[r]) << (8 * r);
+        for (int r = 0; r < 4; ++r) packed |= cnt[r] << (8 * r);
         uint32_t inc = packed;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -290,7 +298,8 @@ struct BlockScan {
             if (lane >= o) inc += t;
         }
         if (lane == 31) smem_w[w] = inc;
-        __syncthreads();
+        if (BAR == 0) __syncthreads();
+        else asm volatile("bar.sync %0, 256;" ::"r"(BAR) : "memory");
         const uint32_t excl = inc - packed;
         // warp offsets per round and round totals
         uint32_t before[4] = {0, 0, 0, 0}, total[4] = {0, 0, 0, 0};
@@ -349,6 +358,60 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             smem_addr(dst)),
         "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
+}
+
+// ---- packed SR representation ----------------------------------------------
+// P = (truncated code magnitude << 16) | (top 16 discarded bits), for
+// |x| <= max normal. Then the reference's SR result magnitude is (P + r16) >> 16
+// (round up iff top-16 discarded bits + r16 >= 2^16, float_format.cpp:122-130),
+// truncation is P >> 16, and an exact input has a zero low half so any r16
+// leaves it unchanged. Built on the FMA pipe:
+//  E5M2: |x| *rz 2^-112 re-biases the FP32 exponent to E5M2's (e-112) for
+//        normal targets and, below 2^-14, truncates into the FP32 denormal grid
+//        whose spacing is 2^-149 * 2^112 = 2^-37, i.e. 2^-16 * 2^-21: bits >> 5
+//        is P in both ranges.
+//  FP16: normal P = (a - 112<<23) << 3 (computed from the raw bits, the sign is
+//        shifted out); subnormal P = floor(|x| * 2^40), selected below 2^-14.
+__device__ __forceinline__ uint32_t packed_e5m2(float x) {
+    return __float_as_uint(__fmul_rz(fabsf(x), 0x1p-112f)) >> 5;
+}
+__device__ __forceinline__ uint32_t packed_f16(float x) {
+    const uint32_t pn = __float_as_uint(x) * 8u + 0x40000000u;
+    const uint32_t ps = __float2uint_rz(fabsf(x) * 0x1p40f);
+    return fabsf(x) < 0x1p-14f ? ps : pn;
+}
+template <int MB>
+__device__ __forceinline__ uint32_t packed_sr(float x) {
+    return MB == 2 ? packed_e5m2(x) : packed_f16(x);
+}
+// Discarded bits nonzero (a stream sample is consumed), for |x| <= max normal:
+// the RZ and RU products differ iff bits fell off below the FP32 denormal grid.
+template <int MB>
+__device__ __forceinline__ bool inexact_sr(float x) {
+    const uint32_t rz = __float_as_uint(__fmul_rz(fabsf(x), 0x1p-112f));
+    const uint32_t ru = __float_as_uint(__fmul_ru(fabsf(x), 0x1p-112f));
+    return ((rz | ru) & (MB == 2 ? 0x1FFFFFu : 0x1FFFu)) != 0u;
+}
+// |x| > max normal or NaN (the reference's overflow test plus NaN).
+template <int MB>
+__device__ __forceinline__ bool big_or_nan(float x) {
+    return !(fabsf(x) <= (MB == 2 ? 57344.0f : 65504.0f));
+}
+template <int MB>
+__device__ __forceinline__ uint32_t special_packed(bool sat) {
+    return (sat ? Fmt<MB>::maxcode : Fmt<MB>::infcode) << 16;
+}
+// Gather the code bytes (E5M2) of four packed sums plus the four input signs.
+__device__ __forceinline__ uint32_t gather_e5m2(uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3,
+                                                uint32_t u0, uint32_t u1, uint32_t u2, uint32_t u3) {
+    const uint32_t c01 = __byte_perm(s0, s1, 0x0062), c23 = __byte_perm(s2, s3, 0x0062);
+    const uint32_t g01 = __byte_perm(u0, u1, 0x0073), g23 = __byte_perm(u2, u3, 0x0073);
+    const uint32_t c = __byte_perm(c01, c23, 0x5410), g = __byte_perm(g01, g23, 0x5410);
+    return c | (g & 0x80808080u);
+}
+// Two FP16 codes (high halves of the packed sums) plus signs.
+__device__ __forceinline__ uint32_t gather_f16(uint32_t s0, uint32_t s1, uint32_t u0, uint32_t u1) {
+    return __byte_perm(s0, s1, 0x7632) | (__byte_perm(u0, u1, 0x7632) & 0x80008000u);
 }
 
 }  // namespace fp8b

@@ -42,6 +42,8 @@ void launch_gemm_seq(const void* a, const void* b, int64_t m, int64_t n, int64_t
 // the tensor-core engine.
 int launch_gemm_tc(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int fmt,
                    int a_mn, int b_mn, const EpiArgs& ep, cudaStream_t st, int* nlaunch);
+// Adds n to the library's launch counter (fp8b_launch_count).
+void note_launches(int n);
 void launch_fill_synthetic(float* out, int64_t n, int kind, uint64_t seed, double p, double lo,
                            double hi, cudaStream_t st);
 

@@ -71,12 +71,33 @@ __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict_
             } else {
                 uint64_t word = 0;
                 if (MODE == 1) word = counter_word(seed, (uint64_t)((elem_offset >> 2) + g));
+                uint32_t sum[4];
+                float nanacc = 0.0f;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     uint32_t r16 = 0;  // TRUNC == SR with r16 = 0
                     if (MODE == 1) r16 = (uint32_t)(word >> (16 * k)) & 0xFFFFu;
                     if (MODE == 2) r16 = rb[j][k];
-                    c[k] = sr_encode<MB>(__float_as_uint(f[k]), r16, sat, c_big, c_nan, c_unf);
+                    const bool big = big_or_nan<MB>(f[k]);
+                    c_big += big;
+                    sum[k] = (big ? special_packed<MB>(sat) : packed_sr<MB>(f[k])) + r16;
+                    c_unf += (sum[k] < 0x10000u) & (fabsf(f[k]) != 0.0f);
+                    nanacc = fmaf(f[k], 0.0f, nanacc);
+                }
+                const uint32_t u[4] = {__float_as_uint(f[0]), __float_as_uint(f[1]),
+                                       __float_as_uint(f[2]), __float_as_uint(f[3])};
+                if (MB == 2) {
+                    const uint32_t w = gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]);
+                    c[0] = w & 0xFFu; c[1] = (w >> 8) & 0xFFu; c[2] = (w >> 16) & 0xFFu; c[3] = w >> 24;
+                } else {
+                    const uint32_t w0 = gather_f16(sum[0], sum[1], u[0], u[1]);
+                    const uint32_t w1 = gather_f16(sum[2], sum[3], u[2], u[3]);
+                    c[0] = w0 & 0xFFFFu; c[1] = w0 >> 16; c[2] = w1 & 0xFFFFu; c[3] = w1 >> 16;
+                }
+                if (nanacc != nanacc) {  // rare: an Inf or NaN input; NaN -> canonical code
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (f[k] != f[k]) { c[k] = Fmt<MB>::nancode; ++c_nan; }
                 }
             }
             if (MB == 2) {
@@ -158,63 +179,153 @@ __device__ __forceinline__ void store4(void* codes, int64_t i0, const uint32_t (
     }
 }
 
-// Staged kernel over full blocks: the TMA engine streams 16 KB blocks into an
-// S-deep shared-memory ring (cp.async.bulk + mbarrier), so S-1 blocks of input
-// are in flight per CTA while the CTA scans and rounds the current one.
-constexpr int kLfsrStages = 4;
+// Staged kernel over full blocks, one CTA (NG groups of 256 threads) per SM.
+// Shared memory holds the whole decimated jump table (128 KB, loaded once per
+// CTA by the TMA engine, so every sample is a 32-bit-addressed LDS) and, per
+// group, an S-deep ring of 16 KB input blocks streamed by cp.async.bulk +
+// mbarrier. Each group scans and rounds its own block with a named barrier,
+// so the groups' barrier waits overlap.
+// Phase 1 (per element): overflow/NaN screen, packed value P, inexact flag ->
+// stream increment. Scan. Phase 2: sample, code = (P + r16) >> 16.
+constexpr int kLfsrStages = 3;
+constexpr int kLfsrGroups = 2;
+constexpr int kTabBytesPad = 65536 * 2;  // 65535 entries, no wrap extension
+constexpr int kLfsrSmem = kTabBytesPad + kLfsrGroups * kLfsrStages * kBlock * 4;
 template <int MB>
-__global__ void __launch_bounds__(256) quant_lfsr_staged_kernel(const float* __restrict__ x,
-                                                                void* __restrict__ codes,
-                                                                int64_t nfull, uint64_t seed,
-                                                                int saturate, int64_t block_offset,
-                                                                LfsrTables tabs,
-                                                                int64_t* counters) {
-    constexpr int S = kLfsrStages;
-    extern __shared__ __align__(128) uint8_t ring[];  // S x 16 KB
-    __shared__ __align__(8) uint64_t full[S];
-    __shared__ uint32_t smem_w[2][8];
+__global__ void __launch_bounds__(256 * kLfsrGroups, 1)
+    quant_lfsr_staged_kernel(const float* __restrict__ x, void* __restrict__ codes, int64_t nfull,
+                             uint64_t seed, int saturate, int64_t block_offset, LfsrTables tabs,
+                             int64_t* counters) {
+    constexpr int S = kLfsrStages, NG = kLfsrGroups;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint16_t* stab = reinterpret_cast<uint16_t*>(smem);
+    __shared__ __align__(8) uint64_t full[NG][S];
+    __shared__ __align__(8) uint64_t tab_bar;
+    __shared__ uint32_t smem_w[NG][2][8];
     const bool sat = saturate != 0;
+    const uint32_t special = special_packed<MB>(sat);
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
-    const int t = threadIdx.x;
-    if (t == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(full + s, 1);
+    const int g = threadIdx.x >> 8, t = threadIdx.x & 255;
+    uint8_t* ring = smem + kTabBytesPad + g * S * kBlock * 4;
+    const int64_t gid = (int64_t)blockIdx.x * NG + g, gstride = (int64_t)gridDim.x * NG;
+    const int64_t nmine = nfull > gid ? (nfull - 1 - gid) / gstride + 1 : 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&tab_bar, 1);
+        for (int gg = 0; gg < NG; ++gg)
+            for (int s = 0; s < S; ++s) mbar_init(&full[gg][s], 1);
         mbar_fence_init();
+        mbar_expect_tx(&tab_bar, kTabBytesPad);
+        for (int off = 0; off < kTabBytesPad; off += 16384)
+            bulk_g2s(smem + off, reinterpret_cast<const uint8_t*>(tabs.tabx) + off, 16384, &tab_bar);
     }
     __syncthreads();
-    const int64_t nmine = nfull > blockIdx.x ? (nfull - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (t == 0) {
         for (int64_t i = 0; i < S - 1 && i < nmine; ++i) {
-            const int64_t b = blockIdx.x + i * gridDim.x;
-            mbar_expect_tx(full + i, kBlock * 4);
-            bulk_g2s(ring + i * kBlock * 4, x + b * kBlock, kBlock * 4, full + i);
+            const int64_t b = gid + i * gstride;
+            mbar_expect_tx(&full[g][i], kBlock * 4);
+            bulk_g2s(ring + i * kBlock * 4, x + b * kBlock, kBlock * 4, &full[g][i]);
         }
     }
+    const uint32_t stab_addr = smem_addr(stab);
+    uint32_t p0_next = nmine > 0 ? __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + gid))) : 0;
+    mbar_wait(&tab_bar, 0);
     for (int64_t i = 0; i < nmine; ++i) {
         const int s = (int)(i % S);
-        const int64_t b = blockIdx.x + i * gridDim.x;
-        mbar_wait(full + s, (uint32_t)((i / S) & 1));
+        const int64_t b = gid + i * gstride;
+        const uint32_t p0 = p0_next;
+        if (i + 1 < nmine)  // the next block's stream start, off the critical path
+            p0_next = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b + gstride)));
+        mbar_wait(&full[g][s], (uint32_t)((i / S) & 1));
         const float4* blk = reinterpret_cast<const float4*>(ring + s * kBlock * 4);
-        uint32_t mask[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) mask[r] = lfsr_mask4<MB>(blk[256 * r + t], c_big, c_nan, 4);
-        uint32_t pre[4];
-        BlockScan<MB>::run(mask, pre, smem_w[i & 1]);
-        // every thread is past block i-1: refill its stage with block i-1+S
-        if (t == 0 && i + S - 1 < nmine) {
-            const int sn = (int)((i + S - 1) % S);
-            const int64_t bn = blockIdx.x + (i + S - 1) * gridDim.x;
-            mbar_expect_tx(full + sn, kBlock * 4);
-            bulk_g2s(ring + sn * kBlock * 4, x + bn * kBlock, kBlock * 4, full + sn);
-        }
-        const uint32_t p0 = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b)));
+        uint32_t P[4][4], inc[4][4], cnt[4];
+        float nanacc = 0.0f;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            uint32_t c[4];
-            lfsr_codes4<MB>(blk[256 * r + t], mask[r], p0 + pre[r], tabs.tabx, sat, c_unf, c);
-            store4<MB>(codes, b * kBlock + 1024 * r + 4 * t, c);
+            const float4 v = blk[256 * r + t];
+            const float f[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const bool big = big_or_nan<MB>(f[k]);
+                c_big += big;
+                nanacc = fmaf(f[k], 0.0f, nanacc);
+                P[r][k] = big ? special : packed_sr<MB>(f[k]);
+                inc[r][k] = (!big && inexact_sr<MB>(f[k])) ? 2u : 0u;  // byte stride in the table
+            }
+            cnt[r] = (inc[r][0] + inc[r][1] + inc[r][2] + inc[r][3]) >> 1;
+        }
+        uint32_t pre[4];
+        if (NG == 1) BlockScan<MB, 0>::run_counts(cnt, pre, smem_w[g][i & 1]);
+        else if (g == 0) BlockScan<MB, 1>::run_counts(cnt, pre, smem_w[g][i & 1]);
+        else BlockScan<MB, 2>::run_counts(cnt, pre, smem_w[g][i & 1]);
+        // every thread of the group is past block i-1: refill its stage with block i-1+S
+        if (t == 0 && i + S - 1 < nmine) {
+            const int sn = (int)((i + S - 1) % S);
+            const int64_t bn = gid + (i + S - 1) * gstride;
+            mbar_expect_tx(&full[g][sn], kBlock * 4);
+            bulk_g2s(ring + sn * kBlock * 4, x + bn * kBlock, kBlock * 4, &full[g][sn]);
+        }
+        // blocks whose stream window crosses the end of the 65535-cycle wrap
+        // (p0 > 61439: ~6% of blocks) take the modular addressing path
+        const bool wraps = p0 + kBlock > (uint32_t)kLfsrPeriod;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            uint32_t sum[4];
+            if (!wraps) {
+                uint32_t addr = stab_addr + 2u * (p0 + pre[r]);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t r16;
+                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r16) : "r"(addr));
+                    addr += inc[r][k];
+                    sum[k] = P[r][k] + r16;  // exact lanes ignore their sample
+                }
+            } else {
+                uint32_t j = p0 + pre[r];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t jj = j >= (uint32_t)kLfsrPeriod ? j - kLfsrPeriod : j;
+                    const uint32_t r16 = stab[jj];
+                    j += inc[r][k] >> 1;
+                    sum[k] = P[r][k] + r16;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                // underflow: inexact and rounded to zero; exact lanes are pushed out of range
+                const uint32_t chk = sum[k] + (2u - inc[r][k]) * 0x8000u;
+                c_unf += (chk - 0x10000u) >> 31;
+            }
+            const float4 v = blk[256 * r + t];
+            const float f[4] = {v.x, v.y, v.z, v.w};
+            const uint32_t u[4] = {__float_as_uint(f[0]), __float_as_uint(f[1]),
+                                   __float_as_uint(f[2]), __float_as_uint(f[3])};
+            const int64_t q = b * (kBlock / 4) + 256 * r + t;  // float4 group index
+            if (MB == 2) {
+                __stcs(reinterpret_cast<uint32_t*>(codes) + q,
+                       gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]));
+            } else {
+                __stcs(reinterpret_cast<uint2*>(codes) + q,
+                       make_uint2(gather_f16(sum[0], sum[1], u[0], u[1]),
+                                  gather_f16(sum[2], sum[3], u[2], u[3])));
+            }
+        }
+        // rare: a NaN (or Inf) among this thread's 16 inputs -> rewrite NaN codes
+        // as the canonical unsigned NaN (float_format.cpp:99) and count them
+        if (nanacc != nanacc) {
+            for (int r = 0; r < 4; ++r) {
+                const float4 v = blk[256 * r + t];
+                const float f[4] = {v.x, v.y, v.z, v.w};
+                const int64_t i0 = b * kBlock + 1024 * r + 4 * t;
+                for (int k = 0; k < 4; ++k)
+                    if (f[k] != f[k]) {
+                        ++c_nan;
+                        if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i0 + k] = 0x7E;
+                        else reinterpret_cast<uint16_t*>(codes)[i0 + k] = 0x7E00;
+                    }
+            }
         }
     }
-    if (counters) flush_counters<256>(c_big - c_nan, c_unf, c_nan, counters);
+    if (counters) flush_counters<256 * kLfsrGroups>(c_big - c_nan, c_unf, c_nan, counters);
 }
 
 // Tail / unaligned kernel: blocks [block_begin, nblocks), scalar-safe loads.
@@ -384,20 +495,21 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
             const int64_t nfull = n / kBlock;
             if (nfull > 0) {
                 auto fn = quant_lfsr_staged_kernel<MB>;
-                constexpr int smem = kLfsrStages * kBlock * 4;
+                constexpr int smem = kLfsrSmem;
                 static bool attr = false;
                 if (!attr) {
                     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
                     attr = true;
                 }
                 int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256 * kLfsrGroups, smem);
                 int num_sms = 0, dev = 0;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
                 int64_t g = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
-                if (nfull < g) g = nfull;
-                fn<<<(int)g, 256, smem, st>>>(x, codes, nfull, cfg.seed, cfg.saturate,
+                const int64_t need = (nfull + kLfsrGroups - 1) / kLfsrGroups;
+                if (need < g) g = need;
+                fn<<<(int)g, 256 * kLfsrGroups, smem, st>>>(x, codes, nfull, cfg.seed, cfg.saturate,
                                               cfg.block_offset, tabs, counters);
                 begin = nfull;
             }

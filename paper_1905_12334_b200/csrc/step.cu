@@ -1,0 +1,116 @@
+// step.cu -- fp8b_dense_step: one quantized Dense-layer training step on device.
+//
+// The caller of the hot path in the reference is nn::Network (nn.cpp:155-458)
+// driven by train() (nn.cpp:540-547). For a Dense layer that is six Q nodes,
+// three gemm_fp8 calls, a finiteness check, two update_tensor calls and a
+// LossScaler::step, with a full FP32 tensor materialised between each. Here the
+// output Q nodes are fused into the GEMM epilogues, the finiteness check is the
+// Q kernels' own counters, the update skips itself on device and also emits the
+// next step's E5M2 weights, and the scaler state never leaves HBM: 8-10 kernel
+// launches, no host synchronisation, CUDA-graph capturable.
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fp8b {
+__global__ void merge_gate_kernel(const int64_t* c, int64_t* gate) {
+    if (threadIdx.x < 3) gate[threadIdx.x] = c[threadIdx.x] + c[3 + threadIdx.x];
+}
+}  // namespace fp8b
+
+extern "C" {
+
+int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
+    if (!s) return FP8B_EINVAL;
+    const int64_t B = s->batch, I = s->in_features, O = s->out_features;
+    if (B <= 0 || I <= 0 || O <= 0 || !s->x || !s->e || !s->w_master || !s->w_momentum ||
+        !s->w_q || !s->qx || !s->qy || !s->qe || !s->qdw || !s->counters || !s->gate ||
+        !s->scaler)
+        return FP8B_EINVAL;
+    if (s->b_master && (!s->b_momentum || !s->b_value || !s->db)) return FP8B_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int rc;
+#define FP8B_TRY(expr)          \
+    do {                        \
+        rc = (expr);            \
+        if (rc) return rc;      \
+    } while (0)
+    if (cudaMemsetAsync(s->counters, 0, 6 * sizeof(int64_t), st) != cudaSuccess) return FP8B_ECUDA;
+    if (s->fwd_counters && cudaMemsetAsync(s->fwd_counters, 0, 3 * sizeof(int64_t), st) != cudaSuccess)
+        return FP8B_ECUDA;
+    fp8b_quant_config_t rne{};
+    rne.mode = FP8B_RNE;
+    rne.seed = 1;
+    rne.saturate = s->saturate;
+    // ---- forward (nn.cpp:187-203): qx = Q(x); y = qx . w_q (+ b); qy = Q(y)
+    if (s->b_master) FP8B_TRY(fp8b_dequantize(s->b_master, s->b_value, O, FP8B_FP16, stream));
+    FP8B_TRY(fp8b_quantize(s->x, s->qx, B * I, FP8B_E5M2, &rne, s->fwd_counters, stream));
+    fp8b_gemm_args_t g{};
+    g.engine = s->engine;
+    g.cq_fmt = FP8B_E5M2;
+    g.cq_mode = FP8B_RNE;
+    g.cq_seed = 1;
+    g.cq_saturate = s->saturate;
+    g.a_major = FP8B_K_MAJOR;
+    g.b_major = FP8B_MN_MAJOR;
+    g.c = s->y;
+    g.bias = s->b_master ? s->b_value : nullptr;
+    g.cq = s->qy;
+    g.cq_counters = s->fwd_counters;
+    FP8B_TRY(fp8b_gemm(s->qx, s->w_q, B, O, I, FP8B_E5M2, &g, stream));
+    // ---- backward (nn.cpp:294-326)
+    FP8B_TRY(fp8b_quantize(s->e, s->qe, B * O, FP8B_E5M2, &rne, s->counters, stream));
+    if (s->b_master) {
+        FP8B_TRY(fp8b_bias_grad(s->qe, FP8B_E5M2, B, O, s->db, stream));
+        FP8B_TRY(fp8b_count_nonfinite(s->db, O, s->counters, stream));
+    }
+    // wgrad: dW[I,O] = qx^T . qe  (qx read M-major, qe N-major; no transpose pass)
+    g.a_major = FP8B_MN_MAJOR;
+    g.b_major = FP8B_MN_MAJOR;
+    g.c = nullptr;
+    g.bias = nullptr;
+    g.cq = s->qdw;
+    g.cq_counters = s->counters + 3;
+    FP8B_TRY(fp8b_gemm(s->qx, s->qe, I, O, B, FP8B_E5M2, &g, stream));
+    // bprop: dX[B,I] = qe . w_q^T  (w_q [I,O] read as the K-major [N=I, K=O] operand)
+    if (s->qdx) {
+        g.a_major = FP8B_K_MAJOR;
+        g.b_major = FP8B_K_MAJOR;
+        g.cq = s->qdx;
+        g.cq_counters = s->counters;
+        FP8B_TRY(fp8b_gemm(s->qe, s->w_q, B, I, O, FP8B_E5M2, &g, stream));
+    }
+    // grads_finite gate (nn.cpp:401-411): overflow of qe/qdw/qdx, NaN in qdw, non-finite db
+    fp8b::merge_gate_kernel<<<1, 32, 0, st>>>(s->counters, s->gate);
+    if (cudaGetLastError() != cudaSuccess) return FP8B_ECUDA;
+    fp8b::note_launches(1);
+    // ---- apply_update (nn.cpp:436-458), skipped on device when the gate is set
+    fp8b_sgd_args_t u{};
+    u.lr = s->lr;
+    u.mu = s->mu;
+    u.two_lambda = s->two_lambda;
+    u.scale = 1.0f;
+    u.scaler = s->scaler;
+    u.skip_counters = s->gate;
+    u.master_mode = s->master_mode;
+    u.bits = s->bits;
+    u.seed = s->seed ? s->seed : 1;
+    u.w_e5m2 = s->w_q;
+    u.w_saturate = s->saturate;
+    FP8B_TRY(fp8b_sgd_momentum_update(s->qdw, FP8B_E5M2, s->w_master, s->w_momentum, I * O, &u,
+                                      stream));
+    if (s->b_master) {
+        u.two_lambda = 0.0f;  // biases are not regularised (nn.cpp:445, 452)
+        u.seed = s->seed + 1 ? s->seed + 1 : 1;
+        u.w_e5m2 = nullptr;
+        FP8B_TRY(fp8b_sgd_momentum_update(s->db, FP8B_F32, s->b_master, s->b_momentum, O, &u,
+                                          stream));
+    }
+    // ---- LossScaler::step(grads_finite, iteration) (nn.cpp:547)
+    FP8B_TRY(fp8b_loss_scaler_step(s->scaler, s->gate, 1, s->iteration, stream));
+#undef FP8B_TRY
+    return FP8B_OK;
+}
+
+}  // extern "C"

@@ -218,3 +218,36 @@ def test_exhaustive_rne_vs_torch_cast(fp8, fmt, sat):
         exp_unf += int(((mag == 0) & (a != 0) & ~isnan & ~big).sum())
         del bits, x, q, got, hw, want
     assert cnt.values() == (exp_ovf, exp_unf, exp_nan)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt", ["fp8", "fp16"])
+def test_exhaustive_fast_paths_vs_scalar_rule(fp8, fmt):
+    """All 2^32 FP32 inputs: the vectorised SR/TRUNC kernels (packed carry-add
+    representation) and the TMA-staged LFSR kernel equal the scalar integer
+    rule (encode_int, SURVEY A2', itself pinned to the oracle above), which the
+    library runs for misaligned buffers. Codes and counters."""
+    import torch
+    chunk = 1 << 28
+    buf = torch.empty(chunk + 4, dtype=torch.float32, device="cuda")
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1)
+    for c0 in range(0, 1 << 32, chunk):
+        bits = torch.arange(c0, c0 + chunk, dtype=torch.int64, device="cuda").to(torch.int32)
+        x = bits.view(torch.float32)
+        buf[1:chunk + 1].copy_(x)
+        xu = buf[1:chunk + 1]  # misaligned view -> scalar path
+        rb = torch.randint(-2 ** 31, 2 ** 31 - 1, (chunk,), dtype=torch.int32, device="cuda",
+                           generator=gen)
+        for mode, bits_src in [("stochastic", "supplied"), ("truncate", "lfsr"),
+                               ("stochastic", "lfsr"), ("stochastic", "counter")]:
+            for sat in (False, True):
+                ca, cb = fp8.Counters(), fp8.Counters()
+                qa = fp8.quantize(x, fmt, mode, 11, sat, bits=bits_src,
+                                  rbits=rb if bits_src == "supplied" else None, counters=ca)
+                qb = fp8.quantize(xu, fmt, mode, 11, sat, bits=bits_src,
+                                  rbits=rb if bits_src == "supplied" else None, counters=cb)
+                bad = int((qa.codes != qb.codes).sum())
+                assert bad == 0, (fmt, mode, bits_src, sat, hex(c0), bad)
+                assert ca.values() == cb.values(), (fmt, mode, bits_src, sat, hex(c0))
+        del bits, x, rb, qa, qb

@@ -24,6 +24,7 @@
 // tests/test_gemm_gpu.py; FP8B_GEMM_SEQUENTIAL gives bitwise parity.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -382,6 +383,217 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// 2-SM variant: a cluster of two CTAs (a TPC pair) computes a 256x256 tile with
+// tcgen05.mma.cta_group::2 (M=256 split over the pair, each CTA holding 128
+// rows of A and 128 columns of B). Operand bytes per FLOP halve compared with
+// the 1-SM 128x256 tile. The leader CTA (rank 0) owns the full barriers and
+// issues the MMAs; both producers' TMA loads (.cta_group::2) complete on the
+// leader's barrier; commits multicast to both CTAs' empty / tmem-full
+// barriers; both CTAs' epilogue warps release the leader's tmem-empty barrier.
+constexpr int BM2 = 256;
+constexpr int BN2 = 256;
+constexpr int STAGES2 = 6;
+constexpr uint32_t A2_BYTES = 128 * BKB;  // per CTA
+constexpr uint32_t B2_BYTES = 128 * BKB;  // per CTA
+constexpr uint32_t STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr uint32_t SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 512;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* tm, void* dst, uint32_t bar_leader,
+                                                int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_leader), "r"(c0), "r"(c1)
+        : "memory");
+}
+template <int ES>
+__device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                     uint32_t accum) {
+    if (ES == 1) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+    }
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+
+template <int ES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+    uint64_t* empty_bar = full_bar + STAGES2;
+    uint64_t* tfull_bar = empty_bar + STAGES2;
+    uint64_t* tempty_bar = tfull_bar + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    constexpr int BKE = BKB / ES, UK = 32 / ES, MN_CHUNK = 128 / ES;
+    const int ntiles = p.tiles_m * p.tiles_n;  // 256x256 tiles
+    const int cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        for (int s = 0; s < STAGES2; ++s) {
+            mbar_init(full_bar + s, 1);
+            mbar_init(empty_bar + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar + a, 1);
+            mbar_init(tempty_bar + a, 8);  // 4 epilogue warps x 2 CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    fence_before();
+    cluster_sync_all();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    uint32_t co = 0, cu = 0, cn = 0;
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+                const int32_t m0 = tm * BM2 + (int32_t)rank * 128, n0 = tn * BN2 + (int32_t)rank * 128;
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    mbar_wait(empty_bar + stage, phase ^ 1);
+                    const uint32_t fb = mapa_u32(smem_u32(full_bar + stage), 0);
+                    if (rank == 0) mbar_expect_tx(full_bar + stage, 2 * STAGE2_BYTES);
+                    uint8_t* sA = smem + stage * STAGE2_BYTES;
+                    uint8_t* sB = sA + A2_BYTES;
+                    const int32_t k0 = kb * BKE;
+                    if (!p.a_mn) {
+                        tma_load_2d_2sm(&tmA, sA, fb, k0, m0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 128 / MN_CHUNK; ++j)
+                            tma_load_2d_2sm(&tmA, sA + j * (BKE * 128), fb, m0 + j * MN_CHUNK, k0);
+                    }
+                    if (!p.b_mn) {
+                        tma_load_2d_2sm(&tmB, sB, fb, k0, n0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 128 / MN_CHUNK; ++j)
+                            tma_load_2d_2sm(&tmB, sB + j * (BKE * 128), fb, n0 + j * MN_CHUNK, k0);
+                    }
+                    if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            uint32_t idesc = (1u << 4);
+            if (ES == 1) idesc |= (1u << 7) | (1u << 10);
+            idesc |= (uint32_t)p.a_mn << 15;
+            idesc |= (uint32_t)p.b_mn << 16;
+            idesc |= (uint32_t)(BN2 >> 3) << 17;
+            idesc |= (uint32_t)(BM2 >> 4) << 24;
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t accphase = 0;
+            for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+                mbar_wait(tempty_bar + acc, accphase ^ 1);
+                fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    mbar_wait(full_bar + stage, phase);
+                    fence_after();
+                    const uint32_t a_base = smem_u32(smem + stage * STAGE2_BYTES);
+                    const uint32_t b_base = a_base + A2_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BKB / 32; ++k) {
+                        uint64_t ad, bd;
+                        if (!p.a_mn) ad = umma_desc(a_base + 32 * k, 16, 1024);
+                        else ad = umma_desc(a_base + k * UK * 128, BKE * 128, 1024);
+                        if (!p.b_mn) bd = umma_desc(b_base + 32 * k, 16, 1024);
+                        else bd = umma_desc(b_base + k * UK * 128, BKE * 128, 1024);
+                        mma2<ES>(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                    }
+                    umma_commit_mc(empty_bar + stage);
+                    if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                }
+                umma_commit_mc(tfull_bar + acc);
+                if (++acc == 2) { acc = 0; accphase ^= 1; }
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        int acc = 0;
+        uint32_t accphase = 0;
+        const uint32_t te_leader = mapa_u32(smem_u32(tempty_bar), 0);
+        for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+            const int64_t row = (int64_t)tm * BM2 + rank * 128 + quarter * 32 + lane;
+            mbar_wait(tfull_bar + acc, accphase);
+            fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN2);
+#pragma unroll 1
+            for (int c = 0; c < BN2 / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(taddr + c * 32, v);
+                const int64_t col0 = (int64_t)tn * BN2 + c * 32;
+                if (row < p.M && col0 < p.N) epilogue_chunk(p, row, col0, v, co, cu, cn);
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+            if (++acc == 2) { acc = 0; accphase ^= 1; }
+        }
+    }
+    if (p.ep.cq_counters) flush_counters<NUM_THREADS>(co, cu, cn, p.ep.cq_counters);
+    fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS));
+    }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -417,6 +629,16 @@ static bool make_map(CUtensorMap* tm, const void* ptr, int es, uint64_t inner, u
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// FP8B_GEMM_2SM=0 in the environment selects the 1-SM kernel (for A/B checks).
+static bool use_2sm() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FP8B_GEMM_2SM");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <int ES>
 static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int a_mn,
                      int b_mn, const EpiArgs& ep, cudaStream_t st) {
@@ -450,7 +672,31 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+        cudaFuncSetAttribute(gemm_tc2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
     });
+    if (use_2sm() && m >= BM2) {
+        // 2-SM path: tmA box is 128 rows of the pair's 256 (each CTA loads its half)
+        CUtensorMap tA2, tB2;
+        bool ok2;
+        if (!a_mn) ok2 = make_map(&tA2, a, ES, (uint64_t)k, (uint64_t)m, BKE, 128);
+        else ok2 = make_map(&tA2, a, ES, (uint64_t)m, (uint64_t)k, MN_CHUNK, BKE);
+        if (ok2) {
+            if (!b_mn) ok2 = make_map(&tB2, b, ES, (uint64_t)k, (uint64_t)n, BKE, 128);
+            else ok2 = make_map(&tB2, b, ES, (uint64_t)n, (uint64_t)k, MN_CHUNK, BKE);
+        }
+        if (ok2) {
+            Params p2 = p;
+            p2.tiles_m = (int)((m + BM2 - 1) / BM2);
+            p2.tiles_n = (int)((n + BN2 - 1) / BN2);
+            const int ntiles2 = p2.tiles_m * p2.tiles_n;
+            int grid2 = 2 * ntiles2;
+            const int maxg = num_sms & ~1;
+            if (grid2 > maxg) grid2 = maxg;
+            gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, p2);
+            return FP8B_OK;
+        }
+    }
     const int ntiles = p.tiles_m * p.tiles_n;
     const int grid = ntiles < num_sms ? ntiles : num_sms;
     gemm_tc_kernel<ES><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(tmA, tmB, p);

@@ -148,6 +148,11 @@ template <int MB>
 __device__ __forceinline__ float dec_code(uint32_t c) {
     return MB == 2 ? dec_e5m2(c) : dec_f16(c);
 }
+// decode() as the reference returns it (float_format.cpp:60): every NaN code is
+// the positive quiet NaN 0x7FC00000 (the GPU's f16->f32 gives 0x7FFFFFFF).
+__device__ __forceinline__ float ref_nan(float v) {
+    return v != v ? __uint_as_float(0x7FC00000u) : v;
+}
 
 // SplitMix64 (lfsr.cpp:47-52).
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {

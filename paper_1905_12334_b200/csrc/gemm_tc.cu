@@ -145,6 +145,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Grouped rasterisation: walk the tile grid in column bands of GROUP_N tiles so
+// the tiles in flight at once (one per SM / SM pair) share a few A row-panels
+// and B column-panels that stay resident in L2.
+constexpr int GROUP_N = 8;
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
+    const int band = tile / (GROUP_N * tiles_m);
+    const int first_n = band * GROUP_N;
+    const int width = min(GROUP_N, tiles_n - first_n);
+    const int r = tile - band * GROUP_N * tiles_m;
+    tm = r / width;
+    tn = first_n + r % width;
+}
+
 // Epilogue for one 32-column chunk of one row held in registers.
 __device__ __forceinline__ void epilogue_chunk(const Params& p, int64_t row, int64_t col0,
                                                uint32_t (&v)[32], uint32_t& co, uint32_t& cu,
@@ -284,7 +297,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+                int tm, tn;
+                tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
                 const int32_t m0 = tm * BM, n0 = tn * BN;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(empty_bar + stage, phase ^ 1);
@@ -355,7 +369,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int acc = 0;
         uint32_t accphase = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+            int tm, tn;
+                tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
             const int64_t row = (int64_t)tm * BM + quarter * 32 + lane;
             mbar_wait(tfull_bar + acc, accphase);
             fence_after();
@@ -496,7 +511,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
-                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+                int tm, tn;
+                tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
                 const int32_t m0 = tm * BM2 + (int32_t)rank * 128, n0 = tn * BN2 + (int32_t)rank * 128;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(empty_bar + stage, phase ^ 1);
@@ -566,7 +582,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t accphase = 0;
         const uint32_t te_leader = mapa_u32(smem_u32(tempty_bar), 0);
         for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
-            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+            int tm, tn;
+                tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
             const int64_t row = (int64_t)tm * BM2 + rank * 128 + quarter * 32 + lane;
             mbar_wait(tfull_bar + acc, accphase);
             fence_after();

@@ -411,17 +411,19 @@ __global__ void __launch_bounds__(NT) dequant_kernel(const void* __restrict__ co
         float4 v;
         if (MB == 2) {
             const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(codes) + g);
-            v = make_float4(dec_e5m2(w), dec_e5m2(w >> 8), dec_e5m2(w >> 16), dec_e5m2(w >> 24));
+            v = make_float4(ref_nan(dec_e5m2(w)), ref_nan(dec_e5m2(w >> 8)),
+                            ref_nan(dec_e5m2(w >> 16)), ref_nan(dec_e5m2(w >> 24)));
         } else {
             const uint2 w = __ldcs(reinterpret_cast<const uint2*>(codes) + g);
-            v = make_float4(dec_f16(w.x), dec_f16(w.x >> 16), dec_f16(w.y), dec_f16(w.y >> 16));
+            v = make_float4(ref_nan(dec_f16(w.x)), ref_nan(dec_f16(w.x >> 16)),
+                            ref_nan(dec_f16(w.y)), ref_nan(dec_f16(w.y >> 16)));
         }
         __stcs(reinterpret_cast<float4*>(out) + g, v);
     }
     if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
         const int64_t i = (ngroups << 2) + threadIdx.x;
-        out[i] = MB == 2 ? dec_e5m2(reinterpret_cast<const uint8_t*>(codes)[i])
-                         : dec_f16(reinterpret_cast<const uint16_t*>(codes)[i]);
+        out[i] = ref_nan(MB == 2 ? dec_e5m2(reinterpret_cast<const uint8_t*>(codes)[i])
+                                 : dec_f16(reinterpret_cast<const uint16_t*>(codes)[i]));
     }
 }
 

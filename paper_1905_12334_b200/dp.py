@@ -1,0 +1,117 @@
+"""Multi-GPU plumbing for the FP8 training primitives.
+
+* ``block_shard``: contiguous ranges of whole 4096-element blocks per rank, with
+  the ``block_offset`` that makes each rank's stochastic-rounding stream the
+  slice of the single-GPU stream (the reference's schedule-independence
+  contract, tensor.hpp:55-58). Quantize / update shard with no collective.
+* ``DataParallelDense``: a Dense layer trained data-parallel. Each rank runs the
+  forward, Q(e), bprop and a *FP32* wgrad on its batch shard; the FP32 partial
+  dW are summed with one all-reduce (NCCL over NVLink on B200, gloo in the CPU
+  tests) **before** the single Q(dW) node, matching the reference's one Q node
+  on the full-batch sum (nn.cpp:302-303; only the FP32 summation order
+  differs). The overflow counters are all-reduced too, so every rank skips the
+  update together (nn.cpp:546), and every rank applies the identical update to
+  its replica of the FP16 masters.
+
+The arithmetic goes through an ``ops`` object; the default is this library's
+CUDA kernels (``GpuOps``). Tests substitute a CPU implementation to cover the
+multi-process orchestration with world_size 2 over gloo.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+BLOCK = 4096
+
+
+def block_shard(n: int, world: int, rank: int, block: int = BLOCK):
+    """(start, end, block_offset) of rank's share of n elements, whole blocks."""
+    nblocks = (n + block - 1) // block
+    per = (nblocks + world - 1) // world
+    b0 = min(rank * per, nblocks)
+    b1 = min(b0 + per, nblocks)
+    return min(b0 * block, n), min(b1 * block, n), b0
+
+
+class GpuOps:
+    """The hot path on this library's kernels (tensors on the current CUDA device)."""
+
+    def __init__(self, engine: str = "tensor"):
+        from . import Counters, gemm_codes, quantize, sgd_momentum_update
+        self._q, self._g, self._u, self._C = quantize, gemm_codes, sgd_momentum_update, Counters
+        self.engine = engine
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def counters(self):
+        return self._C(self.device)
+
+    @staticmethod
+    def ctensor(c):
+        return c.t
+
+    def quantize(self, x, fmt="fp8", mode="nearest-even", seed=1, block_offset=0, counters=None):
+        return self._q(x, fmt, mode, seed, block_offset=block_offset, counters=counters).codes
+
+    def gemm_f32(self, a, b, m, n, k, a_major="k", b_major="n"):
+        c, _ = self._g(a, b, m, n, k, "fp8", a_major=a_major, b_major=b_major, engine=self.engine)
+        return c
+
+    def gemm_q(self, a, b, m, n, k, a_major="k", b_major="n", counters=None):
+        _, cq = self._g(a, b, m, n, k, "fp8", a_major=a_major, b_major=b_major,
+                        engine=self.engine, want_c=False, out_fmt="fp8", out_counters=counters)
+        return cq
+
+    def update(self, qdw, master, momentum, *, lr, mu, two_lambda, scaler, skip_counters,
+               master_mode, seed, w_e5m2=None):
+        self._u(qdw, "fp8", master, momentum, lr=lr, mu=mu, two_lambda=two_lambda,
+                scaler=scaler, skip_counters=skip_counters, master_mode=master_mode, seed=seed,
+                w_e5m2=w_e5m2)
+
+
+class DataParallelDense:
+    """Batch-sharded Dense layer; weights [in, out] replicated on every rank."""
+
+    def __init__(self, w_master, w_q, *, batch_per_rank: int, lr: float, mu: float,
+                 two_lambda: float = 0.0, scaler=None, ops=None, group=None,
+                 master_mode: str = "nearest-even", seed: int = 1):
+        self.ops = ops or GpuOps()
+        self.group = group
+        self.w_master = w_master            # FP16 codes [in, out]
+        self.w_q = w_q                      # E5M2 codes [in, out]: Q(decode(master))
+        self.in_f, self.out_f = w_master.shape
+        self.momentum = torch.zeros(self.in_f, self.out_f, dtype=torch.float32,
+                                    device=w_master.device)
+        self.bpr = batch_per_rank
+        self.lr, self.mu, self.two_lambda = lr, mu, two_lambda
+        self.scaler = scaler
+        self.master_mode, self.seed = master_mode, seed
+
+    def step(self, x_local, e_local, iteration: int):
+        """One DP training step; returns (qy_local, qdx_local, gate counters)."""
+        B, I, O = self.bpr, self.in_f, self.out_f
+        ops = self.ops
+        fwd = ops.counters()
+        bwd = ops.counters()
+        qx = ops.quantize(x_local.reshape(-1), counters=fwd)
+        qy = ops.gemm_q(qx, self.w_q, B, O, I, "k", "n", counters=fwd)
+        qe = ops.quantize(e_local.reshape(-1), counters=bwd)
+        # FP32 partial dW on this rank's rows, summed across ranks before Q(dW)
+        dw = ops.gemm_f32(qx, qe, I, O, B, "m", "n")
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(dw, op=dist.ReduceOp.SUM, group=self.group)
+        qdx = ops.gemm_q(qe, self.w_q, B, I, O, "k", "k", counters=bwd)
+        qdw = ops.quantize(dw.reshape(-1), counters=bwd)
+        gate = ops.ctensor(bwd)
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            # every rank must agree on grads_finite (nn.cpp:401-411, 546)
+            dist.all_reduce(gate, op=dist.ReduceOp.SUM, group=self.group)
+        ops.update(qdw, self.w_master.reshape(-1), self.momentum.reshape(-1), lr=self.lr,
+                   mu=self.mu, two_lambda=self.two_lambda, scaler=self.scaler,
+                   skip_counters=bwd, master_mode=self.master_mode, seed=self.seed,
+                   w_e5m2=self.w_q.reshape(-1))
+        if self.scaler is not None and hasattr(self.scaler, "step_async"):
+            self.scaler.step_async(True, iteration, counters=bwd)
+        return qy, qdx, gate

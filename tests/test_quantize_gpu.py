@@ -156,9 +156,8 @@ def test_dequantize_all_codes(fp8, fmt):
     q = fp8.QuantizedTensor(codes, [ncodes], 0 if fmt == "fp8" else 1, 0, fp8.Counters())
     got = fp8.dequantize(q).cpu().numpy()
     want = O.dequantize(np.arange(ncodes, dtype=np.uint16), fmt)
-    nanm = np.isnan(want)
-    assert (np.isnan(got) == nanm).all()
-    np.testing.assert_array_equal(got[~nanm].view(np.uint32), want[~nanm].view(np.uint32))
+    # bitwise, NaN included: every NaN code decodes to the reference's 0x7FC00000
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
 def test_roundtrip_all_finite_codes(fp8):

@@ -306,24 +306,28 @@ struct BlockScan {
         if (BAR == 0) __syncthreads();
         else asm volatile("bar.sync %0, 256;" ::"r"(BAR) : "memory");
         const uint32_t excl = inc - packed;
-        // warp offsets per round and round totals
-        uint32_t before[4] = {0, 0, 0, 0}, total[4] = {0, 0, 0, 0};
+        // Cross-warp part, warp-cooperative: lanes 0..7 hold the 8 warp totals,
+        // split into 16-bit fields (rounds 0,2 in lo; 1,3 in hi) and scanned
+        // with three shuffles; every warp does it redundantly (no 2nd barrier).
+        const uint32_t tw = smem_w[lane & 7];
+        uint32_t lo = tw & 0x00FF00FFu, hi = (tw >> 8) & 0x00FF00FFu;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint32_t t = smem_w[i];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const uint32_t c = (t >> (8 * r)) & 0xFFu;
-                total[r] += c;
-                if (i < w) before[r] += c;
-            }
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t tl = __shfl_up_sync(0xffffffffu, lo, o);
+            const uint32_t th = __shfl_up_sync(0xffffffffu, hi, o);
+            if ((lane & 7) >= o) { lo += tl; hi += th; }
         }
-        uint32_t run_total = 0;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            pre[r] = run_total + before[r] + ((excl >> (8 * r)) & 0xFFu);
-            run_total += total[r];
-        }
+        // inclusive over warps 0..7 -> totals (lane 7) and this warp's exclusive prefix
+        const uint32_t tot_lo = __shfl_sync(0xffffffffu, lo, 7);
+        const uint32_t tot_hi = __shfl_sync(0xffffffffu, hi, 7);
+        uint32_t bef_lo = __shfl_sync(0xffffffffu, lo, (w + 7) & 7);
+        uint32_t bef_hi = __shfl_sync(0xffffffffu, hi, (w + 7) & 7);
+        if (w == 0) { bef_lo = 0; bef_hi = 0; }
+        const uint32_t t0 = tot_lo & 0xFFFFu, t1 = tot_hi & 0xFFFFu, t2 = tot_lo >> 16;
+        pre[0] = (bef_lo & 0xFFFFu) + (excl & 0xFFu);
+        pre[1] = t0 + (bef_hi & 0xFFFFu) + ((excl >> 8) & 0xFFu);
+        pre[2] = t0 + t1 + (bef_lo >> 16) + ((excl >> 16) & 0xFFu);
+        pre[3] = t0 + t1 + t2 + (bef_hi >> 16) + (excl >> 24);
     }
 };
 

@@ -202,13 +202,14 @@ __global__ void __launch_bounds__(256 * kLfsrGroups, 1)
     __shared__ __align__(8) uint64_t full[NG][S];
     __shared__ __align__(8) uint64_t tab_bar;
     __shared__ uint32_t smem_w[NG][2][8];
+    __shared__ uint32_t p0s[NG][2];  // stream start of the group's current / next block
     const bool sat = saturate != 0;
     const uint32_t special = special_packed<MB>(sat);
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int g = threadIdx.x >> 8, t = threadIdx.x & 255;
     uint8_t* ring = smem + kTabBytesPad + g * S * kBlock * 4;
     const int64_t gid = (int64_t)blockIdx.x * NG + g, gstride = (int64_t)gridDim.x * NG;
-    const int64_t nmine = nfull > gid ? (nfull - 1 - gid) / gstride + 1 : 0;
+    const int nmine = nfull > gid ? (int)((nfull - 1 - gid) / gstride + 1) : 0;
     if (threadIdx.x == 0) {
         mbar_init(&tab_bar, 1);
         for (int gg = 0; gg < NG; ++gg)
@@ -220,21 +221,20 @@ __global__ void __launch_bounds__(256 * kLfsrGroups, 1)
     }
     __syncthreads();
     if (t == 0) {
-        for (int64_t i = 0; i < S - 1 && i < nmine; ++i) {
+        for (int i = 0; i < S - 1 && i < nmine; ++i) {
             const int64_t b = gid + i * gstride;
             mbar_expect_tx(&full[g][i], kBlock * 4);
             bulk_g2s(ring + i * kBlock * 4, x + b * kBlock, kBlock * 4, &full[g][i]);
         }
     }
     const uint32_t stab_addr = smem_addr(stab);
-    uint32_t p0_next = nmine > 0 ? __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + gid))) : 0;
+    // one thread per group derives LfsrStream::split(seed, block) (a SplitMix64
+    // chain + a jump-table lookup) and publishes it through shared memory
+    if (t == 0 && nmine > 0) p0s[g][0] = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + gid)));
     mbar_wait(&tab_bar, 0);
-    for (int64_t i = 0; i < nmine; ++i) {
-        const int s = (int)(i % S);
-        const int64_t b = gid + i * gstride;
-        const uint32_t p0 = p0_next;
-        if (i + 1 < nmine)  // the next block's stream start, off the critical path
-            p0_next = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b + gstride)));
+    for (int i = 0; i < nmine; ++i) {
+        const int s = i % S;
+        const int64_t b = gid + (int64_t)i * gstride;
         mbar_wait(&full[g][s], (uint32_t)((i / S) & 1));
         const float4* blk = reinterpret_cast<const float4*>(ring + s * kBlock * 4);
         uint32_t P[4][4], inc[4][4], cnt[4];
@@ -257,10 +257,11 @@ __global__ void __launch_bounds__(256 * kLfsrGroups, 1)
         if (NG == 1) BlockScan<MB, 0>::run_counts(cnt, pre, smem_w[g][i & 1]);
         else if (g == 0) BlockScan<MB, 1>::run_counts(cnt, pre, smem_w[g][i & 1]);
         else BlockScan<MB, 2>::run_counts(cnt, pre, smem_w[g][i & 1]);
+        const uint32_t p0 = p0s[g][i & 1];
         // every thread of the group is past block i-1: refill its stage with block i-1+S
         if (t == 0 && i + S - 1 < nmine) {
-            const int sn = (int)((i + S - 1) % S);
-            const int64_t bn = gid + (i + S - 1) * gstride;
+            const int sn = (i + S - 1) % S;
+            const int64_t bn = gid + (int64_t)(i + S - 1) * gstride;
             mbar_expect_tx(&full[g][sn], kBlock * 4);
             bulk_g2s(ring + sn * kBlock * 4, x + bn * kBlock, kBlock * 4, &full[g][sn]);
         }
@@ -309,6 +310,8 @@ __global__ void __launch_bounds__(256 * kLfsrGroups, 1)
                                   gather_f16(sum[2], sum[3], u[2], u[3])));
             }
         }
+        if (t == 0 && i + 1 < nmine)  // next block's stream start, read after the next barrier
+            p0s[g][(i + 1) & 1] = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b + gstride)));
         // rare: a NaN (or Inf) among this thread's 16 inputs -> rewrite NaN codes
         // as the canonical unsigned NaN (float_format.cpp:99) and count them
         if (nanacc != nanacc) {

@@ -11,6 +11,8 @@
 //                        is its rank among the block's inexact elements (a
 //                        CTA-wide exclusive scan), and the sample itself is a
 //                        lookup in the decimated-cycle table.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -187,8 +189,8 @@ __device__ __forceinline__ void store4(void* codes, int64_t i0, const uint32_t (
 // so the groups' barrier waits overlap.
 // Phase 1 (per element): overflow/NaN screen, packed value P, inexact flag ->
 // stream increment. Scan. Phase 2: sample, code = (P + r16) >> 16.
-constexpr int kLfsrStages = 3;
-constexpr int kLfsrGroups = 2;
+constexpr int kLfsrStages = 2;
+constexpr int kLfsrGroups = 3;
 constexpr int kTabBytesPad = 65536 * 2;  // 65535 entries, no wrap extension
 constexpr int kLfsrSmem = kTabBytesPad + kLfsrGroups * kLfsrStages * kBlock * 4;
 template <int MB>
@@ -256,7 +258,8 @@ __global__ void __launch_bounds__(256 * kLfsrGroups, 1)
         uint32_t pre[4];
         if (NG == 1) BlockScan<MB, 0>::run_counts(cnt, pre, smem_w[g][i & 1]);
         else if (g == 0) BlockScan<MB, 1>::run_counts(cnt, pre, smem_w[g][i & 1]);
-        else BlockScan<MB, 2>::run_counts(cnt, pre, smem_w[g][i & 1]);
+        else if (g == 1) BlockScan<MB, 2>::run_counts(cnt, pre, smem_w[g][i & 1]);
+        else BlockScan<MB, 3>::run_counts(cnt, pre, smem_w[g][i & 1]);
         const uint32_t p0 = p0s[g][i & 1];
         // every thread of the group is past block i-1: refill its stage with block i-1+S
         if (t == 0 && i + S - 1 < nmine) {
@@ -268,48 +271,52 @@ __global__ void __launch_bounds__(256 * kLfsrGroups, 1)
         // blocks whose stream window crosses the end of the 65535-cycle wrap
         // (p0 > 61439: ~6% of blocks) take the modular addressing path
         const bool wraps = p0 + kBlock > (uint32_t)kLfsrPeriod;
+        auto phase2 = [&](auto wrap_tag) {
+            constexpr bool WRAP = decltype(wrap_tag)::value;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            uint32_t sum[4];
-            if (!wraps) {
-                uint32_t addr = stab_addr + 2u * (p0 + pre[r]);
+            for (int r = 0; r < 4; ++r) {
+                uint32_t sum[4];
+                if (!WRAP) {
+                    uint32_t addr = stab_addr + 2u * (p0 + pre[r]);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        uint32_t r16;
+                        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r16) : "r"(addr));
+                        addr += inc[r][k];
+                        sum[k] = P[r][k] + r16;  // exact lanes ignore their sample
+                    }
+                } else {
+                    uint32_t j = p0 + pre[r];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t jj = j >= (uint32_t)kLfsrPeriod ? j - kLfsrPeriod : j;
+                        const uint32_t r16 = stab[jj];
+                        j += inc[r][k] >> 1;
+                        sum[k] = P[r][k] + r16;
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    uint32_t r16;
-                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r16) : "r"(addr));
-                    addr += inc[r][k];
-                    sum[k] = P[r][k] + r16;  // exact lanes ignore their sample
+                    // underflow: inexact and rounded to zero; exact lanes pushed out of range
+                    const uint32_t chk = sum[k] + (2u - inc[r][k]) * 0x8000u;
+                    c_unf += (chk - 0x10000u) >> 31;
                 }
-            } else {
-                uint32_t j = p0 + pre[r];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t jj = j >= (uint32_t)kLfsrPeriod ? j - kLfsrPeriod : j;
-                    const uint32_t r16 = stab[jj];
-                    j += inc[r][k] >> 1;
-                    sum[k] = P[r][k] + r16;
+                const float4 v = blk[256 * r + t];
+                const uint32_t u[4] = {__float_as_uint(v.x), __float_as_uint(v.y),
+                                       __float_as_uint(v.z), __float_as_uint(v.w)};
+                const int64_t q = b * (kBlock / 4) + 256 * r + t;  // float4 group index
+                if (MB == 2) {
+                    __stcs(reinterpret_cast<uint32_t*>(codes) + q,
+                           gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]));
+                } else {
+                    __stcs(reinterpret_cast<uint2*>(codes) + q,
+                           make_uint2(gather_f16(sum[0], sum[1], u[0], u[1]),
+                                      gather_f16(sum[2], sum[3], u[2], u[3])));
                 }
             }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                // underflow: inexact and rounded to zero; exact lanes are pushed out of range
-                const uint32_t chk = sum[k] + (2u - inc[r][k]) * 0x8000u;
-                c_unf += (chk - 0x10000u) >> 31;
-            }
-            const float4 v = blk[256 * r + t];
-            const float f[4] = {v.x, v.y, v.z, v.w};
-            const uint32_t u[4] = {__float_as_uint(f[0]), __float_as_uint(f[1]),
-                                   __float_as_uint(f[2]), __float_as_uint(f[3])};
-            const int64_t q = b * (kBlock / 4) + 256 * r + t;  // float4 group index
-            if (MB == 2) {
-                __stcs(reinterpret_cast<uint32_t*>(codes) + q,
-                       gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]));
-            } else {
-                __stcs(reinterpret_cast<uint2*>(codes) + q,
-                       make_uint2(gather_f16(sum[0], sum[1], u[0], u[1]),
-                                  gather_f16(sum[2], sum[3], u[2], u[3])));
-            }
-        }
+        };
+        if (!wraps) phase2(std::false_type{});
+        else phase2(std::true_type{});
         if (t == 0 && i + 1 < nmine)  // next block's stream start, read after the next barrier
             p0s[g][(i + 1) & 1] = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b + gstride)));
         // rare: a NaN (or Inf) among this thread's 16 inputs -> rewrite NaN codes

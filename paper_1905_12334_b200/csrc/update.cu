@@ -120,7 +120,7 @@ __device__ __forceinline__ void master4(const float (&w)[4], uint64_t word, cons
 }
 
 // Position-independent master rounding, 8 parameters per thread per iteration.
-template <int GFMT, int MODE, int NT>
+template <int GFMT, int MODE, int NT, bool CNT>
 __global__ void __launch_bounds__(NT) sgd_elem_kernel(const void* __restrict__ grad,
                                                       uint16_t* __restrict__ master,
                                                       float* __restrict__ mom, int64_t n,
@@ -182,8 +182,9 @@ __global__ void __launch_bounds__(NT) sgd_elem_kernel(const void* __restrict__ g
         mom[i] = m;
         if (a.w8) a.w8[i] = (uint8_t)w8_code1(c, wsat, wb, wn, wu);
     }
-    if (a.mcnt) flush_counters<NT>(mb - mn, mu_, mn, a.mcnt);
-    if (a.wcnt) flush_counters<NT>(wb - wn, wu, wn, a.wcnt);
+    // counters are dead code (and compiled out) unless the caller asked for them
+    if (CNT && a.mcnt) flush_counters<NT>(mb - mn, mu_, mn, a.mcnt);
+    if (CNT && a.wcnt) flush_counters<NT>(wb - wn, wu, wn, a.wcnt);
 }
 
 // Reference-stream SR master: quantize(Tensor(w32), kFp16, {Stochastic, seed})
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(NT) sgd_elem_kernel(const void* __restrict__ g
 // phase 1 computes w32 (kept in the ring, over the momentum it consumed) and
 // the inexact flags, phase 2 rounds with the block's LFSR samples.
 constexpr int kUpdStages = 3;
-template <int GFMT>
+template <int GFMT, bool CNT>
 __global__ void __launch_bounds__(256) sgd_lfsr_staged_kernel(const void* __restrict__ grad,
                                                               uint16_t* __restrict__ master,
                                                               float* __restrict__ mom,
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(256) sgd_lfsr_staged_kernel(const void* __rest
     extern __shared__ __align__(128) uint8_t ring[];
     __shared__ __align__(8) uint64_t full[S];
     __shared__ uint32_t smem_w[2][8];
+    __shared__ uint32_t p0s[2];
     if (upd_skipped(a)) return;
     const Unscale us(upd_scale(a));
     const bool wsat = a.w_sat != 0;
@@ -229,8 +231,10 @@ __global__ void __launch_bounds__(256) sgd_lfsr_staged_kernel(const void* __rest
         bulk_g2s(st + GB, master + b * kBlock, MB_, full + s);
         bulk_g2s(st + GB + MB_, mom + b * kBlock, VB, full + s);
     };
-    if (t == 0)
+    if (t == 0) {
         for (int64_t i = 0; i < S - 1 && i < nmine; ++i) issue(i);
+        if (nmine > 0) p0s[0] = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + blockIdx.x)));
+    }
     for (int64_t i = 0; i < nmine; ++i) {
         const int s = (int)(i % S);
         const int64_t b = blockIdx.x + i * gridDim.x;
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(256) sgd_lfsr_staged_kernel(const void* __rest
         uint32_t pre[4];
         BlockScan<10>::run(mask, pre, smem_w[i & 1]);
         if (t == 0 && i + S - 1 < nmine) issue(i + S - 1);
-        const uint32_t p0 = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + b)));
+        const uint32_t p0 = p0s[i & 1];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int q = 256 * r + t;
@@ -292,9 +296,11 @@ __global__ void __launch_bounds__(256) sgd_lfsr_staged_kernel(const void* __rest
                 __stcs(reinterpret_cast<uint32_t*>(a.w8) + b * (kBlock / 4) + q,
                        w8_pack4(out, wsat, wb, wn, wu));
         }
+        if (t == 0 && i + 1 < nmine)  // next block's stream start, read after the next barrier
+            p0s[(i + 1) & 1] = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + b + gridDim.x)));
     }
-    if (a.mcnt) flush_counters<256>(mb - mn, mu_, mn, a.mcnt);
-    if (a.wcnt) flush_counters<256>(wb - wn, wu, wn, a.wcnt);
+    if (CNT && a.mcnt) flush_counters<256>(mb - mn, mu_, mn, a.mcnt);
+    if (CNT && a.wcnt) flush_counters<256>(wb - wn, wu, wn, a.wcnt);
 }
 
 // Tail / unaligned variant: blocks [block_begin, nblocks) with scalar accesses.
@@ -425,6 +431,7 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     a.mcnt = args.master_counters; a.w8 = args.w_e5m2; a.w_sat = args.w_saturate;
     a.wcnt = args.w_counters;
     constexpr int NT = 256;
+    const bool cnt = a.mcnt != nullptr || a.wcnt != nullptr;
     const bool aligned = ((uintptr_t)grad % 16 == 0) && ((uintptr_t)master % 16 == 0) &&
                          ((uintptr_t)mom % 16 == 0) && (a.w8 == nullptr || (uintptr_t)a.w8 % 16 == 0) &&
                          (a.rbits == nullptr || (uintptr_t)a.rbits % 16 == 0);
@@ -434,12 +441,8 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
         if (aligned && n / kBlock > 0) {
             const int64_t nfull = n / kBlock;
             constexpr int smem = kUpdStages * kBlock * (grad_bytes<GFMT>() + 2 + 4);
-            auto fn = sgd_lfsr_staged_kernel<GFMT>;
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                attr = true;
-            }
+            auto fn = cnt ? sgd_lfsr_staged_kernel<GFMT, true> : sgd_lfsr_staged_kernel<GFMT, false>;
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             int per_sm = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
             int64_t g = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
@@ -460,12 +463,16 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     int64_t g = (int64_t)sm_count() * 8;
     const int64_t need = ((aligned ? n / 8 : n) + NT - 1) / NT;
     if (need < g) g = need < 1 ? 1 : need;
-    if (args.master_mode == FP8B_RNE)
-        sgd_elem_kernel<GFMT, 0, NT><<<(int)g, NT, 0, st>>>(grad, master, mom, n, a, aligned ? 1 : 0);
-    else if (args.bits == FP8B_BITS_COUNTER)
-        sgd_elem_kernel<GFMT, 1, NT><<<(int)g, NT, 0, st>>>(grad, master, mom, n, a, aligned ? 1 : 0);
-    else
-        sgd_elem_kernel<GFMT, 2, NT><<<(int)g, NT, 0, st>>>(grad, master, mom, n, a, aligned ? 1 : 0);
+    const int al = aligned ? 1 : 0;
+#define FP8B_SGD(MODE)                                                                              \
+    {                                                                                               \
+        if (cnt) sgd_elem_kernel<GFMT, MODE, NT, true><<<(int)g, NT, 0, st>>>(grad, master, mom, n, a, al); \
+        else sgd_elem_kernel<GFMT, MODE, NT, false><<<(int)g, NT, 0, st>>>(grad, master, mom, n, a, al);   \
+    }
+    if (args.master_mode == FP8B_RNE) FP8B_SGD(0)
+    else if (args.bits == FP8B_BITS_COUNTER) FP8B_SGD(1)
+    else FP8B_SGD(2)
+#undef FP8B_SGD
 }
 
 void launch_sgd(const void* grad, int grad_fmt, uint16_t* master, float* mom, int64_t n,

@@ -207,6 +207,40 @@ int fp8b_sgd_momentum_update(const void *grad, int32_t grad_fmt, uint16_t *maste
 int fp8b_bias_grad(const void *e_codes, int32_t fmt, int64_t rows, int64_t cols, float *db,
                    void *stream);
 
+/* -------------------------------------------------------- convolutions ---- */
+/* The conv family of kernels.hpp:13-50. Layout FP8B_NCHW is the reference's
+ * (x [N,C,H,W], w [F,C,kH,kW], y [N,F,OH,OW]); FP8B_NHWC is the B200 layout of
+ * BASELINE config 4 (x [N,H,W,C], w [F,kH,kW,C], y [N,OH,OW,F]). Outputs are
+ * FP32 (unquantized, as the reference returns them).
+ * Engines: FP8B_GEMM_SEQUENTIAL reproduces the reference's accumulation order
+ * (fprop (c,kh,kw), dgrad (f,kh,kw), wgrad (n,oh,ow)) bit for bit in either
+ * layout; FP8B_GEMM_TENSOR runs implicit GEMM on tcgen05 (NHWC, E5M2, stride
+ * 1; other cases fall back to the sequential engine) within the GEMM tolerance. */
+enum { FP8B_NCHW = 0, FP8B_NHWC = 1 };
+typedef struct {
+    int64_t n, c, h, w;       /* input batch, channels, height, width */
+    int64_t f, kh, kw;        /* filters and kernel size */
+    int64_t stride, pad;      /* ConvGeometry (kernels.hpp:13-16) */
+    int32_t layout;           /* FP8B_NCHW / FP8B_NHWC */
+    int32_t engine;           /* FP8B_GEMM_TENSOR / FP8B_GEMM_SEQUENTIAL */
+} fp8b_conv_t;
+
+/* conv2d_fp8 (kernels.hpp:22-23): y = x * w */
+int fp8b_conv2d_fprop(const void *x, const void *w, float *y, int32_t fmt, const fp8b_conv_t *g,
+                      void *stream);
+/* conv2d_backward_data_fp8 (kernels.hpp:39-41): dx from e [N,F,OH,OW] and w */
+int fp8b_conv2d_dgrad(const void *e, const void *w, float *dx, int32_t fmt,
+                      const fp8b_conv_t *g, void *stream);
+/* conv2d_backward_weights_fp8 (kernels.hpp:46-48): dw from x and e */
+int fp8b_conv2d_wgrad(const void *x, const void *e, float *dw, int32_t fmt,
+                      const fp8b_conv_t *g, void *stream);
+
+/* im2col (kernels.hpp:25-30): pure code movement, zero code for padded taps.
+ * FP8B_NCHW gives the reference's patch matrix [C*kH*kW, N*OH*OW] (rows
+ * (c,kh,kw), cols (n,oh,ow)); FP8B_NHWC gives its transpose in the NHWC tap
+ * order, [N*OH*OW, kH*kW*C] (K-major A operand of fp8b_gemm). */
+int fp8b_im2col(const void *x, void *cols, int32_t fmt, const fp8b_conv_t *g, void *stream);
+
 /* ---------------------------------------------------------- layer step ---- */
 /* One quantized Dense-layer training step on device, the composition
  * Network::forward -> backward -> apply_update -> LossScaler::step performs for a

@@ -83,6 +83,10 @@ def _load_oracle():
                                   _P(np.float32, flags="C"), _i64, C.c_float, C.c_float,
                                   C.c_float, C.c_float, C.c_int, C.c_int, _u64, _i64,
                                   C.c_void_p, C.c_void_p, _P(np.int64, flags="C")]
+    for fn in ("or_conv2d", "or_conv2d_dgrad", "or_conv2d_wgrad"):
+        getattr(lib, fn).restype = None
+        getattr(lib, fn).argtypes = [_P(np.uint16, flags="C"), _P(np.uint16, flags="C")] + \
+            [_i64] * 9 + [C.c_int, _P(np.float32, flags="C")]
     lib.or_bias_grad.restype = None
     lib.or_bias_grad.argtypes = [_P(np.float32, flags="C"), _i64, _i64,
                                  _P(np.float32, flags="C")]
@@ -152,6 +156,9 @@ def ref():
         r.ref_gemm_mt.restype = C.c_int
         r.ref_gemm_mt.argtypes = [_P(np.uint16, flags="C"), _P(np.uint16, flags="C"), _i64,
                                   _i64, _i64, C.c_int, _P(np.float32, flags="C"), C.c_int]
+        r.ref_conv.restype = C.c_int
+        r.ref_conv.argtypes = [C.c_int, _P(np.uint16, flags="C"), _P(np.uint16, flags="C")] + \
+            [_i64] * 9 + [C.c_int, _P(np.float32, flags="C")]
         r.ref_scaler_new.restype = C.c_void_p
         r.ref_scaler_new.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, _i64,
                                      C.c_int, C.c_void_p, C.c_void_p]
@@ -238,6 +245,37 @@ def gemm_exact(a_codes, b_codes, m, k, n, fmt="fp8"):
     d = np.zeros(m * n, dtype=np.float64)
     lib().or_gemm_exact(a, b, m, k, n, FMT[fmt], c, d)
     return c.reshape(m, n), d.reshape(m, n)
+
+
+def conv_out(n, k, s, p):
+    return (n + 2 * p - k) // s + 1
+
+
+def conv2d(x_codes, w_codes, n, c, h, w, f, kh, kw, stride=1, pad=0, fmt="fp8", kind="fprop"):
+    """Oracle conv family in NCHW / [F,C,kh,kw] (kernels.cpp:106-253).
+    kind fprop: (x, w) -> y [N,F,OH,OW]; dgrad: (e, w) -> dx [N,C,H,W];
+    wgrad: (x, e) -> dw [F,C,kh,kw]."""
+    oh, ow = conv_out(h, kh, stride, pad), conv_out(w, kw, stride, pad)
+    a = np.ascontiguousarray(x_codes, dtype=np.uint16).reshape(-1)
+    b = np.ascontiguousarray(w_codes, dtype=np.uint16).reshape(-1)
+    shape = {"fprop": (n, f, oh, ow), "dgrad": (n, c, h, w), "wgrad": (f, c, kh, kw)}[kind]
+    out = np.zeros(int(np.prod(shape)), dtype=np.float32)
+    fn = {"fprop": lib().or_conv2d, "dgrad": lib().or_conv2d_dgrad, "wgrad": lib().or_conv2d_wgrad}[kind]
+    fn(a, b, n, c, h, w, f, kh, kw, stride, pad, FMT[fmt], out)
+    return out.reshape(shape)
+
+
+def ref_conv2d(a_codes, b_codes, n, c, h, w, f, kh, kw, stride=1, pad=0, fmt="fp8", kind="fprop"):
+    oh, ow = conv_out(h, kh, stride, pad), conv_out(w, kw, stride, pad)
+    a = np.ascontiguousarray(a_codes, dtype=np.uint16).reshape(-1)
+    b = np.ascontiguousarray(b_codes, dtype=np.uint16).reshape(-1)
+    shape = {"fprop": (n, f, oh, ow), "dgrad": (n, c, h, w), "wgrad": (f, c, kh, kw)}[kind]
+    out = np.zeros(int(np.prod(shape)), dtype=np.float32)
+    rc = ref().ref_conv({"fprop": 0, "dgrad": 1, "wgrad": 2}[kind], a, b, n, c, h, w, f, kh, kw,
+                        stride, pad, FMT[fmt], out)
+    if rc != 0:
+        raise ValueError("convolution geometry does not fit input")
+    return out.reshape(shape)
 
 
 def sgd_update(master, momentum, g, scale, lr, mu, two_lambda=0.0, master_mode="nearest-even",

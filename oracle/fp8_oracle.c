@@ -258,6 +258,79 @@ void or_gemm(const uint16_t *a, const uint16_t *b, int64_t m, int64_t k,
     free(db);
 }
 
+static int64_t conv_out(int64_t in, int64_t k, int64_t s, int64_t p) { return (in + 2 * p - k) / s + 1; }
+
+/* kernels.cpp:106-151 */
+void or_conv2d(const uint16_t *x, const uint16_t *w, int64_t n, int64_t c, int64_t h,
+               int64_t wd, int64_t f, int64_t kh, int64_t kw, int64_t stride, int64_t pad,
+               int fmt, float *y) {
+    const int64_t oh = conv_out(h, kh, stride, pad), ow = conv_out(wd, kw, stride, pad);
+    for (int64_t ni = 0; ni < n; ++ni)
+        for (int64_t fi = 0; fi < f; ++fi)
+            for (int64_t oi = 0; oi < oh; ++oi)
+                for (int64_t oj = 0; oj < ow; ++oj) {
+                    float acc = 0.0f;
+                    for (int64_t ci = 0; ci < c; ++ci)
+                        for (int64_t ki = 0; ki < kh; ++ki) {
+                            const int64_t ii = oi * stride - pad + ki;
+                            for (int64_t kj = 0; kj < kw; ++kj) {
+                                const int64_t jj = oj * stride - pad + kj;
+                                float xv = 0.0f;
+                                if (ii >= 0 && ii < h && jj >= 0 && jj < wd)
+                                    xv = (float)or_decode(x[((ni * c + ci) * h + ii) * wd + jj], fmt);
+                                acc += xv * (float)or_decode(w[((fi * c + ci) * kh + ki) * kw + kj], fmt);
+                            }
+                        }
+                    y[((ni * f + fi) * oh + oi) * ow + oj] = acc;
+                }
+}
+
+/* kernels.cpp:153-205 */
+void or_conv2d_dgrad(const uint16_t *e, const uint16_t *w, int64_t n, int64_t c, int64_t h,
+                     int64_t wd, int64_t f, int64_t kh, int64_t kw, int64_t stride,
+                     int64_t pad, int fmt, float *dx) {
+    const int64_t oh = conv_out(h, kh, stride, pad), ow = conv_out(wd, kw, stride, pad);
+    for (int64_t ni = 0; ni < n; ++ni)
+        for (int64_t ci = 0; ci < c; ++ci)
+            for (int64_t i = 0; i < h; ++i)
+                for (int64_t j = 0; j < wd; ++j) {
+                    float acc = 0.0f;
+                    for (int64_t fi = 0; fi < f; ++fi)
+                        for (int64_t ki = 0; ki < kh; ++ki)
+                            for (int64_t kj = 0; kj < kw; ++kj) {
+                                const int64_t on = i + pad - ki, pn = j + pad - kj;
+                                if (on % stride || pn % stride) continue;
+                                const int64_t oi = on / stride, oj = pn / stride;
+                                if (oi < 0 || oi >= oh || oj < 0 || oj >= ow) continue;
+                                acc += (float)or_decode(w[((fi * c + ci) * kh + ki) * kw + kj], fmt) *
+                                       (float)or_decode(e[((ni * f + fi) * oh + oi) * ow + oj], fmt);
+                            }
+                    dx[((ni * c + ci) * h + i) * wd + j] = acc;
+                }
+}
+
+/* kernels.cpp:207-253 */
+void or_conv2d_wgrad(const uint16_t *x, const uint16_t *e, int64_t n, int64_t c, int64_t h,
+                     int64_t wd, int64_t f, int64_t kh, int64_t kw, int64_t stride,
+                     int64_t pad, int fmt, float *dw) {
+    const int64_t oh = conv_out(h, kh, stride, pad), ow = conv_out(wd, kw, stride, pad);
+    for (int64_t fi = 0; fi < f; ++fi)
+        for (int64_t ci = 0; ci < c; ++ci)
+            for (int64_t ki = 0; ki < kh; ++ki)
+                for (int64_t kj = 0; kj < kw; ++kj) {
+                    float acc = 0.0f;
+                    for (int64_t ni = 0; ni < n; ++ni)
+                        for (int64_t oi = 0; oi < oh; ++oi)
+                            for (int64_t oj = 0; oj < ow; ++oj) {
+                                const int64_t ii = oi * stride - pad + ki, jj = oj * stride - pad + kj;
+                                if (ii < 0 || ii >= h || jj < 0 || jj >= wd) continue;
+                                acc += (float)or_decode(x[((ni * c + ci) * h + ii) * wd + jj], fmt) *
+                                       (float)or_decode(e[((ni * f + fi) * oh + oi) * ow + oj], fmt);
+                            }
+                    dw[((fi * c + ci) * kh + ki) * kw + kj] = acc;
+                }
+}
+
 void or_gemm_exact(const uint16_t *a, const uint16_t *b, int64_t m, int64_t k,
                    int64_t n, int fmt, double *c_exact, double *c_absdot) {
     for (int64_t i = 0; i < m; ++i)

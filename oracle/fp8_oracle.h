@@ -56,6 +56,19 @@ void or_dequantize(const uint16_t *codes, int64_t n, int fmt, float *out);
 void or_gemm(const uint16_t *a, const uint16_t *b, int64_t m, int64_t k,
              int64_t n, int fmt, float *c);
 
+/* Convolutions over codes, NCHW / FCkk, FP32 accumulation in the reference's
+ * fixed orders (kernels.cpp:106-253): fprop (c,kh,kw) with explicit zero
+ * products for padded taps; dgrad (f,kh,kw) skipping holes; wgrad (n,oh,ow). */
+void or_conv2d(const uint16_t *x, const uint16_t *w, int64_t n, int64_t c, int64_t h,
+               int64_t wd, int64_t f, int64_t kh, int64_t kw, int64_t stride, int64_t pad,
+               int fmt, float *y);
+void or_conv2d_dgrad(const uint16_t *e, const uint16_t *w, int64_t n, int64_t c, int64_t h,
+                     int64_t wd, int64_t f, int64_t kh, int64_t kw, int64_t stride,
+                     int64_t pad, int fmt, float *dx);
+void or_conv2d_wgrad(const uint16_t *x, const uint16_t *e, int64_t n, int64_t c, int64_t h,
+                     int64_t wd, int64_t f, int64_t kh, int64_t kw, int64_t stride,
+                     int64_t pad, int fmt, float *dw);
+
 /* Exact (long double) sum and sum of |products| for the GEMM tolerance. */
 void or_gemm_exact(const uint16_t *a, const uint16_t *b, int64_t m, int64_t k,
                    int64_t n, int fmt, double *c_exact, double *c_absdot);

@@ -187,6 +187,31 @@ int ref_gemm_mt(const uint16_t* a, const uint16_t* b, int64_t m, int64_t k, int6
     return 0;
 }
 
+// conv family (kernels.hpp:22-50). kind: 0 fprop, 1 dgrad, 2 wgrad.
+int ref_conv(int kind, const uint16_t* a, const uint16_t* b, int64_t n, int64_t c, int64_t h,
+             int64_t wd, int64_t f, int64_t kh, int64_t kw, int64_t stride, int64_t pad, int fmt,
+             float* out) {
+    try {
+        const ConvGeometry g{stride, pad};
+        const int64_t oh = conv_out_dim(h, kh, stride, pad), ow = conv_out_dim(wd, kw, stride, pad);
+        auto qt = [&](const uint16_t* p, std::vector<int64_t> shape) {
+            QuantizedTensor q;
+            q.shape = shape;
+            q.codes.assign(p, p + shape_numel(shape));
+            q.fmt = fmt_of(fmt);
+            return q;
+        };
+        Tensor y;
+        if (kind == 0) y = conv2d_fp8(qt(a, {n, c, h, wd}), qt(b, {f, c, kh, kw}), g);
+        else if (kind == 1) y = conv2d_backward_data_fp8(qt(a, {n, f, oh, ow}), qt(b, {f, c, kh, kw}), g, h, wd);
+        else y = conv2d_backward_weights_fp8(qt(a, {n, c, h, wd}), qt(b, {n, f, oh, ow}), kh, kw, g);
+        std::memcpy(out, y.data.data(), sizeof(float) * y.data.size());
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 22;
+    }
+}
+
 // LossScaler (loss_scaling.hpp:26-68) behind an opaque handle.
 void* ref_scaler_new(int kind, double scale, double backoff, double growth,
                      int64_t interval, int nsched, const int64_t* it, const double* sc) {

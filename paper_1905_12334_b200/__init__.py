@@ -33,6 +33,7 @@ __all__ = [
     "QuantizedTensor", "ScaleEvent", "LossScaler", "quantize", "dequantize", "transpose",
     "gemm", "gemm_codes", "encode", "decode", "sgd_momentum_update", "bias_grad",
     "count_nonfinite", "fill_synthetic", "Counters", "launch_count", "version",
+    "conv2d", "conv2d_backward_data", "conv2d_backward_weights", "im2col", "conv_out_dim",
 ]
 
 _FMT = {"fp8": _lib.E5M2, "FP8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16,
@@ -266,6 +267,123 @@ def gemm(a: QuantizedTensor, b: QuantizedTensor, *, engine: str = "tensor",
     c, _ = gemm_codes(a.codes, b.codes, m, n, k, _FMT_NAME[a.fmt_id].lower(), engine=engine,
                       stream=stream)
     return c
+
+
+
+# ---------------------------------------------------------------- convolutions
+
+
+def conv_out_dim(size: int, k: int, stride: int, pad: int) -> int:
+    """conv_out_dim (kernels.cpp:28-35)."""
+    span = size + 2 * pad - k
+    if span < 0 or stride < 1:
+        raise ValueError("convolution geometry does not fit input")
+    return span // stride + 1
+
+
+def _conv_geom(n, c, h, w, f, kh, kw, stride, pad, layout, engine):
+    if layout not in ("nchw", "nhwc"):
+        raise ValueError(f"unknown layout: {layout}")
+    if engine not in ("tensor", "sequential"):
+        raise ValueError(f"unknown engine: {engine}")
+    return _lib.ConvGeom(n, c, h, w, f, kh, kw, stride, pad,
+                         _lib.NCHW if layout == "nchw" else _lib.NHWC,
+                         _lib.GEMM_TENSOR if engine == "tensor" else _lib.GEMM_SEQUENTIAL)
+
+
+def _nchw_dims(shape, layout):
+    if len(shape) != 4:
+        return None
+    if layout == "nchw":
+        return shape[0], shape[1], shape[2], shape[3]
+    return shape[0], shape[3], shape[1], shape[2]
+
+
+def conv2d(x: QuantizedTensor, w: QuantizedTensor, stride: int = 1, pad: int = 0, *,
+           layout: str = "nchw", engine: str = "sequential", stream=None) -> torch.Tensor:
+    """fp8emu.conv2d (bindings.cpp:191-198 -> kernels.cpp:106-151): FP32 output.
+
+    layout "nchw": x [N,C,H,W], w [F,C,kH,kW] -> y [N,F,OH,OW] (the reference);
+    layout "nhwc": x [N,H,W,C], w [F,kH,kW,C] -> y [N,OH,OW,F].
+    engine "sequential" is bitwise the reference; "tensor" runs tcgen05 implicit
+    GEMM where supported (NHWC E5M2 stride 1) within the GEMM tolerance."""
+    xd, wd = _nchw_dims(x.shape, layout), _nchw_dims(w.shape, layout)
+    if xd is None or wd is None:
+        raise ValueError("conv2d_fp8 expects [N,C,H,W] and [F,C,kH,kW]")
+    n, c, h, wi = xd
+    f, wc, kh, kw = wd
+    if c != wc:
+        raise ValueError("conv2d_fp8 channel counts disagree")
+    if x.fmt_id != w.fmt_id:
+        raise ValueError("kernel operands must share one format")
+    oh, ow = conv_out_dim(h, kh, stride, pad), conv_out_dim(wi, kw, stride, pad)
+    shape = (n, f, oh, ow) if layout == "nchw" else (n, oh, ow, f)
+    y = torch.empty(shape, dtype=torch.float32, device=x.codes.device)
+    g = _conv_geom(n, c, h, wi, f, kh, kw, stride, pad, layout, engine)
+    check(LIB.fp8b_conv2d_fprop(x.codes.data_ptr(), w.codes.data_ptr(), y.data_ptr(), x.fmt_id,
+                                g, _stream(stream)), "conv2d_fp8")
+    return y
+
+
+def conv2d_backward_data(e: QuantizedTensor, w: QuantizedTensor, stride: int, pad: int, h: int,
+                         w_dim: int, *, layout: str = "nchw", engine: str = "sequential",
+                         stream=None) -> torch.Tensor:
+    """conv2d_backward_data_fp8 (kernels.cpp:153-205): dx [N,C,H,W] (or NHWC)."""
+    ed, wd = _nchw_dims(e.shape, layout), _nchw_dims(w.shape, layout)
+    if ed is None or wd is None:
+        raise ValueError("conv backward expects rank-4 operands")
+    n, f, oh, ow = ed
+    wf, c, kh, kw = wd
+    if f != wf:
+        raise ValueError("conv backward filter counts disagree")
+    if e.fmt_id != w.fmt_id:
+        raise ValueError("kernel operands must share one format")
+    if conv_out_dim(h, kh, stride, pad) != oh or conv_out_dim(w_dim, kw, stride, pad) != ow:
+        raise ValueError("conv backward geometry disagrees with error")
+    shape = (n, c, h, w_dim) if layout == "nchw" else (n, h, w_dim, c)
+    dx = torch.empty(shape, dtype=torch.float32, device=e.codes.device)
+    g = _conv_geom(n, c, h, w_dim, f, kh, kw, stride, pad, layout, engine)
+    check(LIB.fp8b_conv2d_dgrad(e.codes.data_ptr(), w.codes.data_ptr(), dx.data_ptr(), e.fmt_id,
+                                g, _stream(stream)), "conv2d_backward_data_fp8")
+    return dx
+
+
+def conv2d_backward_weights(x: QuantizedTensor, e: QuantizedTensor, kh: int, kw: int,
+                            stride: int, pad: int, *, layout: str = "nchw",
+                            engine: str = "sequential", stream=None) -> torch.Tensor:
+    """conv2d_backward_weights_fp8 (kernels.cpp:207-253): dw [F,C,kH,kW] (or [F,kH,kW,C])."""
+    xd, ed = _nchw_dims(x.shape, layout), _nchw_dims(e.shape, layout)
+    if xd is None or ed is None or xd[0] != ed[0]:
+        raise ValueError("conv backward expects matching rank-4 operands")
+    if x.fmt_id != e.fmt_id:
+        raise ValueError("kernel operands must share one format")
+    n, c, h, wi = xd
+    _, f, oh, ow = ed
+    if conv_out_dim(h, kh, stride, pad) != oh or conv_out_dim(wi, kw, stride, pad) != ow:
+        raise ValueError("conv backward geometry disagrees with error")
+    shape = (f, c, kh, kw) if layout == "nchw" else (f, kh, kw, c)
+    dw = torch.empty(shape, dtype=torch.float32, device=x.codes.device)
+    g = _conv_geom(n, c, h, wi, f, kh, kw, stride, pad, layout, engine)
+    check(LIB.fp8b_conv2d_wgrad(x.codes.data_ptr(), e.codes.data_ptr(), dw.data_ptr(), x.fmt_id,
+                                g, _stream(stream)), "conv2d_backward_weights_fp8")
+    return dw
+
+
+def im2col(x: QuantizedTensor, kh: int, kw: int, stride: int = 1, pad: int = 0, *,
+           layout: str = "nchw", stream=None) -> QuantizedTensor:
+    """im2col (kernels.cpp:64-104): NCHW -> [C*kH*kW, N*OH*OW] (the reference);
+    NHWC -> [N*OH*OW, kH*kW*C]."""
+    xd = _nchw_dims(x.shape, layout)
+    if xd is None:
+        raise ValueError("im2col expects [N, C, H, W]")
+    n, c, h, wi = xd
+    oh, ow = conv_out_dim(h, kh, stride, pad), conv_out_dim(wi, kw, stride, pad)
+    rows, cols = (c * kh * kw, n * oh * ow) if layout == "nchw" else (n * oh * ow, kh * kw * c)
+    out = torch.empty(rows * cols, dtype=x.codes.dtype, device=x.codes.device)
+    g = _conv_geom(n, c, h, wi, 1, kh, kw, stride, pad, layout, "sequential")
+    check(LIB.fp8b_im2col(x.codes.data_ptr(), out.data_ptr(), x.fmt_id, g, _stream(stream)),
+          "im2col")
+    return QuantizedTensor(out, [rows, cols], x.fmt_id, x.mode_id, x.counters)
 
 
 def encode(x: float, fmt: str = "fp8", mode: str = "nearest-even", seed: int = 1,

@@ -19,6 +19,7 @@ BITS_LFSR, BITS_COUNTER, BITS_SUPPLIED = 0, 1, 2
 K_MAJOR, MN_MAJOR = 0, 1
 GEMM_TENSOR, GEMM_SEQUENTIAL = 0, 1
 SCALER_CONSTANT, SCALER_DYNAMIC_BACKOFF = 0, 1
+NCHW, NHWC = 0, 1
 MAX_SCHEDULE = 16
 
 _vp = C.c_void_p
@@ -66,6 +67,11 @@ class DenseStep(C.Structure):
                 ("seed", _u64)]
 
 
+class ConvGeom(C.Structure):
+    _fields_ = [("n", _i64), ("c", _i64), ("h", _i64), ("w", _i64), ("f", _i64), ("kh", _i64),
+                ("kw", _i64), ("stride", _i64), ("pad", _i64), ("layout", _i32), ("engine", _i32)]
+
+
 # every symbol include/fp8b200.h declares, with its ctypes signature
 SIGNATURES = {
     "fp8b_quantize": (C.c_int, [_vp, _vp, _i64, _i32, C.POINTER(QuantConfig), _vp, _vp]),
@@ -79,6 +85,10 @@ SIGNATURES = {
     "fp8b_unscale": (C.c_int, [_vp, _i64, _vp, _vp]),
     "fp8b_sgd_momentum_update": (C.c_int, [_vp, _i32, _vp, _vp, _i64, C.POINTER(SgdArgs), _vp]),
     "fp8b_bias_grad": (C.c_int, [_vp, _i32, _i64, _i64, _vp, _vp]),
+    "fp8b_conv2d_fprop": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
+    "fp8b_conv2d_dgrad": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
+    "fp8b_conv2d_wgrad": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
+    "fp8b_im2col": (C.c_int, [_vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
     "fp8b_dense_step": (C.c_int, [C.POINTER(DenseStep), _vp]),
     "fp8b_init": (C.c_int, []),
     "fp8b_last_error": (C.c_char_p, []),

@@ -213,6 +213,67 @@ int fp8b_gemm_tensor_supported(const void* a, const void* b, int64_t m, int64_t 
     return 1;
 }
 
+// ---- conv family (kernels.cpp:28-253) -------------------------------------
+static int conv_validate(const fp8b_conv_t* g, int32_t fmt, const char* who) {
+    if (!g) return fail(FP8B_EINVAL, "conv: null geometry");
+    if (g->n < 0 || g->c < 0 || g->h < 0 || g->w < 0 || g->f < 0 || g->kh < 0 || g->kw < 0)
+        return fail(FP8B_EINVAL, who);
+    // conv_out_dim (kernels.cpp:28-35)
+    if (g->stride < 1 || g->h + 2 * g->pad - g->kh < 0 || g->w + 2 * g->pad - g->kw < 0 ||
+        g->pad < 0)
+        return fail(FP8B_EINVAL, "convolution geometry does not fit input");
+    if (g->layout != FP8B_NCHW && g->layout != FP8B_NHWC) return fail(FP8B_EINVAL, "conv: bad layout");
+    if (g->engine != FP8B_GEMM_TENSOR && g->engine != FP8B_GEMM_SEQUENTIAL)
+        return fail(FP8B_EINVAL, "conv: bad engine");
+    if (!valid_fmt(fmt)) return fail(FP8B_EINVAL, "kernel operands must share one format");
+    return FP8B_OK;
+}
+
+static int conv_common(int kind, const void* a, const void* b, float* out, int32_t fmt,
+                       const fp8b_conv_t* g, void* stream, const char* who) {
+    const int rc = conv_validate(g, fmt, who);
+    if (rc) return rc;
+    const int64_t oh = (g->h + 2 * g->pad - g->kh) / g->stride + 1;
+    const int64_t ow = (g->w + 2 * g->pad - g->kw) / g->stride + 1;
+    const int64_t nout = kind == 0 ? g->n * g->f * oh * ow
+                         : kind == 1 ? g->n * g->c * g->h * g->w
+                                     : g->f * g->c * g->kh * g->kw;
+    if (nout == 0) return FP8B_OK;
+    if (!out || !a || !b) return fail(FP8B_EINVAL, "conv: null tensor");
+    if (g->engine == FP8B_GEMM_TENSOR) {
+        int nl = 0;
+        const int r = fp8b::launch_conv_tc(kind, a, b, out, fmt, *g, S(stream), &nl);
+        if (r == FP8B_OK) return check_launch(nl);
+        if (r != FP8B_ENOTSUP) return r;
+    }
+    fp8b::launch_conv_seq(kind, a, b, out, fmt, *g, S(stream));
+    return check_launch(1);
+}
+
+int fp8b_conv2d_fprop(const void* x, const void* w, float* y, int32_t fmt, const fp8b_conv_t* g,
+                      void* stream) {
+    return conv_common(0, x, w, y, fmt, g, stream, "conv2d_fp8 expects [N,C,H,W] and [F,C,kH,kW]");
+}
+int fp8b_conv2d_dgrad(const void* e, const void* w, float* dx, int32_t fmt, const fp8b_conv_t* g,
+                      void* stream) {
+    return conv_common(1, e, w, dx, fmt, g, stream, "conv backward expects rank-4 operands");
+}
+int fp8b_conv2d_wgrad(const void* x, const void* e, float* dw, int32_t fmt, const fp8b_conv_t* g,
+                      void* stream) {
+    return conv_common(2, x, e, dw, fmt, g, stream,
+                       "conv backward expects matching rank-4 operands");
+}
+int fp8b_im2col(const void* x, void* cols, int32_t fmt, const fp8b_conv_t* g, void* stream) {
+    const int rc = conv_validate(g, fmt, "im2col expects [N, C, H, W]");
+    if (rc) return rc;
+    const int64_t oh = (g->h + 2 * g->pad - g->kh) / g->stride + 1;
+    const int64_t ow = (g->w + 2 * g->pad - g->kw) / g->stride + 1;
+    if (g->n * oh * ow * g->c * g->kh * g->kw == 0) return FP8B_OK;
+    if (!x || !cols) return fail(FP8B_EINVAL, "im2col: null tensor");
+    fp8b::launch_im2col(x, cols, fmt, *g, S(stream));
+    return check_launch(1);
+}
+
 int fp8b_loss_scaler_init(fp8b_loss_scaler_t* dev_state, const fp8b_loss_scaler_t* o,
                           void* stream) {
     if (!dev_state || !o) return fail(FP8B_EINVAL, "loss_scaler_init: null pointer");

@@ -42,6 +42,13 @@ void launch_gemm_seq(const void* a, const void* b, int64_t m, int64_t n, int64_t
 // the tensor-core engine.
 int launch_gemm_tc(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int fmt,
                    int a_mn, int b_mn, const EpiArgs& ep, cudaStream_t st, int* nlaunch);
+// Conv family: kind 0 fprop, 1 dgrad, 2 wgrad.
+void launch_conv_seq(int kind, const void* a, const void* b, float* out, int fmt,
+                     const fp8b_conv_t& g, cudaStream_t st);
+// Returns FP8B_ENOTSUP when the tensor engine does not cover the case.
+int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
+                   const fp8b_conv_t& g, cudaStream_t st, int* nlaunch);
+void launch_im2col(const void* x, void* cols, int fmt, const fp8b_conv_t& g, cudaStream_t st);
 // Adds n to the library's launch counter (fp8b_launch_count).
 void note_launches(int n);
 void launch_fill_synthetic(float* out, int64_t n, int kind, uint64_t seed, double p, double lo,

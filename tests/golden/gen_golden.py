@@ -182,6 +182,27 @@ def main():
     with open(os.path.join(HERE, "gemm_golden.json"), "w") as f:
         json.dump(gm, f, indent=1)
 
+    # ---- conv family from the reference (kernels.cpp:106-253), NCHW
+    rngc = np.random.default_rng(17)
+    cg = {}
+    cmeta = []
+    shapes = [(2, 3, 7, 6, 4, 3, 1, 1), (1, 2, 9, 9, 3, 3, 2, 1), (2, 4, 5, 5, 2, 1, 1, 0),
+              (1, 3, 8, 7, 2, 3, 2, 0), (2, 16, 6, 6, 8, 3, 1, 1), (1, 8, 5, 5, 16, 1, 1, 0)]
+    for i, (n_, c, h, w, f, k, st, pd) in enumerate(shapes):
+        oh, ow = O.conv_out(h, k, st, pd), O.conv_out(w, k, st, pd)
+        x, _ = O.ref_quantize(rngc.uniform(-2, 2, n_ * c * h * w).astype(np.float32))
+        wt, _ = O.ref_quantize(rngc.uniform(-2, 2, f * c * k * k).astype(np.float32))
+        e, _ = O.ref_quantize(rngc.uniform(-2, 2, n_ * f * oh * ow).astype(np.float32))
+        cg[f"x_{i}"], cg[f"w_{i}"], cg[f"e_{i}"] = x, wt, e
+        cg[f"y_{i}"] = O.ref_conv2d(x, wt, n_, c, h, w, f, k, k, st, pd, kind="fprop")
+        cg[f"dx_{i}"] = O.ref_conv2d(e, wt, n_, c, h, w, f, k, k, st, pd, kind="dgrad")
+        cg[f"dw_{i}"] = O.ref_conv2d(x, e, n_, c, h, w, f, k, k, st, pd, kind="wgrad")
+        cmeta.append({"i": i, "n": n_, "c": c, "h": h, "w": w, "f": f, "k": k, "stride": st,
+                      "pad": pd})
+    np.savez_compressed(os.path.join(HERE, "conv_golden.npz"), **cg)
+    with open(os.path.join(HERE, "conv_golden.json"), "w") as f_:
+        json.dump(cmeta, f_, indent=1)
+
     # ---- loss scaler traces from the reference
     traces = []
     def trace(opts, steps, cite):

@@ -269,3 +269,17 @@ def test_reference_mt_harness_bit_identical():
         c2, k2 = O.ref_quantize_mt(x, "fp8", mode, 1337, nthreads=4)
         np.testing.assert_array_equal(c1.astype(np.uint8), c2)
         np.testing.assert_array_equal(k1, k2)
+
+
+CG = np.load(os.path.join(GOLD, "conv_golden.npz"))
+
+
+@pytest.mark.parametrize("m", _load("conv_golden.json"), ids=lambda m: str(m["i"]))
+def test_conv_family_golden_bitwise(m):
+    """conv2d_fp8 / backward_data / backward_weights (kernels.cpp:106-253)."""
+    i = m["i"]
+    args = (m["n"], m["c"], m["h"], m["w"], m["f"], m["k"], m["k"], m["stride"], m["pad"])
+    for kind, a, b, want in [("fprop", "x", "w", "y"), ("dgrad", "e", "w", "dx"),
+                             ("wgrad", "x", "e", "dw")]:
+        got = O.conv2d(CG[f"{a}_{i}"], CG[f"{b}_{i}"], *args, kind=kind)
+        np.testing.assert_array_equal(got.view(np.uint32), CG[f"{want}_{i}"].view(np.uint32))

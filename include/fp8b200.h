@@ -235,6 +235,10 @@ int fp8b_conv2d_dgrad(const void *e, const void *w, float *dx, int32_t fmt,
 int fp8b_conv2d_wgrad(const void *x, const void *e, float *dw, int32_t fmt,
                       const fp8b_conv_t *g, void *stream);
 
+/* 1 if FP8B_GEMM_TENSOR runs this conv (kind 0 fprop, 1 dgrad, 2 wgrad) on the
+ * tensor cores for 16-byte-aligned operands, 0 if it takes the sequential engine. */
+int fp8b_conv_tensor_supported(const fp8b_conv_t *g, int32_t fmt, int32_t kind);
+
 /* im2col (kernels.hpp:25-30): pure code movement, zero code for padded taps.
  * FP8B_NCHW gives the reference's patch matrix [C*kH*kW, N*OH*OW] (rows
  * (c,kh,kw), cols (n,oh,ow)); FP8B_NHWC gives its transpose in the NHWC tap

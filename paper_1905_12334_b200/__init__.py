@@ -33,7 +33,7 @@ __all__ = [
     "QuantizedTensor", "ScaleEvent", "LossScaler", "quantize", "dequantize", "transpose",
     "gemm", "gemm_codes", "encode", "decode", "sgd_momentum_update", "bias_grad",
     "count_nonfinite", "fill_synthetic", "Counters", "launch_count", "version",
-    "conv2d", "conv2d_backward_data", "conv2d_backward_weights", "im2col", "conv_out_dim",
+    "conv2d", "conv2d_backward_data", "conv2d_backward_weights", "im2col", "conv_out_dim", "conv_tensor_supported",
 ]
 
 _FMT = {"fp8": _lib.E5M2, "FP8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16,
@@ -367,6 +367,14 @@ def conv2d_backward_weights(x: QuantizedTensor, e: QuantizedTensor, kh: int, kw:
     check(LIB.fp8b_conv2d_wgrad(x.codes.data_ptr(), e.codes.data_ptr(), dw.data_ptr(), x.fmt_id,
                                 g, _stream(stream)), "conv2d_backward_weights_fp8")
     return dw
+
+
+def conv_tensor_supported(n, c, h, w, f, k, stride=1, pad=0, fmt="fp8", kind="fprop",
+                          layout="nhwc") -> bool:
+    """True if engine="tensor" runs this conv on tcgen05 (else the sequential engine)."""
+    g = _conv_geom(n, c, h, w, f, k, k, stride, pad, layout, "tensor")
+    return bool(LIB.fp8b_conv_tensor_supported(g, _fmt(fmt),
+                                               {"fprop": 0, "dgrad": 1, "wgrad": 2}[kind]))
 
 
 def im2col(x: QuantizedTensor, kh: int, kw: int, stride: int = 1, pad: int = 0, *,

@@ -88,6 +88,7 @@ SIGNATURES = {
     "fp8b_conv2d_fprop": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
     "fp8b_conv2d_dgrad": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
     "fp8b_conv2d_wgrad": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
+    "fp8b_conv_tensor_supported": (C.c_int, [C.POINTER(ConvGeom), _i32, _i32]),
     "fp8b_im2col": (C.c_int, [_vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
     "fp8b_dense_step": (C.c_int, [C.POINTER(DenseStep), _vp]),
     "fp8b_init": (C.c_int, []),

@@ -263,6 +263,10 @@ int fp8b_conv2d_wgrad(const void* x, const void* e, float* dw, int32_t fmt, cons
     return conv_common(2, x, e, dw, fmt, g, stream,
                        "conv backward expects matching rank-4 operands");
 }
+int fp8b_conv_tensor_supported(const fp8b_conv_t* g, int32_t fmt, int32_t kind) {
+    if (!g || conv_validate(g, fmt, "conv") != FP8B_OK || kind < 0 || kind > 2) return 0;
+    return fp8b::conv_tc_supported(kind, fmt, *g);
+}
 int fp8b_im2col(const void* x, void* cols, int32_t fmt, const fp8b_conv_t* g, void* stream) {
     const int rc = conv_validate(g, fmt, "im2col expects [N, C, H, W]");
     if (rc) return rc;

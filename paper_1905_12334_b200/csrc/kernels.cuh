@@ -48,6 +48,7 @@ void launch_conv_seq(int kind, const void* a, const void* b, float* out, int fmt
 // Returns FP8B_ENOTSUP when the tensor engine does not cover the case.
 int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
                    const fp8b_conv_t& g, cudaStream_t st, int* nlaunch);
+int conv_tc_supported(int kind, int fmt, const fp8b_conv_t& g);
 void launch_im2col(const void* x, void* cols, int fmt, const fp8b_conv_t& g, cudaStream_t st);
 // Adds n to the library's launch counter (fp8b_launch_count).
 void note_launches(int n);

@@ -208,6 +208,7 @@ def run_ours(args):
     if rank == 0 and not args.no_extras:
         result["update"] = bench_update(F, args)
         result["gemm"] = bench_gemm(F, args, bf16_peak)
+        result["conv"] = bench_conv(F, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(x, args)
     if dist:
@@ -353,6 +354,84 @@ def bench_gemm(F, args, bf16_peak):
     return res
 
 
+RESNET_LAYERS = [  # (name, C, F, H=W, k): BASELINE config 4, stride 1, pad k//2
+    ("3x3_64@56", 64, 64, 56, 3), ("3x3_128@28", 128, 128, 28, 3),
+    ("3x3_256@14", 256, 256, 14, 3), ("3x3_512@7", 512, 512, 7, 3),
+    ("1x1_64-256@56", 64, 256, 56, 1), ("1x1_256-64@56", 256, 64, 56, 1),
+    ("1x1_128-512@28", 128, 512, 28, 1), ("1x1_512-128@28", 512, 128, 28, 1),
+    ("1x1_256-1024@14", 256, 1024, 14, 1), ("1x1_1024-256@14", 1024, 256, 14, 1),
+    ("1x1_512-2048@7", 512, 2048, 7, 1), ("1x1_2048-512@7", 2048, 512, 7, 1),
+]
+
+
+def bench_conv(F, args, reps=5, only=None):
+    """BASELINE config 4: ResNet-50-shaped conv layers, batch N NHWC, E5M2 codes,
+    implicit GEMM on tcgen05 for fprop / dgrad / wgrad (FP32 outputs). Inputs:
+    half-normal activations, He-init weights, N(0, 1e-5) errors x 2^13 loss
+    scale, quantized RNE to E5M2 by our own kernels."""
+    import torch
+    from paper_1905_12334_b200 import _lib
+    nb = args.conv_batch
+    res = {}
+    tot_flop = tot_ms = 0.0
+    for name, c, f, hw, k in RESNET_LAYERS:
+        if only and name not in only:
+            continue
+        pad = k // 2
+        P = nb * hw * hw
+        xs = torch.empty(P * c, dtype=torch.float32, device="cuda")
+        F.fill_synthetic(xs, "halfnormal", 11, 1.0)
+        ws = torch.empty(f * k * k * c, dtype=torch.float32, device="cuda")
+        F.fill_synthetic(ws, "normal", 12, (2.0 / (k * k * c)) ** 0.5)
+        es = torch.empty(P * f, dtype=torch.float32, device="cuda")
+        F.fill_synthetic(es, "normal", 13, 1e-5 * 8192.0)
+        X = F.quantize(xs).reshaped([nb, hw, hw, c])
+        W = F.quantize(ws).reshaped([f, k, k, c])
+        E = F.quantize(es).reshaped([nb, hw, hw, f])
+        del xs, ws, es
+        flop = 2.0 * P * f * k * k * c
+        row = {}
+        calls = {
+            "fprop": lambda: F.conv2d(X, W, 1, pad, layout="nhwc", engine="tensor"),
+            "dgrad": lambda: F.conv2d_backward_data(E, W, 1, pad, hw, hw, layout="nhwc",
+                                                    engine="tensor"),
+            "wgrad": lambda: F.conv2d_backward_weights(X, E, k, k, 1, pad, layout="nhwc",
+                                                       engine="tensor"),
+        }
+        for kind, fn in calls.items():
+            assert F.conv_tensor_supported(nb, c, hw, hw, f, k, 1, pad, "fp8", kind)
+            out = fn()
+            del out
+            torch.cuda.synchronize()
+            # one pass captured in a CUDA graph: replays measure device time only
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                out = fn()
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / reps
+            del g, out
+            row[kind] = {"ms": round(ms, 3), "tflops": round(flop / (ms * 1e-3) / 1e12, 1)}
+            tot_flop += flop
+            tot_ms += ms
+        res[name] = row
+        del X, W, E
+        torch.cuda.empty_cache()
+    res["all_layers_fprop_dgrad_wgrad"] = {"ms": round(tot_ms, 3),
+                                           "tflops": round(tot_flop / (tot_ms * 1e-3) / 1e12, 1)}
+    res["config"] = {"batch": nb, "layout": "NHWC", "dtype": "e5m2 x e5m2 -> f32",
+                     "timing": "CUDA-graph replays of one pass (device time incl. dgrad's weight "
+                               "flip and wgrad's split-K sum)"}
+    _ = _lib
+    return res
+
+
 def cpu_baseline(x_dev, args):
     """The reference's own quantize (oracle/_ref, compiled from /root/reference)
     on this host's cores, block-parallel (bit-identical to serial), over a bounded
@@ -428,6 +507,7 @@ def main():
     ap.add_argument("--e2e-log2n", type=int, default=28)
     ap.add_argument("--cpu-log2n", type=int, default=23)
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--conv-batch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

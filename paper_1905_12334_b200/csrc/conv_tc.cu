@@ -18,6 +18,7 @@
 // those of gemm_tc.cu. Sums are reordered relative to the reference, so parity
 // is the GEMM tolerance |y - y_exact| <= 1e-6 * (|x| * |w|) (tests/test_conv_gpu.py).
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "tc_common.cuh"
@@ -35,6 +36,7 @@ struct CParams {
     int cblocks;   // fprop: channel blocks per tap
     int C;         // channels of the im2col'd tensor
     int KW, pad, OH, OW;
+    int c_tma;     // outputs go through the TMA-store epilogue
     float* ws;     // wgrad: split-K partials [splits][M][N]
 };
 
@@ -96,8 +98,9 @@ struct Geo {
     static constexpr uint32_t A_BYTES = MODE == 0 ? 128u * CB : 128u * 128u;
     static constexpr uint32_t B_BYTES = MODE == 0 ? (uint32_t)BN * CB : (uint32_t)KPIX * CB;
     static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (200 * 1024 / STAGE) > 8 ? 8 : (200 * 1024 / STAGE);
-    static constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 256;
+    static constexpr int BUDGET = 232448 - (int)EPI_STAGE_BYTES - 1280;
+    static constexpr int STAGES = (BUDGET / (int)STAGE) > 8 ? 8 : (BUDGET / (int)STAGE);
+    static constexpr uint32_t SMEM = STAGES * STAGE + EPI_STAGE_BYTES + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr uint32_t SWZ_LAYOUT = CB == 128 ? 2u : 4u;  // UMMA layout code
     static constexpr uint32_t SBO = 8u * CB;                     // 8 rows of one swizzle atom
@@ -108,12 +111,12 @@ struct Geo {
 template <int ES, int MODE, int BN, int CB>
 __global__ void __launch_bounds__(THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const CParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const CParams p) {
     using G = Geo<ES, MODE, BN, CB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE + EPI_STAGE_BYTES);
     uint64_t* empty_bar = full_bar + G::STAGES;
     uint64_t* tfull_bar = empty_bar + G::STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -249,6 +252,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else {
         const int quarter = warp & 3;
+        uint8_t* sbuf = smem + G::STAGES * G::STAGE + quarter * 8192;
+        uint32_t nst = 0;
         int acc = 0;
         uint32_t accphase = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
@@ -263,7 +268,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                 uint32_t v[32];
                 tmem_ld32(taddr + c * 32, v);
                 const int64_t col0 = (int64_t)tn * BN + c * 32;
-                if (row >= p.M || col0 >= p.N) continue;
+                if (col0 >= p.N) continue;
+                const int64_t row0 = (int64_t)tm * 128 + quarter * 32;
+                if (p.c_tma) {
+                    if (MODE == 0) {
+                        epilogue_chunk(p, row, col0, v, co, cu, cn, &tmC, sbuf + (nst++ & 1) * 4096,
+                                       row0, lane);
+                    } else {
+                        float y[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]);
+                        stage_store_c(&tmC, sbuf + (nst++ & 1) * 4096, y, lane, (int32_t)col0,
+                                      (int32_t)row0, s);
+                    }
+                    continue;
+                }
+                if (row >= p.M) continue;
                 if (MODE == 0) {
                     epilogue_chunk(p, row, col0, v, co, cu, cn);
                 } else {
@@ -281,6 +301,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (++acc == 2) { acc = 0; accphase ^= 1; }
         }
     }
+    if (p.c_tma && warp >= 2 && lane == 0) bulk_wait_all();
     if (MODE == 0 && p.ep.cq_counters) flush_counters<THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     __syncthreads();
@@ -314,6 +335,28 @@ __global__ void flip_kernel(const T* __restrict__ w, T* __restrict__ wf, int64_t
     }
 }
 
+static bool epi_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FP8B_EPI_TMA");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// 3-D store map over the split-K workspace [splits][m][n] FP32 (32x32x1 boxes).
+static bool make_ws_map(CUtensorMap* tm, float* ws, int splits, int64_t m, int64_t n) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc || (uintptr_t)ws % 16 || (n * 4) % 16) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)m, (cuuint64_t)splits};
+    cuuint64_t strides[2] = {(cuuint64_t)(n * 4), (cuuint64_t)(m * n * 4)};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ws, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int num_sms() {
     static int v = 0;
     static std::once_flag once;
@@ -326,7 +369,8 @@ static int num_sms() {
 }
 
 template <int ES, int MODE, int BN, int CB>
-static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CParams& p, cudaStream_t st) {
+static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, const CParams& p,
+               cudaStream_t st) {
     using G = Geo<ES, MODE, BN, CB>;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -335,7 +379,7 @@ static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CParams& p, c
     });
     const int items = p.tiles_m * p.tiles_n * p.splits;
     const int grid = items < num_sms() ? items : num_sms();
-    conv_tc_kernel<ES, MODE, BN, CB><<<grid, THREADS, G::SMEM, st>>>(ta, tb, p);
+    conv_tc_kernel<ES, MODE, BN, CB><<<grid, THREADS, G::SMEM, st>>>(ta, tb, tcm, p);
     return FP8B_OK;
 }
 
@@ -362,14 +406,17 @@ static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, i
     p.num_kb = k * k * p.cblocks;
     p.splits = 1;
     p.C = (int)c; p.KW = k; p.pad = pad; p.OH = (int)oh; p.OW = (int)ow;
+    CUtensorMap tcm;
+    memset(&tcm, 0, sizeof(tcm));
+    p.c_tma = (epi_tma() && make_c_map(&tcm, y, P, f)) ? 1 : 0;
     if (cb_bytes == 128) {
-        if (bn == 64) return run<ES, 0, 64, 128>(ta, tb, p, st);
-        if (bn == 128) return run<ES, 0, 128, 128>(ta, tb, p, st);
-        return run<ES, 0, 256, 128>(ta, tb, p, st);
+        if (bn == 64) return run<ES, 0, 64, 128>(ta, tb, tcm, p, st);
+        if (bn == 128) return run<ES, 0, 128, 128>(ta, tb, tcm, p, st);
+        return run<ES, 0, 256, 128>(ta, tb, tcm, p, st);
     }
-    if (bn == 64) return run<ES, 0, 64, 64>(ta, tb, p, st);
-    if (bn == 128) return run<ES, 0, 128, 64>(ta, tb, p, st);
-    return run<ES, 0, 256, 64>(ta, tb, p, st);
+    if (bn == 64) return run<ES, 0, 64, 64>(ta, tb, tcm, p, st);
+    if (bn == 128) return run<ES, 0, 128, 64>(ta, tb, tcm, p, st);
+    return run<ES, 0, 256, 64>(ta, tb, tcm, p, st);
 }
 
 // wgrad: dw [f, k, k, c] from x [n, h, w, c] and e [n, oh, ow, f]
@@ -404,9 +451,12 @@ static int wgrad(const void* x, const void* e, float* dw, int64_t n, int64_t h, 
             return FP8B_ECUDA;
     }
     p.ws = ws;
+    CUtensorMap tcm;
+    memset(&tcm, 0, sizeof(tcm));
+    p.c_tma = (epi_tma() && make_ws_map(&tcm, ws, splits, p.M, p.N)) ? 1 : 0;
     int rc;
-    if (cb_bytes == 128) rc = run<ES, 1, 128 / ES, 128>(ta, tb, p, st);
-    else rc = run<ES, 1, 64 / ES, 64>(ta, tb, p, st);
+    if (cb_bytes == 128) rc = run<ES, 1, 128 / ES, 128>(ta, tb, tcm, p, st);
+    else rc = run<ES, 1, 64 / ES, 64>(ta, tb, tcm, p, st);
     *nl = 1;
     if (splits > 1) {
         int64_t b = (mn + 255) / 256;

@@ -23,6 +23,7 @@
 // hence tolerance-level parity: |C - C_exact| <= 1e-6 * (|A||B|)_ij, checked in
 // tests/test_gemm_gpu.py; FP8B_GEMM_SEQUENTIAL gives bitwise parity.
 #include <cstdlib>
+#include <cstring>
 
 #include "tc_common.cuh"
 
@@ -38,23 +39,24 @@ constexpr uint32_t A_BYTES = BM * BKB;
 constexpr uint32_t B_BYTES = BN * BKB;
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t TMEM_COLS = 512;  // 2 accumulators x 256 FP32 columns
-constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + EPI_STAGE_BYTES + 1024 + 256;
 
 struct Params {
     int64_t M, N, K;
     int a_mn, b_mn;
     int tiles_m, tiles_n, num_kb;
+    int c_tma;  // FP32 C goes out through the TMA-store epilogue
     EpiArgs ep;
 };
 
 template <int ES>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const Params p) {
+                   const __grid_constant__ CUtensorMap tmC, const Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + EPI_STAGE_BYTES);
     uint64_t* empty_bar = full_bar + STAGES;
     uint64_t* tfull_bar = empty_bar + STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -165,6 +167,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else {
         const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+        uint8_t* sbuf = smem + STAGES * STAGE_BYTES + quarter * 8192;
+        uint32_t nst = 0;
         int acc = 0;
         uint32_t accphase = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -179,7 +183,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 uint32_t v[32];
                 tmem_ld32(taddr + c * 32, v);
                 const int64_t col0 = (int64_t)tn * BN + c * 32;
-                if (row < p.M && col0 < p.N) epilogue_chunk(p, row, col0, v, co, cu, cn);
+                if (p.c_tma) {
+                    if (col0 < p.N)
+                        epilogue_chunk(p, row, col0, v, co, cu, cn, &tmC, sbuf + (nst++ & 1) * 4096,
+                                       (int64_t)tm * BM + quarter * 32, lane);
+                } else if (row < p.M && col0 < p.N) {
+                    epilogue_chunk(p, row, col0, v, co, cu, cn);
+                }
             }
             fence_before();
             __syncwarp();
@@ -187,6 +197,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (++acc == 2) { acc = 0; accphase ^= 1; }
         }
     }
+    if (p.c_tma && warp >= 2 && lane == 0) bulk_wait_all();
     if (p.ep.cq_counters) flush_counters<NUM_THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     __syncthreads();
@@ -211,7 +222,7 @@ constexpr int STAGES2 = 6;
 constexpr uint32_t A2_BYTES = 128 * BKB;  // per CTA
 constexpr uint32_t B2_BYTES = 128 * BKB;  // per CTA
 constexpr uint32_t STAGE2_BYTES = A2_BYTES + B2_BYTES;
-constexpr uint32_t SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 512;
+constexpr uint32_t SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 512;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -264,11 +275,11 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
 template <int ES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const Params p) {
+                    const __grid_constant__ CUtensorMap tmC, const Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES + EPI_STAGE_BYTES);
     uint64_t* empty_bar = full_bar + STAGES2;
     uint64_t* tfull_bar = empty_bar + STAGES2;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -377,6 +388,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
     } else {
         const int quarter = warp & 3;
+        uint8_t* sbuf = smem + STAGES2 * STAGE2_BYTES + quarter * 8192;
+        uint32_t nst = 0;
         int acc = 0;
         uint32_t accphase = 0;
         const uint32_t te_leader = mapa_u32(smem_u32(tempty_bar), 0);
@@ -392,7 +405,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 uint32_t v[32];
                 tmem_ld32(taddr + c * 32, v);
                 const int64_t col0 = (int64_t)tn * BN2 + c * 32;
-                if (row < p.M && col0 < p.N) epilogue_chunk(p, row, col0, v, co, cu, cn);
+                if (p.c_tma) {
+                    if (col0 < p.N)
+                        epilogue_chunk(p, row, col0, v, co, cu, cn, &tmC, sbuf + (nst++ & 1) * 4096,
+                                       (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane);
+                } else if (row < p.M && col0 < p.N) {
+                    epilogue_chunk(p, row, col0, v, co, cu, cn);
+                }
             }
             fence_before();
             __syncwarp();
@@ -400,6 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (++acc == 2) { acc = 0; accphase ^= 1; }
         }
     }
+    if (p.c_tma && warp >= 2 && lane == 0) bulk_wait_all();
     if (p.ep.cq_counters) flush_counters<NUM_THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     cluster_sync_all();
@@ -416,6 +436,16 @@ static bool use_2sm() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FP8B_GEMM_2SM");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// FP8B_EPI_TMA=0 selects the direct-store epilogue (for A/B checks).
+static bool use_epi_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FP8B_EPI_TMA");
         v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
@@ -446,6 +476,9 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
     p.tiles_n = (int)((n + BN - 1) / BN);
     p.num_kb = (int)((k + BKE - 1) / BKE);
     p.ep = ep;
+    CUtensorMap tmC;
+    memset(&tmC, 0, sizeof(tmC));
+    p.c_tma = (use_epi_tma() && ep.c && make_c_map(&tmC, ep.c, m, n)) ? 1 : 0;
     static int num_sms = 0;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -475,13 +508,13 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
             int grid2 = 2 * ntiles2;
             const int maxg = num_sms & ~1;
             if (grid2 > maxg) grid2 = maxg;
-            gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, p2);
+            gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, tmC, p2);
             return FP8B_OK;
         }
     }
     const int ntiles = p.tiles_m * p.tiles_n;
     const int grid = ntiles < num_sms ? ntiles : num_sms;
-    gemm_tc_kernel<ES><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(tmA, tmB, p);
+    gemm_tc_kernel<ES><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(tmA, tmB, tmC, p);
     return FP8B_OK;
 }
 

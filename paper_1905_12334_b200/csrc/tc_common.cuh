@@ -122,10 +122,59 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 }
 
 // Epilogue for one 32-column chunk of one row held in registers.
+// TMA-store staging for the FP32 output: each epilogue warp owns two 4 KB
+// buffers (32 rows x 32 FP32, 128B-swizzled to match the C tensor map), fills
+// one per 32-column chunk with st.shared.v4 and hands it to the TMA engine with
+// one cp.async.bulk.tensor store (rows/cols outside C are clipped by TMA).
+constexpr uint32_t EPI_STAGE_BYTES = 4 * 2 * 4096;  // 4 warps x 2 buffers
+
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void stage_store_c(const CUtensorMap* tmC, uint8_t* buf, const float (&y)[32],
+                                              int lane, int32_t col0, int32_t row0, int32_t z = -1) {
+    if (lane == 0) bulk_wait_read1();  // the buffer's previous store has read it
+    __syncwarp();
+    const uint32_t base = smem_u32(buf) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t a = base + ((uint32_t)(j ^ (lane & 7)) << 4);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(y[4 * j]),
+                     "f"(y[4 * j + 1]), "f"(y[4 * j + 2]), "f"(y[4 * j + 3])
+                     : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        if (z < 0)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(tmC)),
+                "r"(smem_u32(buf)), "r"(col0), "r"(row0)
+                : "memory");
+        else
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(tmC)),
+                "r"(smem_u32(buf)), "r"(col0), "r"(row0), "r"(z)
+                : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+}
+
+// Epilogue of one 32-column chunk; one row per lane. With tmC set, the whole
+// warp must call it (rows >= M included: TMA clips them) and C goes out through
+// stage_store_c; otherwise rows >= M return early.
 template <class P>
 __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t col0,
                                                uint32_t (&v)[32], uint32_t& co, uint32_t& cu,
-                                               uint32_t& cn) {
+                                               uint32_t& cn, const CUtensorMap* tmC = nullptr,
+                                               uint8_t* sbuf = nullptr, int64_t row0 = 0,
+                                               int lane = 0) {
     const EpiArgs& ep = p.ep;
     float y[32];
 #pragma unroll
@@ -136,8 +185,10 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
         for (int j = 0; j < 32; ++j)
             if (full || col0 + j < p.N) y[j] = __fadd_rn(y[j], __ldg(ep.bias + col0 + j));
     }
+    if (tmC) stage_store_c(tmC, sbuf, y, lane, (int32_t)col0, (int32_t)row0);
+    if (row >= p.M) return;
     const int64_t base = row * p.N + col0;
-    if (ep.c) {
+    if (ep.c && !tmC) {
         if (full && (p.N % 4 == 0)) {
             float4* dst = reinterpret_cast<float4*>(ep.c + base);
 #pragma unroll
@@ -235,18 +286,30 @@ static inline EncodeTiledFn get_encode() {
 static inline bool make_map(CUtensorMap* tm, const void* ptr, int es, uint64_t inner,
                             uint64_t outer, uint32_t box_inner, uint32_t box_outer,
                             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+    // es: 1 = u8 codes, 2 = u16 codes, 4 = FP32
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {inner * (uint64_t)es};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
-    return enc(tm, es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
+    const CUtensorMapDataType dt = es == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    return enc(tm, dt, 2,
                const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+
+// Store map for an FP32 [m, n] output (32x32 boxes, 128B swizzle); false when
+// TMA cannot address it (row stride not a multiple of 16 bytes).
+static inline bool make_c_map(CUtensorMap* tm, const float* c, int64_t m, int64_t n) {
+    if (!c || (uintptr_t)c % 16 || (n * 4) % 16 || m <= 0 || n <= 0) return false;
+    if (m > INT32_MAX || n > INT32_MAX) return false;
+    return make_map(tm, c, 4, (uint64_t)n, (uint64_t)m, 32, 32);
+}
 
 }  // namespace tc
 }  // namespace fp8b

@@ -505,7 +505,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--log2n", type=int, default=28)
     ap.add_argument("--e2e-log2n", type=int, default=28)
-    ap.add_argument("--cpu-log2n", type=int, default=23)
+    ap.add_argument("--cpu-log2n", type=int, default=27)
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--conv-batch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")

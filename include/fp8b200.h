@@ -245,6 +245,27 @@ int fp8b_conv_tensor_supported(const fp8b_conv_t *g, int32_t fmt, int32_t kind);
  * order, [N*OH*OW, kH*kW*C] (K-major A operand of fp8b_gemm). */
 int fp8b_im2col(const void *x, void *cols, int32_t fmt, const fp8b_conv_t *g, void *stream);
 
+/* ------------------------------------------------ FP8T container (host) ---- */
+/* The reference's binary tensor file (tensor_io.hpp:18-31, tensor_io.cpp:47-187):
+ * "FP8T", version 1, dtype (0 FP32, 1 FP8 codes, 2 FP16 codes), rank, rounding
+ * mode tag (0 none, 1 nearest-even, 2 stochastic, 3 truncate), 8 reserved zero
+ * bytes, rank big-endian uint64 dims, then the big-endian row-major payload.
+ * Host buffers in native byte order: float32, uint8 codes, uint16 codes.
+ * Errors: FP8B_EIO with the reference's IoError message in fp8b_last_error(). */
+enum { FP8B_FP8T_F32 = 0, FP8B_FP8T_FP8 = 1, FP8B_FP8T_FP16 = 2 };
+enum { FP8B_EIO = 5 };
+#define FP8B_FP8T_MAX_RANK 255
+
+/* save_tensor (tensor_io.cpp:107-140) */
+int fp8b_fp8t_save(const char *path, int32_t dtype, int32_t mode_tag, int32_t rank,
+                   const int64_t *dims, const void *data);
+/* header of a file: dtype, mode tag, rank and up to max_rank dims */
+int fp8b_fp8t_peek(const char *path, int32_t *dtype, int32_t *mode_tag, int32_t *rank,
+                   int64_t *dims, int32_t max_rank);
+/* load_tensor_fp32 / load_tensor_codes (tensor_io.cpp:142-187): expect_dtype
+ * FP8B_FP8T_F32, or -1 for "codes of either width"; capacity in elements. */
+int fp8b_fp8t_load(const char *path, int32_t expect_dtype, void *data, int64_t capacity);
+
 /* ---------------------------------------------------------- layer step ---- */
 /* One quantized Dense-layer training step on device, the composition
  * Network::forward -> backward -> apply_update -> LossScaler::step performs for a

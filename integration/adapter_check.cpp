@@ -213,6 +213,45 @@ static std::string check_update() {
     return "";
 }
 
+static std::string check_conv() {
+    // test_kernels.cpp:97-184 style: random NCHW shapes, every conv-family entry
+    // point bitwise against the reference library.
+    LfsrStream dims = LfsrStream::split(0xC0, 0);
+    QuantConfig cfg;
+    for (int trial = 0; trial < 24; ++trial) {
+        const int64_t n = 1 + dims.next_bits() % 2, c = 1 + dims.next_bits() % 4,
+                      h = 3 + dims.next_bits() % 6, w = 3 + dims.next_bits() % 6,
+                      f = 1 + dims.next_bits() % 4, kh = 1 + dims.next_bits() % 3,
+                      kw = 1 + dims.next_bits() % 3;
+        ConvGeometry g;
+        g.stride = 1 + dims.next_bits() % 2;
+        g.pad = dims.next_bits() % 2;
+        if (conv_out_dim(h, kh, g.stride, g.pad) < 1 || conv_out_dim(w, kw, g.stride, g.pad) < 1)
+            continue;
+        const int64_t oh = conv_out_dim(h, kh, g.stride, g.pad), ow = conv_out_dim(w, kw, g.stride, g.pad);
+        const FloatFormat& fm = (trial & 1) ? kFp16 : kFp8;
+        const QuantizedTensor x = fp8emu::quantize(random_tensor({n, c, h, w}, 300 + trial, -2, 2), fm, cfg);
+        const QuantizedTensor k = fp8emu::quantize(random_tensor({f, c, kh, kw}, 400 + trial, -2, 2), fm, cfg);
+        const QuantizedTensor e = fp8emu::quantize(random_tensor({n, f, oh, ow}, 500 + trial, -2, 2), fm, cfg);
+        auto same = [](const Tensor& a, const Tensor& b) {
+            return a.shape == b.shape && std::memcmp(a.data.data(), b.data.data(), 4 * a.data.size()) == 0;
+        };
+        if (!same(fp8emu::conv2d_fp8(x, k, g), fp8emu::b200::conv2d_fp8(x, k, g)))
+            return "conv2d_fp8 differs at trial " + std::to_string(trial);
+        if (!same(fp8emu::conv2d_fp8_im2col(x, k, g), fp8emu::b200::conv2d_fp8_im2col(x, k, g)))
+            return "conv2d_fp8_im2col differs at trial " + std::to_string(trial);
+        if (!same(fp8emu::conv2d_backward_data_fp8(e, k, g, h, w),
+                  fp8emu::b200::conv2d_backward_data_fp8(e, k, g, h, w)))
+            return "conv2d_backward_data_fp8 differs at trial " + std::to_string(trial);
+        if (!same(fp8emu::conv2d_backward_weights_fp8(x, e, kh, kw, g),
+                  fp8emu::b200::conv2d_backward_weights_fp8(x, e, kh, kw, g)))
+            return "conv2d_backward_weights_fp8 differs at trial " + std::to_string(trial);
+        if (fp8emu::im2col(x, kh, kw, g).codes != fp8emu::b200::im2col(x, kh, kw, g).codes)
+            return "im2col differs at trial " + std::to_string(trial);
+    }
+    return "";
+}
+
 static std::string check_errors() {
     Tensor t({4});
     QuantConfig cfg;
@@ -230,6 +269,7 @@ int main() {
     report("gemm_criterion5_bitwise_and_tolerance", check_gemm());
     report("loss_scaler_criterion6", check_scaler());
     report("update_tensor_rne_and_sr", check_update());
+    report("conv_family_bitwise", check_conv());
     report("error_behaviour", check_errors());
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;

@@ -167,6 +167,117 @@ Tensor gemm_fp8_exact(const QuantizedTensor& a, const QuantizedTensor& b) {
     return gemm_impl(a, b, FP8B_GEMM_SEQUENTIAL);
 }
 
+// ---- conv family (kernels.cpp:28-281), NCHW, sequential engine ------------
+namespace {
+
+int64_t out_dim(int64_t in, int64_t k, const ConvGeometry& g) {
+    const int64_t span = in + 2 * g.pad - k;
+    if (span < 0 || g.stride < 1) throw std::invalid_argument("convolution geometry does not fit input");
+    return span / g.stride + 1;
+}
+
+fp8b_conv_t geom_of(int64_t n, int64_t c, int64_t h, int64_t w, int64_t f, int64_t kh, int64_t kw,
+                    const ConvGeometry& g) {
+    fp8b_conv_t cg{};
+    cg.n = n; cg.c = c; cg.h = h; cg.w = w; cg.f = f; cg.kh = kh; cg.kw = kw;
+    cg.stride = g.stride; cg.pad = g.pad;
+    cg.layout = FP8B_NCHW;
+    cg.engine = FP8B_GEMM_SEQUENTIAL;
+    return cg;
+}
+
+using ConvFn = int (*)(const void*, const void*, float*, int32_t, const fp8b_conv_t*, void*);
+
+Tensor run_conv(ConvFn fn, const QuantizedTensor& a, const QuantizedTensor& b,
+                const fp8b_conv_t& cg, std::vector<int64_t> out_shape) {
+    const int fmt = fmt_id(a.fmt);
+    Tensor y(out_shape);
+    if (y.data.empty()) return y;
+    Dev da(a.codes.size() * code_bytes(fmt)), db(b.codes.size() * code_bytes(fmt));
+    Dev dy(sizeof(float) * y.data.size());
+    upload_codes(a, fmt, da.p);
+    upload_codes(b, fmt, db.p);
+    abi_ok(fn(da.p, db.p, dy.as<float>(), fmt, &cg, nullptr));
+    cuda_ok(cudaMemcpy(y.data.data(), dy.p, sizeof(float) * y.data.size(), cudaMemcpyDeviceToHost),
+            "D2H");
+    return y;
+}
+
+}  // namespace
+
+Tensor conv2d_fp8(const QuantizedTensor& x, const QuantizedTensor& w, const ConvGeometry& geom) {
+    if (x.shape.size() != 4 || w.shape.size() != 4)
+        throw std::invalid_argument("conv2d_fp8 expects [N,C,H,W] and [F,C,kH,kW]");
+    if (x.shape[1] != w.shape[1]) throw std::invalid_argument("conv2d_fp8 channel counts disagree");
+    if (!(x.fmt == w.fmt)) throw std::invalid_argument("kernel operands must share one format");
+    const int64_t n = x.shape[0], c = x.shape[1], h = x.shape[2], iw = x.shape[3];
+    const int64_t f = w.shape[0], kh = w.shape[2], kw = w.shape[3];
+    const int64_t oh = out_dim(h, kh, geom), ow = out_dim(iw, kw, geom);
+    return run_conv(fp8b_conv2d_fprop, x, w, geom_of(n, c, h, iw, f, kh, kw, geom), {n, f, oh, ow});
+}
+
+Tensor conv2d_backward_data_fp8(const QuantizedTensor& e, const QuantizedTensor& w,
+                                const ConvGeometry& geom, std::int64_t h, std::int64_t w_dim) {
+    if (e.shape.size() != 4 || w.shape.size() != 4)
+        throw std::invalid_argument("conv backward expects rank-4 operands");
+    if (e.shape[1] != w.shape[0]) throw std::invalid_argument("conv backward filter counts disagree");
+    if (!(e.fmt == w.fmt)) throw std::invalid_argument("kernel operands must share one format");
+    const int64_t n = e.shape[0], f = e.shape[1], c = w.shape[1], kh = w.shape[2], kw = w.shape[3];
+    if (out_dim(h, kh, geom) != e.shape[2] || out_dim(w_dim, kw, geom) != e.shape[3])
+        throw std::invalid_argument("conv backward geometry disagrees with error");
+    return run_conv(fp8b_conv2d_dgrad, e, w, geom_of(n, c, h, w_dim, f, kh, kw, geom), {n, c, h, w_dim});
+}
+
+Tensor conv2d_backward_weights_fp8(const QuantizedTensor& x, const QuantizedTensor& e,
+                                   std::int64_t kh, std::int64_t kw, const ConvGeometry& geom) {
+    if (x.shape.size() != 4 || e.shape.size() != 4 || x.shape[0] != e.shape[0])
+        throw std::invalid_argument("conv backward expects matching rank-4 operands");
+    if (!(x.fmt == e.fmt)) throw std::invalid_argument("kernel operands must share one format");
+    const int64_t n = x.shape[0], c = x.shape[1], h = x.shape[2], iw = x.shape[3], f = e.shape[1];
+    if (out_dim(h, kh, geom) != e.shape[2] || out_dim(iw, kw, geom) != e.shape[3])
+        throw std::invalid_argument("conv backward geometry disagrees with error");
+    return run_conv(fp8b_conv2d_wgrad, x, e, geom_of(n, c, h, iw, f, kh, kw, geom), {f, c, kh, kw});
+}
+
+QuantizedTensor im2col(const QuantizedTensor& x, std::int64_t kh, std::int64_t kw,
+                       const ConvGeometry& geom) {
+    if (x.shape.size() != 4) throw std::invalid_argument("im2col expects [N, C, H, W]");
+    const int64_t n = x.shape[0], c = x.shape[1], h = x.shape[2], iw = x.shape[3];
+    const int64_t oh = out_dim(h, kh, geom), ow = out_dim(iw, kw, geom);
+    const int fmt = fmt_id(x.fmt);
+    QuantizedTensor cols;
+    cols.fmt = x.fmt;
+    cols.mode_used = x.mode_used;
+    cols.shape = {c * kh * kw, n * oh * ow};
+    cols.codes.assign(static_cast<size_t>(cols.shape[0] * cols.shape[1]), 0);
+    if (cols.codes.empty()) return cols;
+    Dev dx(x.codes.size() * code_bytes(fmt)), dc(cols.codes.size() * code_bytes(fmt));
+    upload_codes(x, fmt, dx.p);
+    const fp8b_conv_t cg = geom_of(n, c, h, iw, 1, kh, kw, geom);
+    abi_ok(fp8b_im2col(dx.p, dc.p, fmt, &cg, nullptr));
+    download_codes(dc.p, fmt, cols.codes);
+    return cols;
+}
+
+Tensor conv2d_fp8_im2col(const QuantizedTensor& x, const QuantizedTensor& w,
+                         const ConvGeometry& geom) {
+    // kernels.cpp:255-281: W [F, C*kh*kw] x cols [C*kh*kw, N*OH*OW], then NCHW
+    const int64_t n = x.shape[0];
+    const int64_t f = w.shape[0], c = w.shape[1], kh = w.shape[2], kw = w.shape[3];
+    const int64_t oh = out_dim(x.shape[2], kh, geom), ow = out_dim(x.shape[3], kw, geom);
+    const QuantizedTensor cols = b200::im2col(x, kh, kw, geom);
+    const QuantizedTensor wmat = w.reshaped({f, c * kh * kw});
+    const Tensor flat = gemm_fp8_exact(wmat, cols);
+    Tensor y({n, f, oh, ow});
+    const int64_t ncols = n * oh * ow;
+    for (int64_t ni = 0; ni < n; ++ni)
+        for (int64_t fi = 0; fi < f; ++fi)
+            for (int64_t p = 0; p < oh * ow; ++p)
+                y.data[static_cast<size_t>((ni * f + fi) * oh * ow + p)] =
+                    flat.data[static_cast<size_t>(fi * ncols + ni * oh * ow + p)];
+    return y;
+}
+
 LossScaler::LossScaler(const fp8emu::LossScaler::Options& o) : opts_(o) {
     fp8b_loss_scaler_t h{};
     h.kind = o.kind == fp8emu::LossScaler::Kind::Constant ? FP8B_SCALER_CONSTANT

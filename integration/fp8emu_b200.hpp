@@ -15,6 +15,9 @@
 //                                              fp8emu::b200::gemm_fp8_exact (bitwise order)
 //   fp8emu::LossScaler      loss_scaling.hpp   fp8emu::b200::LossScaler     (state in HBM)
 //   update_tensor           nn.cpp:417-432     fp8emu::b200::update_tensor
+//   fp8emu::conv2d_fp8 ...  kernels.hpp:22-50  fp8emu::b200::conv2d_fp8, im2col,
+//                                              conv2d_fp8_im2col, conv2d_backward_data_fp8,
+//                                              conv2d_backward_weights_fp8 (NCHW, bitwise)
 #pragma once
 
 #include <cstdint>
@@ -33,6 +36,17 @@ Tensor dequantize(const QuantizedTensor& q);
 QuantizedTensor transpose(const QuantizedTensor& q);
 Tensor gemm_fp8(const QuantizedTensor& a, const QuantizedTensor& b);
 Tensor gemm_fp8_exact(const QuantizedTensor& a, const QuantizedTensor& b);
+
+// The conv family in the reference's NCHW layout and summation order (bitwise).
+Tensor conv2d_fp8(const QuantizedTensor& x, const QuantizedTensor& w, const ConvGeometry& geom);
+QuantizedTensor im2col(const QuantizedTensor& x, std::int64_t kh, std::int64_t kw,
+                       const ConvGeometry& geom);
+Tensor conv2d_fp8_im2col(const QuantizedTensor& x, const QuantizedTensor& w,
+                         const ConvGeometry& geom);
+Tensor conv2d_backward_data_fp8(const QuantizedTensor& e, const QuantizedTensor& w,
+                                const ConvGeometry& geom, std::int64_t h, std::int64_t w_dim);
+Tensor conv2d_backward_weights_fp8(const QuantizedTensor& x, const QuantizedTensor& e,
+                                   std::int64_t kh, std::int64_t kw, const ConvGeometry& geom);
 
 class LossScaler {
 public:

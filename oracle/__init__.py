@@ -498,3 +498,72 @@ def bitrev16(v: int) -> int:
     for i in range(16):
         r |= ((v >> i) & 1) << (15 - i)
     return r
+
+
+# ---- FP8T container through the reference's own tensor_io.cpp -------------
+def _ref_io():
+    r = ref()
+    if not getattr(r, "_io_ready", False):
+        r.ref_fp8t_save_f32.restype = C.c_int
+        r.ref_fp8t_save_f32.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_char_p]
+        r.ref_fp8t_save_codes.restype = C.c_int
+        r.ref_fp8t_save_codes.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                          C.c_void_p, C.c_char_p]
+        r.ref_fp8t_load_f32.restype = C.c_int
+        r.ref_fp8t_load_f32.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                        C.c_char_p]
+        r.ref_fp8t_load_codes.restype = C.c_int
+        r.ref_fp8t_load_codes.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_char_p]
+        r._io_ready = True
+    return r
+
+
+class RefIoError(RuntimeError):
+    pass
+
+
+def _dims64(shape):
+    return np.ascontiguousarray(np.asarray(list(shape) or [0], dtype=np.int64))
+
+
+def ref_fp8t_save_f32(path, arr):
+    a = np.asarray(arr, dtype=np.float32)
+    flat = np.ascontiguousarray(a.reshape(-1))  # (ascontiguousarray promotes 0-d to 1-d)
+    d, msg = _dims64(a.shape), C.create_string_buffer(256)
+    rc = _ref_io().ref_fp8t_save_f32(os.fsencode(path), a.ndim, d.ctypes.data, flat.ctypes.data, msg)
+    if rc:
+        raise RefIoError(msg.value.decode())
+
+
+def ref_fp8t_save_codes(path, codes, shape, fmt="fp8", mode_tag=1):
+    c = np.ascontiguousarray(np.asarray(codes, dtype=np.uint16).reshape(-1))
+    d, msg = _dims64(shape), C.create_string_buffer(256)
+    rc = _ref_io().ref_fp8t_save_codes(os.fsencode(path), FMT[fmt], mode_tag, len(shape),
+                                       d.ctypes.data, c.ctypes.data, msg)
+    if rc:
+        raise RefIoError(msg.value.decode())
+
+
+def ref_fp8t_load_f32(path, cap=1 << 20):
+    out = np.empty(cap, dtype=np.float32)
+    rank, dims, msg = C.c_int(), np.zeros(16, dtype=np.int64), C.create_string_buffer(256)
+    rc = _ref_io().ref_fp8t_load_f32(os.fsencode(path), out.ctypes.data, cap, C.addressof(rank),
+                                     dims.ctypes.data, msg)
+    if rc:
+        raise RefIoError(msg.value.decode())
+    shape = [int(v) for v in dims[:rank.value]]
+    return out[:int(np.prod(shape)) if shape else 1].reshape(shape)
+
+
+def ref_fp8t_load_codes(path, cap=1 << 20):
+    out = np.empty(cap, dtype=np.uint16)
+    fmt, mode, rank = C.c_int(), C.c_int(), C.c_int()
+    dims, msg = np.zeros(16, dtype=np.int64), C.create_string_buffer(256)
+    rc = _ref_io().ref_fp8t_load_codes(os.fsencode(path), out.ctypes.data, cap, C.addressof(fmt),
+                                       C.addressof(mode), C.addressof(rank), dims.ctypes.data, msg)
+    if rc:
+        raise RefIoError(msg.value.decode())
+    shape = [int(v) for v in dims[:rank.value]]
+    n = int(np.prod(shape)) if shape else 1
+    return out[:n].reshape(shape), ("fp8" if fmt.value == 0 else "fp16"), mode.value

@@ -1,7 +1,7 @@
 // ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.
 //
 // A thin extern "C" shim over the UNMODIFIED reference library
-// (/root/reference/proj/src/{lfsr,float_format,tensor,kernels,loss_scaling}.cpp,
+// (/root/reference/proj/src/{lfsr,float_format,tensor,kernels,loss_scaling,tensor_io}.cpp,
 // compiled in place by oracle/Makefile into oracle/_ref/libfp8emu_ref.so).
 // It lets the pytest suite and bench.py's reference arm drive the reference's
 // public C++ API through ctypes. Nothing here is product code.
@@ -24,6 +24,7 @@
 #include "fp8emu/loss_scaling.hpp"
 #include "fp8emu/rand.hpp"
 #include "fp8emu/tensor.hpp"
+#include "fp8emu/tensor_io.hpp"
 
 using namespace fp8emu;
 
@@ -289,6 +290,69 @@ void ref_rand_fill_normal(uint64_t* st_seed_n, int* have_spare, double* spare,
     st_seed_n[1] = r.n;
     *have_spare = r.have_spare;
     *spare = r.spare;
+}
+
+// FP8T container (tensor_io.cpp): save/load through the reference's own code.
+// Errors come back as 5 with the IoError message copied into msg (256 bytes).
+static int io_err(const std::exception& e, char* msg) {
+    std::strncpy(msg, e.what(), 255);
+    msg[255] = 0;
+    return 5;
+}
+int ref_fp8t_save_f32(const char* path, int rank, const int64_t* dims, const float* data, char* msg) {
+    try {
+        Tensor t(std::vector<int64_t>(dims, dims + rank));
+        std::memcpy(t.data.data(), data, sizeof(float) * t.data.size());
+        save_tensor(path, t);
+        return 0;
+    } catch (const std::exception& e) {
+        return io_err(e, msg);
+    }
+}
+int ref_fp8t_save_codes(const char* path, int fmt, int mode, int rank, const int64_t* dims,
+                        const uint16_t* codes, char* msg) {
+    try {
+        QuantizedTensor q;
+        q.shape.assign(dims, dims + rank);
+        q.fmt = fmt == 0 ? kFp8 : kFp16;
+        q.mode_used = mode == 2 ? RoundingMode::Stochastic
+                    : mode == 3 ? RoundingMode::TruncateTowardZero
+                                : RoundingMode::NearestEven;
+        q.codes.assign(codes, codes + shape_numel(q.shape));
+        save_tensor(path, q);
+        return 0;
+    } catch (const std::exception& e) {
+        return io_err(e, msg);
+    }
+}
+// returns 0 and fills out (capacity elements) / shape
+int ref_fp8t_load_f32(const char* path, float* out, int64_t cap, int* rank, int64_t* dims, char* msg) {
+    try {
+        const Tensor t = load_tensor_fp32(path);
+        if ((int64_t)t.data.size() > cap) return 7;
+        std::memcpy(out, t.data.data(), sizeof(float) * t.data.size());
+        *rank = (int)t.shape.size();
+        for (size_t i = 0; i < t.shape.size() && i < 16; ++i) dims[i] = t.shape[i];
+        return 0;
+    } catch (const std::exception& e) {
+        return io_err(e, msg);
+    }
+}
+int ref_fp8t_load_codes(const char* path, uint16_t* out, int64_t cap, int* fmt, int* mode, int* rank,
+                        int64_t* dims, char* msg) {
+    try {
+        const QuantizedTensor q = load_tensor_codes(path);
+        if ((int64_t)q.codes.size() > cap) return 7;
+        std::memcpy(out, q.codes.data(), sizeof(uint16_t) * q.codes.size());
+        *fmt = q.fmt == kFp8 ? 0 : 1;
+        *mode = q.mode_used == RoundingMode::Stochastic ? 2
+              : q.mode_used == RoundingMode::TruncateTowardZero ? 3 : 1;
+        *rank = (int)q.shape.size();
+        for (size_t i = 0; i < q.shape.size() && i < 16; ++i) dims[i] = q.shape[i];
+        return 0;
+    } catch (const std::exception& e) {
+        return io_err(e, msg);
+    }
 }
 
 }  // extern "C"

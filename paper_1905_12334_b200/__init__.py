@@ -33,7 +33,7 @@ __all__ = [
     "QuantizedTensor", "ScaleEvent", "LossScaler", "quantize", "dequantize", "transpose",
     "gemm", "gemm_codes", "encode", "decode", "sgd_momentum_update", "bias_grad",
     "count_nonfinite", "fill_synthetic", "Counters", "launch_count", "version",
-    "conv2d", "conv2d_backward_data", "conv2d_backward_weights", "im2col", "conv_out_dim", "conv_tensor_supported",
+    "conv2d", "conv2d_backward_data", "conv2d_backward_weights", "im2col", "conv_out_dim", "conv_tensor_supported", "conv2d_im2col",
 ]
 
 _FMT = {"fp8": _lib.E5M2, "FP8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16,
@@ -369,6 +369,21 @@ def conv2d_backward_weights(x: QuantizedTensor, e: QuantizedTensor, kh: int, kw:
     return dw
 
 
+def conv2d_im2col(x: QuantizedTensor, w: QuantizedTensor, stride: int = 1, pad: int = 0, *,
+                  engine: str = "sequential", stream=None) -> torch.Tensor:
+    """conv2d_fp8_im2col (kernels.cpp:255-281): im2col + gemm_fp8, NCHW. With the
+    sequential engine it is bitwise equal to conv2d (the reference's own check,
+    test_kernels.cpp:97-118)."""
+    if len(x.shape) != 4 or len(w.shape) != 4:
+        raise ValueError("conv2d_fp8 expects [N,C,H,W] and [F,C,kH,kW]")
+    n = x.shape[0]
+    f, c, kh, kw = w.shape
+    oh, ow = conv_out_dim(x.shape[2], kh, stride, pad), conv_out_dim(x.shape[3], kw, stride, pad)
+    cols = im2col(x, kh, kw, stride, pad, stream=stream)
+    flat = gemm(w.reshaped([f, c * kh * kw]), cols, engine=engine, stream=stream)  # [F, N*OH*OW]
+    return flat.reshape(f, n, oh, ow).permute(1, 0, 2, 3).contiguous()
+
+
 def conv_tensor_supported(n, c, h, w, f, k, stride=1, pad=0, fmt="fp8", kind="fprop",
                           layout="nhwc") -> bool:
     """True if engine="tensor" runs this conv on tcgen05 (else the sequential engine)."""
@@ -488,6 +503,18 @@ class LossScaler:
         self.step_async(grads_finite, iteration)
         s = self._read()
         return ScaleEvent(int(s.last_iteration), _ACTION[s.last_action], s.last_scale_after)
+
+    def state_dict(self) -> dict:
+        """Device scaler state as a JSON-able dict (checkpoint extension)."""
+        s = self._read()
+        return {"kind": self.kind, "scale": s.scale, "steps_since_overflow": s.steps_since_overflow,
+                "raw": self.state.cpu().numpy().tobytes().hex()}
+
+    def load_state_dict(self, d: dict) -> None:
+        raw = np.frombuffer(bytes.fromhex(d["raw"]), dtype=np.uint8)
+        if raw.size != self.state.numel():
+            raise ValueError("scaler state size mismatch")
+        self.state.copy_(torch.from_numpy(raw.copy()))
 
     def unscale(self, gradients) -> torch.Tensor:
         g = _device_f32(gradients).clone()
@@ -631,6 +658,18 @@ class DenseLayer:
         self._s.iteration = int(iteration)
         check(LIB.fp8b_dense_step(self._s, _stream(stream)), "dense_step")
 
+    def refresh_fprop_weights(self) -> None:
+        """Re-derive the fprop E5M2 weights Q(decode(master)) (nn.cpp:192) and the
+        FP32 bias value decode(b_master) after the masters were replaced."""
+        I, O = self.in_features, self.out_features
+        dev = self.w_master.device
+        wdec = dequantize(QuantizedTensor(self.w_master.reshape(-1), [I * O], _lib.FP16, _lib.RNE,
+                                          Counters(dev)))
+        quantize(wdec, "fp8", out=self.w_q.view(-1))
+        if self.has_bias:
+            self.b_value.copy_(dequantize(QuantizedTensor(self.b_master.reshape(-1), [O], _lib.FP16,
+                                                          _lib.RNE, Counters(dev))))
+
     # step statistics (synchronise)
     def overflow_count(self) -> int:
         c = self.counters.tolist()
@@ -642,3 +681,10 @@ class DenseLayer:
 
     def underflow_fraction(self) -> float:
         return float(self.counters[4].item()) / float(self.in_features * self.out_features)
+
+
+from . import fp8t  # noqa: E402  (FP8T files and checkpoints)
+from .fp8t import (IoError, load_checkpoint, load_tensor_codes, load_tensor_fp32,  # noqa: E402
+                   peek_tensor_dtype, save_checkpoint, save_tensor)
+__all__ += ["fp8t", "IoError", "save_tensor", "load_tensor_fp32", "load_tensor_codes",
+            "peek_tensor_dtype", "save_checkpoint", "load_checkpoint"]

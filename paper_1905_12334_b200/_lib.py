@@ -12,7 +12,9 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfp8b200.so")
 
-OK, EINVAL, ENOTSUP, ECUDA = 0, 22, 95, 1000
+OK, EINVAL, ENOTSUP, ECUDA, EIO = 0, 22, 95, 1000, 5
+FP8T_F32, FP8T_FP8, FP8T_FP16 = 0, 1, 2
+FP8T_MAX_RANK = 255
 E5M2, FP16, F32 = 0, 1, 2
 RNE, SR, TRUNC = 0, 1, 2
 BITS_LFSR, BITS_COUNTER, BITS_SUPPLIED = 0, 1, 2
@@ -90,6 +92,9 @@ SIGNATURES = {
     "fp8b_conv2d_wgrad": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
     "fp8b_conv_tensor_supported": (C.c_int, [C.POINTER(ConvGeom), _i32, _i32]),
     "fp8b_im2col": (C.c_int, [_vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
+    "fp8b_fp8t_save": (C.c_int, [C.c_char_p, _i32, _i32, _i32, _vp, _vp]),
+    "fp8b_fp8t_peek": (C.c_int, [C.c_char_p, _vp, _vp, _vp, _vp, _i32]),
+    "fp8b_fp8t_load": (C.c_int, [C.c_char_p, _i32, _vp, _i64]),
     "fp8b_dense_step": (C.c_int, [C.POINTER(DenseStep), _vp]),
     "fp8b_init": (C.c_int, []),
     "fp8b_last_error": (C.c_char_p, []),
@@ -120,10 +125,16 @@ class Fp8bError(RuntimeError):
     pass
 
 
+class IoError(RuntimeError):
+    """fp8emu::IoError (tensor_io.hpp:13-15): unreadable or garbled files."""
+
+
 def check(rc: int, what: str = "") -> None:
     if rc == OK:
         return
     msg = LIB.fp8b_last_error().decode(errors="replace")
     if rc == EINVAL:
         raise ValueError(f"{what}: {msg}" if what else msg)
+    if rc == EIO:
+        raise IoError(msg)
     raise Fp8bError(f"{what}: [{rc}] {msg}" if what else f"[{rc}] {msg}")

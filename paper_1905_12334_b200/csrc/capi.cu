@@ -92,6 +92,7 @@ bool valid_bits(int32_t b) { return b == FP8B_BITS_LFSR || b == FP8B_BITS_COUNTE
 
 namespace fp8b {
 void note_launches(int n) { g_launches += n; }
+void set_error(const std::string& msg) { g_err = msg; }
 }  // namespace fp8b
 
 extern "C" {

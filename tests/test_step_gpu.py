@@ -166,3 +166,38 @@ def test_step_cuda_graph_replay(fp8, inputs):
     La.step(xs, es, 1)
     torch.cuda.synchronize()
     assert torch.equal(La.w_master, Lb.w_master) and torch.equal(La.w_q, Lb.w_q)
+
+
+def test_checkpoint_resume_is_exact(fp8, inputs, tmp_path):
+    """save_checkpoint/load_checkpoint (nn.cpp:632-701) + momentum and scaler
+    state (extension): a resumed layer continues bit for bit."""
+    import torch
+    X, W, E = inputs
+    xs, es = torch.from_numpy(X).cuda(), torch.from_numpy(E).cuda()
+    sa = fp8.LossScaler("dynamic-backoff", 8192.0, growth_interval=2,
+                        min_threshold_schedule=[(0, 4096.0)])
+    A = fp8.DenseLayer(torch.from_numpy(W.reshape(1024, 1024)).cuda(), torch.zeros(1024).cuda(),
+                       batch=512, lr=0.1, mu=0.9, scaler=sa, engine="tensor",
+                       master_mode="stochastic", seed=3)
+    for it in range(3):
+        A.step(xs, es, it)
+    torch.cuda.synchronize()
+    fp8.save_checkpoint([A], tmp_path, scaler=sa)
+    assert (tmp_path / "manifest.txt").read_text().startswith("layer 0 kind=dense precision=fp8")
+    # the master file is a reference-readable FP16 code tensor
+    codes, fmt, _ = O.ref_fp8t_load_codes(tmp_path / "layer0_w.fp8t", cap=1 << 21)
+    assert fmt == "fp16" and codes.shape == (1024, 1024)
+    np.testing.assert_array_equal(codes.reshape(-1), A.w_master.cpu().numpy().view(np.uint16).reshape(-1))
+    sb = fp8.LossScaler("dynamic-backoff", 1.0, growth_interval=2,
+                        min_threshold_schedule=[(0, 4096.0)])
+    B = fp8.DenseLayer(torch.zeros(1024, 1024).cuda(), torch.ones(1024).cuda(), batch=512, lr=0.1,
+                       mu=0.9, scaler=sb, engine="tensor", master_mode="stochastic", seed=3)
+    fp8.load_checkpoint([B], tmp_path, scaler=sb)
+    assert sb.scale == sa.scale
+    for it in range(3, 6):
+        A.step(xs, es, it)
+        B.step(xs, es, it)
+    torch.cuda.synchronize()
+    assert torch.equal(A.w_master, B.w_master) and torch.equal(A.w_momentum, B.w_momentum)
+    assert torch.equal(A.b_master, B.b_master) and torch.equal(A.w_q, B.w_q)
+    assert sa.scale == sb.scale

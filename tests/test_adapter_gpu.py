@@ -16,4 +16,4 @@ def test_cpp_dropin_matches_reference():
     out = subprocess.run([EXE], capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count("PASS") == 6
+    assert out.stdout.count("PASS") == 7 and "FAIL" not in out.stdout

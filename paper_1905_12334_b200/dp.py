@@ -13,6 +13,13 @@
   update together (nn.cpp:546), and every rank applies the identical update to
   its replica of the FP16 masters.
 
+* ``ZeroDataParallelDense`` (ZeRO stage 1): the FP32 partial dW
+  are reduce-scattered instead of all-reduced; each rank owns a block-aligned
+  shard of the FP16 masters and momentum, runs Q(dW) and the update on it
+  (``block_offset`` keeps the SR streams those of the unsharded update) and
+  the E5M2 fprop weights are all-gathered: 4 + 1 bytes per parameter on the
+  wire instead of 8, and 6/world bytes of optimizer state per parameter.
+
 The arithmetic goes through an ``ops`` object; the default is this library's
 CUDA kernels (``GpuOps``). Tests substitute a CPU implementation to cover the
 multi-process orchestration with world_size 2 over gloo.
@@ -65,10 +72,10 @@ class GpuOps:
         return cq
 
     def update(self, qdw, master, momentum, *, lr, mu, two_lambda, scaler, skip_counters,
-               master_mode, seed, w_e5m2=None):
+               master_mode, seed, w_e5m2=None, block_offset=0):
         self._u(qdw, "fp8", master, momentum, lr=lr, mu=mu, two_lambda=two_lambda,
                 scaler=scaler, skip_counters=skip_counters, master_mode=master_mode, seed=seed,
-                w_e5m2=w_e5m2)
+                w_e5m2=w_e5m2, block_offset=block_offset)
 
 
 class DataParallelDense:
@@ -115,3 +122,90 @@ class DataParallelDense:
         if self.scaler is not None and hasattr(self.scaler, "step_async"):
             self.scaler.step_async(True, iteration, counters=bwd)
         return qy, qdx, gate
+
+
+class ZeroDataParallelDense:
+    """Batch-sharded Dense layer with ZeRO-1 sharded optimizer state.
+
+    Every rank keeps the full E5M2 fprop weights ``w_q`` [in, out]; the FP16
+    masters and FP32 momentum exist only for this rank's block-aligned shard
+    ``[start, end)`` of the flattened weights (block_shard). Per step:
+    forward / Q(e) / bprop / FP32 wgrad on the local batch, reduce-scatter of
+    the FP32 dW (padded to whole equal shards), Q(dW) and the gated update on
+    the shard, all-reduce of the overflow gate, all-gather of the E5M2 shards.
+    Bitwise equal to ``DataParallelDense`` (same FP32 sum order per element)."""
+
+    def __init__(self, w_master_full, w_q, *, batch_per_rank: int, lr: float, mu: float,
+                 two_lambda: float = 0.0, scaler=None, ops=None, group=None,
+                 master_mode: str = "nearest-even", seed: int = 1):
+        self.ops = ops or GpuOps()
+        self.group = group
+        distributed = dist.is_initialized()
+        self.world = dist.get_world_size(group) if distributed else 1
+        self.rank = dist.get_rank(group) if distributed else 0
+        self.in_f, self.out_f = w_q.shape
+        n = self.in_f * self.out_f
+        self.n = n
+        nblocks = (n + BLOCK - 1) // BLOCK
+        self.per = ((nblocks + self.world - 1) // self.world) * BLOCK   # padded shard length
+        self.start, self.end, self.block_offset = block_shard(n, self.world, self.rank)
+        dev = w_q.device
+        self.w_q = w_q                                                   # E5M2 [in, out]
+        self.w_master = w_master_full.reshape(-1)[self.start:self.end].clone()   # FP16 shard
+        self.momentum = torch.zeros(self.end - self.start, dtype=torch.float32, device=dev)
+        self.bpr = batch_per_rank
+        self.lr, self.mu, self.two_lambda = lr, mu, two_lambda
+        self.scaler = scaler
+        self.master_mode, self.seed = master_mode, seed
+        self._wq_pad = torch.zeros(self.per * self.world, dtype=w_q.dtype, device=dev)
+
+    def step(self, x_local, e_local, iteration: int):
+        B, I, O = self.bpr, self.in_f, self.out_f
+        ops = self.ops
+        fwd, bwd = ops.counters(), ops.counters()
+        multi = self.world > 1
+        qx = ops.quantize(x_local.reshape(-1), counters=fwd)
+        qy = ops.gemm_q(qx, self.w_q, B, O, I, "k", "n", counters=fwd)
+        qe = ops.quantize(e_local.reshape(-1), counters=bwd)
+        dw = ops.gemm_f32(qx, qe, I, O, B, "m", "n").reshape(-1)
+        qdx = ops.gemm_q(qe, self.w_q, B, I, O, "k", "k", counters=bwd)
+        full = torch.zeros(self.per * self.world, dtype=torch.float32, device=dw.device)
+        full[: self.n] = dw
+        shard = torch.empty(self.per, dtype=torch.float32, device=dw.device)
+        if multi:
+            dist.reduce_scatter_tensor(shard, full, op=dist.ReduceOp.SUM, group=self.group)
+        else:
+            shard.copy_(full)
+        ns = self.end - self.start
+        qdw = ops.quantize(shard[:ns].contiguous(), block_offset=self.block_offset, counters=bwd) \
+            if ns else shard[:0].to(torch.uint8)
+        gate = ops.ctensor(bwd)
+        if multi:
+            dist.all_reduce(gate, op=dist.ReduceOp.SUM, group=self.group)
+        wq_shard = self._wq_pad[self.rank * self.per: self.rank * self.per + ns]
+        if ns:
+            wq_shard.copy_(self.w_q.reshape(-1)[self.start:self.end])
+            ops.update(qdw, self.w_master, self.momentum, lr=self.lr, mu=self.mu,
+                       two_lambda=self.two_lambda, scaler=self.scaler, skip_counters=bwd,
+                       master_mode=self.master_mode, seed=self.seed, w_e5m2=wq_shard,
+                       block_offset=self.block_offset)
+        if multi:
+            # bytes moved as int32 words (shards are whole 4096-blocks): gloo has
+            # no uint8 all-gather, NCCL does not care
+            mine = self._wq_pad[self.rank * self.per:(self.rank + 1) * self.per].clone()
+            dist.all_gather_into_tensor(self._wq_pad.view(torch.int32), mine.view(torch.int32),
+                                        group=self.group)
+        self.w_q.reshape(-1).copy_(self._wq_pad[: self.n])
+        if self.scaler is not None and hasattr(self.scaler, "step_async"):
+            self.scaler.step_async(True, iteration, counters=bwd)
+        return qy, qdx, gate
+
+    def gather_masters(self):
+        """The full FP16 masters (for checks and checkpoints): all-gather of shards."""
+        pad = torch.zeros(self.per, dtype=self.w_master.dtype, device=self.w_master.device)
+        pad[: self.end - self.start] = self.w_master
+        if self.world == 1:
+            return pad[: self.n].reshape(self.in_f, self.out_f)
+        out = torch.empty(self.per * self.world, dtype=pad.dtype, device=pad.device)
+        dist.all_gather_into_tensor(out.view(torch.int32), pad.view(torch.int32), group=self.group)
+        return out[: self.n].reshape(self.in_f, self.out_f)

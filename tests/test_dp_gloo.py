@@ -16,7 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle as O
-from paper_1905_12334_b200.dp import DataParallelDense, block_shard
+from paper_1905_12334_b200.dp import DataParallelDense, ZeroDataParallelDense, block_shard
 
 
 class CpuOps:
@@ -51,12 +51,13 @@ class CpuOps:
                              counters=counters)
 
     def update(self, qdw, master, momentum, *, lr, mu, two_lambda, scaler, skip_counters,
-               master_mode, seed, w_e5m2=None):
+               master_mode, seed, w_e5m2=None, block_offset=0):
         if int(skip_counters[0] + skip_counters[2]) != 0:
             return
         m1, mo1, _, _ = O.sgd_update(master.numpy().view(np.uint16), momentum.numpy(),
                                      O.dequantize(qdw.numpy().astype(np.uint16)), scaler.scale,
-                                     lr, mu, np.float32(two_lambda), master_mode, "lfsr", seed)
+                                     lr, mu, np.float32(two_lambda), master_mode, "lfsr", seed,
+                                     block_offset=block_offset)
         master.copy_(torch.from_numpy(m1.view(np.int16)))
         momentum.copy_(torch.from_numpy(mo1))
         if w_e5m2 is not None:
@@ -99,6 +100,27 @@ def _worker(rank, world, port, mode, out):
             gathered = [None] * world
             dist.all_gather_object(gathered, codes)
             out[rank] = np.concatenate(gathered)
+        elif mode.startswith("zero"):
+            B, I, O_ = 8, 64, 200  # 12800 params: uneven block shards (2 + 1.125 blocks)
+            x, w, e = _data(B, I, O_, seed=3)
+            mm = "stochastic" if mode.endswith("sr") else "nearest-even"
+            if mode.endswith("overflow") and rank == 0:
+                e = e * np.float32(1e6)
+            m0, _ = O.quantize(w, "fp16")
+            wq, _ = O.quantize(O.dequantize(m0, "fp16"))
+            bpr = B // world
+            layer = ZeroDataParallelDense(
+                torch.from_numpy(m0.view(np.int16).reshape(I, O_)).clone(),
+                torch.from_numpy(wq.astype(np.uint8).reshape(I, O_)).clone(),
+                batch_per_rank=bpr, lr=0.25, mu=0.5, scaler=ConstScale(1.0), ops=CpuOps(),
+                master_mode=mm, seed=9)
+            xs = torch.from_numpy(x.reshape(B, I)[rank * bpr:(rank + 1) * bpr].copy())
+            es = torch.from_numpy(e.reshape(B, O_)[rank * bpr:(rank + 1) * bpr].copy())
+            for it in range(2):
+                qy, qdx, gate = layer.step(xs, es, it)
+            out[rank] = (layer.gather_masters().numpy().copy(), layer.w_q.numpy().copy(),
+                         qdx.numpy().copy(), gate.numpy().copy(),
+                         (layer.start, layer.end, layer.block_offset))
         else:
             B, I, O_ = 8, 64, 32
             x, w, e = _data(B, I, O_)
@@ -181,3 +203,54 @@ def test_block_shard_partition():
                 assert s == min(b0 * 4096, n) and (s % 4096 == 0 or s == n)
                 covered += list(range(s, e))
             assert covered == list(range(n))
+
+
+def _zero_reference(master_mode, steps=2):
+    """Single-process recipe for the ZeRO test (two steps, same batch)."""
+    B, I, O_ = 8, 64, 200
+    x, w, e = _data(B, I, O_, seed=3)
+    m, _ = O.quantize(w, "fp16")
+    mom = np.zeros(I * O_, np.float32)
+    qx, _ = O.quantize(x)
+    qe, _ = O.quantize(e)
+    for _ in range(steps):
+        qw, _ = O.quantize(O.dequantize(m, "fp16"))
+        qdw, _ = O.quantize(O.gemm(qx.reshape(B, I).T.copy(), qe, I, B, O_))
+        m, mom, _, _ = O.sgd_update(m, mom, O.dequantize(qdw), 1.0, 0.25, 0.5,
+                                    master_mode=master_mode, seed=9)
+    qw, _ = O.quantize(O.dequantize(m, "fp16"))
+    return m, qw
+
+
+def test_zero1_step_equals_single_process_rne():
+    res = _run("zero_rne")
+    m, qw = _zero_reference("nearest-even")
+    shards = sorted(res[r][4] for r in range(2))
+    assert shards == [(0, 8192, 0), (8192, 12800, 2)]
+    for r in range(2):
+        wm, wq, _, gate = res[r][:4]
+        np.testing.assert_array_equal(wm.reshape(-1).view(np.uint16), m)
+        np.testing.assert_array_equal(wq.reshape(-1), qw)
+        assert gate[0] == 0 and gate[2] == 0
+
+
+def test_zero1_step_sr_master_stream_is_unsharded():
+    """Each shard's SR update draws the unsharded LFSR block streams (block_offset)."""
+    res = _run("zero_sr")
+    m, qw = _zero_reference("stochastic")
+    for r in range(2):
+        wm, wq = res[r][:2]
+        np.testing.assert_array_equal(wm.reshape(-1).view(np.uint16), m)
+        np.testing.assert_array_equal(wq.reshape(-1), qw)
+
+
+def test_zero1_overflow_on_one_rank_skips_all_shards():
+    res = _run("zero_overflow")
+    _, w, _ = _data(8, 64, 200, seed=3)
+    m0, _ = O.quantize(w, "fp16")
+    qw0, _ = O.quantize(O.dequantize(m0, "fp16"))
+    for r in range(2):
+        wm, wq, _, gate = res[r][:4]
+        assert gate[0] > 0
+        np.testing.assert_array_equal(wm.reshape(-1).view(np.uint16), m0)
+        np.testing.assert_array_equal(wq.reshape(-1), qw0)

@@ -13,6 +13,8 @@
 //                        lookup in the decimated-cycle table.
 #include <type_traits>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -181,161 +183,117 @@ __device__ __forceinline__ void store4(void* codes, int64_t i0, const uint32_t (
     }
 }
 
-// Staged kernel over full blocks, one CTA (NG groups of 256 threads) per SM.
-// Shared memory holds the whole decimated jump table (128 KB, loaded once per
-// CTA by the TMA engine, so every sample is a 32-bit-addressed LDS) and, per
-// group, an S-deep ring of 16 KB input blocks streamed by cp.async.bulk +
-// mbarrier. Each group scans and rounds its own block with a named barrier,
-// so the groups' barrier waits overlap.
-// Phase 1 (per element): overflow/NaN screen, packed value P, inexact flag ->
-// stream increment. Scan. Phase 2: sample, code = (P + r16) >> 16.
-constexpr int kLfsrStages = 2;
-constexpr int kLfsrGroups = 3;
-constexpr int kTabBytesPad = 65536 * 2;  // 65535 entries, no wrap extension
-constexpr int kLfsrSmem = kTabBytesPad + kLfsrGroups * kLfsrStages * kBlock * 4;
+// Warp-per-block kernel over full blocks (the default LFSR path). Each warp
+// owns whole 4096-element blocks, so the stream ranks need no CTA barrier: the
+// warp walks its block in 16 chunks of 256 elements (8 per lane, lane l holding
+// elements [256c + 8l, 256c + 8l + 8) -- one coalesced 1 KB load per chunk,
+// prefetched one chunk ahead from HBM), ranks the chunk's inexact elements with
+// a 5-step shuffle scan of the per-lane counts on top of a running count, and
+// reads its samples from the jump table kept in shared memory. The table copy
+// carries the 4096-entry wrap extension, so no modular addressing is needed.
+constexpr int kWarpLfsrThreads = 768;
+constexpr int kTabWrapBytes = ((kLfsrPeriod + kBlock) * 2 + 15) & ~15;  // 139264
 template <int MB>
-__global__ void __launch_bounds__(256 * kLfsrGroups, 1)
-    quant_lfsr_staged_kernel(const float* __restrict__ x, void* __restrict__ codes, int64_t nfull,
-                             uint64_t seed, int saturate, int64_t block_offset, LfsrTables tabs,
-                             int64_t* counters) {
-    constexpr int S = kLfsrStages, NG = kLfsrGroups;
+__global__ void __launch_bounds__(kWarpLfsrThreads, 1)
+    quant_lfsr_warp_kernel(const float* __restrict__ x, void* __restrict__ codes, int64_t nfull,
+                           uint64_t seed, int saturate, int64_t block_offset, LfsrTables tabs,
+                           int64_t* counters) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint16_t* stab = reinterpret_cast<uint16_t*>(smem);
-    __shared__ __align__(8) uint64_t full[NG][S];
     __shared__ __align__(8) uint64_t tab_bar;
-    __shared__ uint32_t smem_w[NG][2][8];
-    __shared__ uint32_t p0s[NG][2];  // stream start of the group's current / next block
     const bool sat = saturate != 0;
     const uint32_t special = special_packed<MB>(sat);
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
-    const int g = threadIdx.x >> 8, t = threadIdx.x & 255;
-    uint8_t* ring = smem + kTabBytesPad + g * S * kBlock * 4;
-    const int64_t gid = (int64_t)blockIdx.x * NG + g, gstride = (int64_t)gridDim.x * NG;
-    const int nmine = nfull > gid ? (int)((nfull - 1 - gid) / gstride + 1) : 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * kWarpLfsrThreads + threadIdx.x) >> 5;
+    const int64_t wstride = ((int64_t)gridDim.x * kWarpLfsrThreads) >> 5;
     if (threadIdx.x == 0) {
         mbar_init(&tab_bar, 1);
-        for (int gg = 0; gg < NG; ++gg)
-            for (int s = 0; s < S; ++s) mbar_init(&full[gg][s], 1);
         mbar_fence_init();
-        mbar_expect_tx(&tab_bar, kTabBytesPad);
-        for (int off = 0; off < kTabBytesPad; off += 16384)
-            bulk_g2s(smem + off, reinterpret_cast<const uint8_t*>(tabs.tabx) + off, 16384, &tab_bar);
+        mbar_expect_tx(&tab_bar, kTabWrapBytes);
+        for (int off = 0; off < kTabWrapBytes; off += 16384) {
+            const int len = kTabWrapBytes - off < 16384 ? kTabWrapBytes - off : 16384;
+            bulk_g2s(smem + off, reinterpret_cast<const uint8_t*>(tabs.tabx) + off, len, &tab_bar);
+        }
     }
     __syncthreads();
-    if (t == 0) {
-        for (int i = 0; i < S - 1 && i < nmine; ++i) {
-            const int64_t b = gid + i * gstride;
-            mbar_expect_tx(&full[g][i], kBlock * 4);
-            bulk_g2s(ring + i * kBlock * 4, x + b * kBlock, kBlock * 4, &full[g][i]);
-        }
-    }
-    const uint32_t stab_addr = smem_addr(stab);
-    // one thread per group derives LfsrStream::split(seed, block) (a SplitMix64
-    // chain + a jump-table lookup) and publishes it through shared memory
-    if (t == 0 && nmine > 0) p0s[g][0] = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + gid)));
+    const uint32_t stab_addr = smem_addr(smem);
+    // lane 0 derives LfsrStream::split(seed, block) one block ahead
+    uint32_t p0_next = 0;
+    if (lane == 0 && wid < nfull)
+        p0_next = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + wid)));
     mbar_wait(&tab_bar, 0);
-    for (int i = 0; i < nmine; ++i) {
-        const int s = i % S;
-        const int64_t b = gid + (int64_t)i * gstride;
-        mbar_wait(&full[g][s], (uint32_t)((i / S) & 1));
-        const float4* blk = reinterpret_cast<const float4*>(ring + s * kBlock * 4);
-        uint32_t P[4][4], inc[4][4], cnt[4];
-        float nanacc = 0.0f;
+    for (int64_t b = wid; b < nfull; b += wstride) {
+        const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, p0_next, 0);
+        if (lane == 0 && b + wstride < nfull)
+            p0_next = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b + wstride)));
+        const float4* xb = reinterpret_cast<const float4*>(x + b * kBlock) + 2 * lane;
+        float4 va = __ldcs(xb), vb = __ldcs(xb + 1);
+        uint32_t run = stab_addr + 2u * p0;  // table byte address of the chunk's first sample
+#pragma unroll 2
+        for (int c = 0; c < kBlock / 256; ++c) {
+            const uint32_t u[8] = {__float_as_uint(va.x), __float_as_uint(va.y), __float_as_uint(va.z),
+                                   __float_as_uint(va.w), __float_as_uint(vb.x), __float_as_uint(vb.y),
+                                   __float_as_uint(vb.z), __float_as_uint(vb.w)};
+            if (c + 1 < kBlock / 256) {  // prefetch the next chunk
+                va = __ldcs(xb + 64 * (c + 1));
+                vb = __ldcs(xb + 64 * (c + 1) + 1);
+            }
+            uint32_t P[8], inc[8], n = 0;
+            float nanacc = 0.0f;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const float4 v = blk[256 * r + t];
-            const float f[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const bool big = big_or_nan<MB>(f[k]);
+            for (int k = 0; k < 8; ++k) {
+                const float f = __uint_as_float(u[k]);
+                const bool big = big_or_nan<MB>(f);
                 c_big += big;
-                nanacc = fmaf(f[k], 0.0f, nanacc);
-                P[r][k] = big ? special : packed_sr<MB>(f[k]);
-                inc[r][k] = (!big && inexact_sr<MB>(f[k])) ? 2u : 0u;  // byte stride in the table
+                nanacc = fmaf(f, 0.0f, nanacc);
+                P[k] = big ? special : packed_sr<MB>(f);
+                inc[k] = (!big && inexact_sr<MB>(f)) ? 2u : 0u;  // byte stride in the table
+                n += inc[k];
             }
-            cnt[r] = (inc[r][0] + inc[r][1] + inc[r][2] + inc[r][3]) >> 1;
-        }
-        uint32_t pre[4];
-        if (NG == 1) BlockScan<MB, 0>::run_counts(cnt, pre, smem_w[g][i & 1]);
-        else if (g == 0) BlockScan<MB, 1>::run_counts(cnt, pre, smem_w[g][i & 1]);
-        else if (g == 1) BlockScan<MB, 2>::run_counts(cnt, pre, smem_w[g][i & 1]);
-        else BlockScan<MB, 3>::run_counts(cnt, pre, smem_w[g][i & 1]);
-        const uint32_t p0 = p0s[g][i & 1];
-        // every thread of the group is past block i-1: refill its stage with block i-1+S
-        if (t == 0 && i + S - 1 < nmine) {
-            const int sn = (i + S - 1) % S;
-            const int64_t bn = gid + (int64_t)(i + S - 1) * gstride;
-            mbar_expect_tx(&full[g][sn], kBlock * 4);
-            bulk_g2s(ring + sn * kBlock * 4, x + bn * kBlock, kBlock * 4, &full[g][sn]);
-        }
-        // blocks whose stream window crosses the end of the 65535-cycle wrap
-        // (p0 > 61439: ~6% of blocks) take the modular addressing path
-        const bool wraps = p0 + kBlock > (uint32_t)kLfsrPeriod;
-        auto phase2 = [&](auto wrap_tag) {
-            constexpr bool WRAP = decltype(wrap_tag)::value;
+            // inclusive warp scan of the lanes' sample bytes
+            uint32_t incl = n;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                uint32_t sum[4];
-                if (!WRAP) {
-                    uint32_t addr = stab_addr + 2u * (p0 + pre[r]);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        uint32_t r16;
-                        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r16) : "r"(addr));
-                        addr += inc[r][k];
-                        sum[k] = P[r][k] + r16;  // exact lanes ignore their sample
-                    }
-                } else {
-                    uint32_t j = p0 + pre[r];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t jj = j >= (uint32_t)kLfsrPeriod ? j - kLfsrPeriod : j;
-                        const uint32_t r16 = stab[jj];
-                        j += inc[r][k] >> 1;
-                        sum[k] = P[r][k] + r16;
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    // underflow: inexact and rounded to zero; exact lanes pushed out of range
-                    const uint32_t chk = sum[k] + (2u - inc[r][k]) * 0x8000u;
-                    c_unf += (chk - 0x10000u) >> 31;
-                }
-                const float4 v = blk[256 * r + t];
-                const uint32_t u[4] = {__float_as_uint(v.x), __float_as_uint(v.y),
-                                       __float_as_uint(v.z), __float_as_uint(v.w)};
-                const int64_t q = b * (kBlock / 4) + 256 * r + t;  // float4 group index
-                if (MB == 2) {
-                    __stcs(reinterpret_cast<uint32_t*>(codes) + q,
-                           gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]));
-                } else {
-                    __stcs(reinterpret_cast<uint2*>(codes) + q,
-                           make_uint2(gather_f16(sum[0], sum[1], u[0], u[1]),
-                                      gather_f16(sum[2], sum[3], u[2], u[3])));
-                }
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += o;
             }
-        };
-        if (!wraps) phase2(std::false_type{});
-        else phase2(std::true_type{});
-        if (t == 0 && i + 1 < nmine)  // next block's stream start, read after the next barrier
-            p0s[g][(i + 1) & 1] = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b + gstride)));
-        // rare: a NaN (or Inf) among this thread's 16 inputs -> rewrite NaN codes
-        // as the canonical unsigned NaN (float_format.cpp:99) and count them
-        if (nanacc != nanacc) {
-            for (int r = 0; r < 4; ++r) {
-                const float4 v = blk[256 * r + t];
-                const float f[4] = {v.x, v.y, v.z, v.w};
-                const int64_t i0 = b * kBlock + 1024 * r + 4 * t;
-                for (int k = 0; k < 4; ++k)
-                    if (f[k] != f[k]) {
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            uint32_t addr = run + incl - n;
+            run += total;
+            uint32_t sum[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                uint32_t r16;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r16) : "r"(addr));
+                addr += inc[k];
+                sum[k] = P[k] + r16;  // exact lanes ignore their sample
+                // underflow: inexact and rounded to zero; exact lanes pushed out of range
+                const uint32_t chk = sum[k] + (2u - inc[k]) * 0x8000u;
+                c_unf += (chk - 0x10000u) >> 31;
+            }
+            const int64_t e0 = b * kBlock + 256 * c + 8 * lane;  // first element of this lane
+            if (MB == 2) {
+                __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(codes) + e0),
+                       make_uint2(gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]),
+                                  gather_e5m2(sum[4], sum[5], sum[6], sum[7], u[4], u[5], u[6], u[7])));
+            } else {
+                __stcs(reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(codes) + e0),
+                       make_uint4(gather_f16(sum[0], sum[1], u[0], u[1]), gather_f16(sum[2], sum[3], u[2], u[3]),
+                                  gather_f16(sum[4], sum[5], u[4], u[5]), gather_f16(sum[6], sum[7], u[6], u[7])));
+            }
+            // rare: NaN among the lane's inputs -> canonical unsigned NaN code (float_format.cpp:99)
+            if (nanacc != nanacc) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if ((u[k] & 0x7FFFFFFFu) > 0x7F800000u) {
                         ++c_nan;
-                        if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i0 + k] = 0x7E;
-                        else reinterpret_cast<uint16_t*>(codes)[i0 + k] = 0x7E00;
+                        if (MB == 2) reinterpret_cast<uint8_t*>(codes)[e0 + k] = 0x7E;
+                        else reinterpret_cast<uint16_t*>(codes)[e0 + k] = 0x7E00;
                     }
             }
         }
     }
-    if (counters) flush_counters<256 * kLfsrGroups>(c_big - c_nan, c_unf, c_nan, counters);
+    if (counters) flush_counters<kWarpLfsrThreads>(c_big - c_nan, c_unf, c_nan, counters);
 }
 
 // Tail / unaligned kernel: blocks [block_begin, nblocks), scalar-safe loads.
@@ -506,23 +464,21 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
         if (aligned) {
             const int64_t nfull = n / kBlock;
             if (nfull > 0) {
-                auto fn = quant_lfsr_staged_kernel<MB>;
-                constexpr int smem = kLfsrSmem;
-                static bool attr = false;
-                if (!attr) {
+                auto fn = quant_lfsr_warp_kernel<MB>;
+                constexpr int smem = kTabWrapBytes;
+                static bool wattr = false;
+                if (!wattr) {
                     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                    attr = true;
+                    wattr = true;
                 }
-                int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256 * kLfsrGroups, smem);
                 int num_sms = 0, dev = 0;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-                int64_t g = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
-                const int64_t need = (nfull + kLfsrGroups - 1) / kLfsrGroups;
+                int64_t g = num_sms;
+                const int64_t need = (nfull + kWarpLfsrThreads / 32 - 1) / (kWarpLfsrThreads / 32);
                 if (need < g) g = need;
-                fn<<<(int)g, 256 * kLfsrGroups, smem, st>>>(x, codes, nfull, cfg.seed, cfg.saturate,
-                                              cfg.block_offset, tabs, counters);
+                fn<<<(int)g, kWarpLfsrThreads, smem, st>>>(x, codes, nfull, cfg.seed, cfg.saturate,
+                                                          cfg.block_offset, tabs, counters);
                 begin = nfull;
             }
         }

@@ -7,6 +7,8 @@
 // with value == decode(master) (test_nn.cpp:162-178, so no FP32 copy is kept)
 // and IEEE binary32 ops in exactly that order: __fdiv_rn/__fmul_rn/__fadd_rn
 // forbid FMA contraction (the reference objects contain no FMA).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -188,119 +190,140 @@ __global__ void __launch_bounds__(NT) sgd_elem_kernel(const void* __restrict__ g
 }
 
 // Reference-stream SR master: quantize(Tensor(w32), kFp16, {Stochastic, seed})
-// semantics (SURVEY 8c iii), with the block scan of quantize.cu. The TMA engine
-// stages grad / master / momentum of the next blocks in an S-deep shared ring;
-// phase 1 computes w32 (kept in the ring, over the momentum it consumed) and
-// the inexact flags, phase 2 rounds with the block's LFSR samples.
-constexpr int kUpdStages = 3;
+// semantics (SURVEY 8c iii): block b of 4096 parameters rounds with
+// LfsrStream::split(seed, block_offset + b), one sample per inexact w32.
+// Warp-per-block kernel over full blocks: each warp owns whole 4096-parameter
+// blocks and walks them in 16 chunks of 256 (8 per lane, coalesced, prefetched
+// one chunk ahead), so the master SR stream ranks need only a warp shuffle scan
+// on top of a running count -- no CTA barrier. Samples come from the
+// wrap-extended jump table in shared memory; exact lanes add their sample to a
+// zero remainder, which never carries, so no select is needed.
+constexpr int kWarpUpdThreads = 512;
+constexpr int kUpdTabBytes = ((kLfsrPeriod + kBlock) * 2 + 15) & ~15;
 template <int GFMT, bool CNT>
-__global__ void __launch_bounds__(256) sgd_lfsr_staged_kernel(const void* __restrict__ grad,
-                                                              uint16_t* __restrict__ master,
-                                                              float* __restrict__ mom,
-                                                              int64_t nfull, UpdArgs a,
-                                                              int64_t block_offset,
-                                                              LfsrTables tabs) {
-    constexpr int S = kUpdStages;
-    constexpr int GB = kBlock * grad_bytes<GFMT>();
-    constexpr int MB_ = kBlock * 2, VB = kBlock * 4;
-    constexpr int STAGE = GB + MB_ + VB;
-    extern __shared__ __align__(128) uint8_t ring[];
-    __shared__ __align__(8) uint64_t full[S];
-    __shared__ uint32_t smem_w[2][8];
-    __shared__ uint32_t p0s[2];
+__global__ void __launch_bounds__(kWarpUpdThreads, 1)
+    sgd_lfsr_warp_kernel(const void* __restrict__ grad, uint16_t* __restrict__ master,
+                         float* __restrict__ mom, int64_t nfull, UpdArgs a, int64_t block_offset,
+                         LfsrTables tabs) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t tab_bar;
     if (upd_skipped(a)) return;
     const Unscale us(upd_scale(a));
     const bool wsat = a.w_sat != 0;
     uint32_t mb = 0, mn = 0, mu_ = 0, wb = 0, wn = 0, wu = 0;
-    const int t = threadIdx.x;
-    if (t == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(full + s, 1);
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * kWarpUpdThreads + threadIdx.x) >> 5;
+    const int64_t wstride = ((int64_t)gridDim.x * kWarpUpdThreads) >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(&tab_bar, 1);
         mbar_fence_init();
+        mbar_expect_tx(&tab_bar, kUpdTabBytes);
+        for (int off = 0; off < kUpdTabBytes; off += 16384) {
+            const int len = kUpdTabBytes - off < 16384 ? kUpdTabBytes - off : 16384;
+            bulk_g2s(smem + off, reinterpret_cast<const uint8_t*>(tabs.tabx) + off, len, &tab_bar);
+        }
     }
     __syncthreads();
-    const int64_t nmine = nfull > blockIdx.x ? (nfull - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    auto issue = [&](int64_t i) {
-        const int s = (int)(i % S);
-        const int64_t b = blockIdx.x + i * gridDim.x;
-        uint8_t* st = ring + s * STAGE;
-        // the ring slot was last written through the generic proxy (w32); order
-        // those writes before the async-proxy (TMA) refill
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(full + s, STAGE);
-        bulk_g2s(st, reinterpret_cast<const uint8_t*>(grad) + b * GB, GB, full + s);
-        bulk_g2s(st + GB, master + b * kBlock, MB_, full + s);
-        bulk_g2s(st + GB + MB_, mom + b * kBlock, VB, full + s);
+    const uint32_t stab_addr = smem_addr(smem);
+    uint32_t p0_next = 0;
+    if (lane == 0 && wid < nfull)
+        p0_next = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + wid)));
+    mbar_wait(&tab_bar, 0);
+    // per-lane chunk loads: grad (8 codes or floats), 8 masters, 8 momenta
+    struct Chunk {
+        uint4 g;        // E5M2: .x,.y; FP16: all; F32: first 4 floats (second in g2)
+        uint4 g2;
+        uint4 m;        // 8 FP16 masters
+        float4 v0, v1;  // 8 momenta
     };
-    if (t == 0) {
-        for (int64_t i = 0; i < S - 1 && i < nmine; ++i) issue(i);
-        if (nmine > 0) p0s[0] = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + blockIdx.x)));
-    }
-    for (int64_t i = 0; i < nmine; ++i) {
-        const int s = (int)(i % S);
-        const int64_t b = blockIdx.x + i * gridDim.x;
-        mbar_wait(full + s, (uint32_t)((i / S) & 1));
-        uint8_t* st = ring + s * STAGE;
-        float4* wv = reinterpret_cast<float4*>(st + GB + MB_);  // momentum in, w32 out
-        const uint2* mw = reinterpret_cast<const uint2*>(st + GB);
-        uint32_t mask[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int q = 256 * r + t;  // float4 group within the block
-            float gr[4];
-            if (GFMT == FP8B_E5M2) {
-                const uint32_t w = reinterpret_cast<const uint32_t*>(st)[q];
-                gr[0] = dec_e5m2(w); gr[1] = dec_e5m2(w >> 8); gr[2] = dec_e5m2(w >> 16); gr[3] = dec_e5m2(w >> 24);
-            } else if (GFMT == FP8B_FP16) {
-                const uint2 w = reinterpret_cast<const uint2*>(st)[q];
-                gr[0] = dec_f16(w.x); gr[1] = dec_f16(w.x >> 16); gr[2] = dec_f16(w.y); gr[3] = dec_f16(w.y >> 16);
-            } else {
-                const float4 v = reinterpret_cast<const float4*>(st)[q];
-                gr[0] = v.x; gr[1] = v.y; gr[2] = v.z; gr[3] = v.w;
-            }
-            const uint2 m2 = mw[q];
-            const uint32_t mc[4] = {m2.x & 0xFFFFu, m2.x >> 16, m2.y & 0xFFFFu, m2.y >> 16};
-            const float4 mv = wv[q];
-            float m[4] = {mv.x, mv.y, mv.z, mv.w};
-            float w[4];
-            mask[r] = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                w[k] = sgd_w32(gr[k], dec_f16(mc[k]), m[k], us, a);
-                const uint32_t aa = __float_as_uint(w[k]) & 0x7FFFFFFFu;
-                if (sr_inexact<10>(aa, __uint_as_float(aa))) mask[r] |= 1u << k;
-            }
-            __stcs(reinterpret_cast<float4*>(mom) + b * (kBlock / 4) + q, make_float4(m[0], m[1], m[2], m[3]));
-            wv[q] = make_float4(w[0], w[1], w[2], w[3]);
+    auto load = [&](int64_t e0, Chunk& ck) {
+        if (GFMT == FP8B_E5M2) {
+            const uint2 t = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(grad) + e0));
+            ck.g = make_uint4(t.x, t.y, 0, 0);
+        } else if (GFMT == FP8B_FP16) {
+            ck.g = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(grad) + e0));
+        } else {
+            ck.g = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(grad) + e0));
+            ck.g2 = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(grad) + e0) + 1);
         }
-        uint32_t pre[4];
-        BlockScan<10>::run(mask, pre, smem_w[i & 1]);
-        if (t == 0 && i + S - 1 < nmine) issue(i + S - 1);
-        const uint32_t p0 = p0s[i & 1];
+        ck.m = __ldcs(reinterpret_cast<const uint4*>(master + e0));
+        ck.v0 = __ldcs(reinterpret_cast<const float4*>(mom + e0));
+        ck.v1 = __ldcs(reinterpret_cast<const float4*>(mom + e0) + 1);
+    };
+    for (int64_t b = wid; b < nfull; b += wstride) {
+        const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, p0_next, 0);
+        if (lane == 0 && b + wstride < nfull)
+            p0_next = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + b + wstride)));
+        Chunk nx;
+        load(b * kBlock + 8 * lane, nx);
+        uint32_t run = stab_addr + 2u * p0;
+#pragma unroll 1
+        for (int c = 0; c < kBlock / 256; ++c) {
+            const int64_t e0 = b * kBlock + 256 * c + 8 * lane;
+            const Chunk ck = nx;
+            if (c + 1 < kBlock / 256) load(e0 + 256, nx);
+            float gr[8];
+            if (GFMT == FP8B_E5M2) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int q = 256 * r + t;
-            const float4 wq = wv[q];
-            const float w[4] = {wq.x, wq.y, wq.z, wq.w};
-            uint32_t j = p0 + pre[r];
-            uint32_t out[4];
+                for (int k = 0; k < 4; ++k) {
+                    gr[k] = dec_e5m2(ck.g.x >> (8 * k));
+                    gr[4 + k] = dec_e5m2(ck.g.y >> (8 * k));
+                }
+            } else if (GFMT == FP8B_FP16) {
+                const uint32_t gw[4] = {ck.g.x, ck.g.y, ck.g.z, ck.g.w};
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t take = (mask[r] >> k) & 1u;
-                const uint32_t r16 = take ? (uint32_t)__ldg(tabs.tabx + j) : 0u;
-                j += take;
+                for (int k = 0; k < 4; ++k) {
+                    gr[2 * k] = dec_f16(gw[k]);
+                    gr[2 * k + 1] = dec_f16(gw[k] >> 16);
+                }
+            } else {
+                const uint32_t gw[8] = {ck.g.x, ck.g.y, ck.g.z, ck.g.w, ck.g2.x, ck.g2.y, ck.g2.z, ck.g2.w};
+#pragma unroll
+                for (int k = 0; k < 8; ++k) gr[k] = __uint_as_float(gw[k]);
+            }
+            const uint32_t mw[4] = {ck.m.x, ck.m.y, ck.m.z, ck.m.w};
+            float m[8] = {ck.v0.x, ck.v0.y, ck.v0.z, ck.v0.w, ck.v1.x, ck.v1.y, ck.v1.z, ck.v1.w};
+            float w[8];
+            uint32_t inc[8], n = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t mc = (mw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+                w[k] = sgd_w32(gr[k], dec_f16(mc), m[k], us, a);
+                const uint32_t aa = __float_as_uint(w[k]) & 0x7FFFFFFFu;
+                inc[k] = sr_inexact<10>(aa, __uint_as_float(aa)) ? 2u : 0u;
+                n += inc[k];
+            }
+            __stcs(reinterpret_cast<float4*>(mom + e0), make_float4(m[0], m[1], m[2], m[3]));
+            __stcs(reinterpret_cast<float4*>(mom + e0) + 1, make_float4(m[4], m[5], m[6], m[7]));
+            uint32_t incl = n;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += o;
+            }
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            uint32_t addr = run + incl - n;
+            run += total;
+            uint32_t out[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                uint32_t r16;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r16) : "r"(addr));
+                addr += inc[k];
                 out[k] = sr_encode<10>(__float_as_uint(w[k]), r16, false, mb, mn, mu_);
             }
-            __stcs(reinterpret_cast<uint2*>(master) + b * (kBlock / 4) + q,
-                   make_uint2(out[0] | (out[1] << 16), out[2] | (out[3] << 16)));
-            if (a.w8)
-                __stcs(reinterpret_cast<uint32_t*>(a.w8) + b * (kBlock / 4) + q,
-                       w8_pack4(out, wsat, wb, wn, wu));
+            __stcs(reinterpret_cast<uint4*>(master + e0),
+                   make_uint4(out[0] | (out[1] << 16), out[2] | (out[3] << 16), out[4] | (out[5] << 16),
+                              out[6] | (out[7] << 16)));
+            if (a.w8) {
+                const uint32_t lo[4] = {out[0], out[1], out[2], out[3]}, hi[4] = {out[4], out[5], out[6], out[7]};
+                __stcs(reinterpret_cast<uint2*>(a.w8 + e0),
+                       make_uint2(w8_pack4(lo, wsat, wb, wn, wu), w8_pack4(hi, wsat, wb, wn, wu)));
+            }
         }
-        if (t == 0 && i + 1 < nmine)  // next block's stream start, read after the next barrier
-            p0s[(i + 1) & 1] = __ldg(tabs.pos + lfsr_split(a.seed, (uint64_t)(block_offset + b + gridDim.x)));
     }
-    if (CNT && a.mcnt) flush_counters<256>(mb - mn, mu_, mn, a.mcnt);
-    if (CNT && a.wcnt) flush_counters<256>(wb - wn, wu, wn, a.wcnt);
+    if (CNT && a.mcnt) flush_counters<kWarpUpdThreads>(mb - mn, mu_, mn, a.mcnt);
+    if (CNT && a.wcnt) flush_counters<kWarpUpdThreads>(wb - wn, wu, wn, a.wcnt);
 }
 
 // Tail / unaligned variant: blocks [block_begin, nblocks) with scalar accesses.
@@ -440,14 +463,14 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
         int64_t begin = 0;
         if (aligned && n / kBlock > 0) {
             const int64_t nfull = n / kBlock;
-            constexpr int smem = kUpdStages * kBlock * (grad_bytes<GFMT>() + 2 + 4);
-            auto fn = cnt ? sgd_lfsr_staged_kernel<GFMT, true> : sgd_lfsr_staged_kernel<GFMT, false>;
+            constexpr int smem = kUpdTabBytes;
+            auto fn = cnt ? sgd_lfsr_warp_kernel<GFMT, true> : sgd_lfsr_warp_kernel<GFMT, false>;
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
-            int64_t g = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
-            if (nfull < g) g = nfull;
-            fn<<<(int)g, 256, smem, st>>>(grad, master, mom, nfull, a, args.block_offset, tabs);
+            int64_t g = sm_count();
+            const int64_t need = (nfull + kWarpUpdThreads / 32 - 1) / (kWarpUpdThreads / 32);
+            if (need < g) g = need;
+            fn<<<(int)g, kWarpUpdThreads, smem, st>>>(grad, master, mom, nfull, a, args.block_offset,
+                                                      tabs);
             begin = nfull;
         }
         if (begin < nb) {

@@ -239,17 +239,27 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
                 vb = __ldcs(xb + 64 * (c + 1) + 1);
             }
             uint32_t P[8], inc[8], n = 0;
-            float nanacc = 0.0f;
+            float nanacc = 0.0f, amax = 0.0f;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const float f = __uint_as_float(u[k]);
-                const bool big = big_or_nan<MB>(f);
-                c_big += big;
-                nanacc = fmaf(f, 0.0f, nanacc);
-                P[k] = big ? special : packed_sr<MB>(f);
-                inc[k] = (!big && inexact_sr<MB>(f)) ? 2u : 0u;  // byte stride in the table
-                n += inc[k];
+                amax = fmaxf(amax, fabsf(f));
+                nanacc = fmaf(f, 0.0f, nanacc);  // NaN iff some input is NaN or +-Inf
+                P[k] = packed_sr<MB>(f);
+                inc[k] = inexact_sr<MB>(f) ? 2u : 0u;  // byte stride in the table
             }
+            // rare: an overflowing or NaN input in this lane -> the reference's
+            // overflow code (Inf / max when saturating) and no sample taken
+            if (nanacc != nanacc || amax > (MB == 2 ? 57344.0f : 65504.0f)) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool big = big_or_nan<MB>(__uint_as_float(u[k]));
+                    c_big += big;
+                    if (big) { P[k] = special; inc[k] = 0u; }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) n += inc[k];
             // inclusive warp scan of the lanes' sample bytes
             uint32_t incl = n;
 #pragma unroll

@@ -5,8 +5,8 @@ mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 for w in ${PROF_WHAT:-lfsr fp16ctr gemm}; do
   case $w in
-    rne) K=quant_elem_kernel ;; lfsr) K=quant_lfsr_staged ;; fp16ctr) K=quant_elem_kernel ;;
-    upd_rne) K=sgd_elem ;; upd_lfsr) K=sgd_lfsr_staged ;; gemm|gemm_e5m2) K=gemm_tc ;;
+    rne) K=quant_elem_kernel ;; lfsr) K=quant_lfsr_warp ;; fp16ctr) K=quant_elem_kernel ;;
+    upd_rne) K=sgd_elem ;; upd_lfsr) K=sgd_lfsr_warp ;; gemm|gemm_e5m2) K=gemm_tc ;;
   esac
   timeout 300 python scripts/prof.py $w 3 > gpurun_out/prof_plain_$w.log 2>&1 && \
   timeout 600 $NCU --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 \

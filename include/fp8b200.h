@@ -223,9 +223,21 @@ typedef struct {
     int64_t stride, pad;      /* ConvGeometry (kernels.hpp:13-16) */
     int32_t layout;           /* FP8B_NCHW / FP8B_NHWC */
     int32_t engine;           /* FP8B_GEMM_TENSOR / FP8B_GEMM_SEQUENTIAL */
+    /* Optional fused output Q node (the layer's next quantize, nn.cpp:192-200):
+     * when yq != NULL the output is also (or, with a NULL FP32 output, only)
+     * written as codes. yq_mode RNE / TRUNC, or SR with counter bits (yq_seed
+     * nonzero); counters accumulate {overflow, underflow, nan} like fp8b_quantize. */
+    void *yq;
+    int32_t yq_fmt;           /* FP8B_E5M2 / FP8B_FP16 */
+    int32_t yq_mode;          /* FP8B_RNE / FP8B_TRUNC / FP8B_SR (counter bits) */
+    uint64_t yq_seed;
+    int32_t yq_saturate;
+    int32_t reserved;
+    int64_t *yq_counters;     /* device int64[3] or NULL */
 } fp8b_conv_t;
 
-/* conv2d_fp8 (kernels.hpp:22-23): y = x * w */
+/* conv2d_fp8 (kernels.hpp:22-23): y = x * w. The FP32 output pointer may be
+ * NULL when g->yq is set. */
 int fp8b_conv2d_fprop(const void *x, const void *w, float *y, int32_t fmt, const fp8b_conv_t *g,
                       void *stream);
 /* conv2d_backward_data_fp8 (kernels.hpp:39-41): dx from e [N,F,OH,OW] and w */

@@ -291,6 +291,25 @@ def _conv_geom(n, c, h, w, f, kh, kw, stride, pad, layout, engine):
                          _lib.GEMM_TENSOR if engine == "tensor" else _lib.GEMM_SEQUENTIAL)
 
 
+def _conv_out_q(g, shape, device, out_fmt, out_mode, out_seed, out_saturate, out_counters):
+    """Attach the fused output Q node to a ConvGeom; returns the code tensor."""
+    if out_fmt is None:
+        return None, None
+    f = _fmt(out_fmt)
+    n = int(np.prod(shape))
+    codes = torch.empty(n, dtype=_code_dtype(f), device=device)
+    cnt = out_counters if out_counters is not None else Counters(device)
+    g.yq, g.yq_fmt, g.yq_mode = codes.data_ptr(), f, _mode(out_mode)
+    g.yq_seed, g.yq_saturate, g.yq_counters = int(out_seed), int(bool(out_saturate)), cnt.ptr
+    return QuantizedTensor(codes, list(shape), f, _mode(out_mode), cnt), cnt
+
+
+def _conv_ret(y, q, want_y):
+    if q is None:
+        return y
+    return (y if want_y else None), q
+
+
 def _nchw_dims(shape, layout):
     if len(shape) != 4:
         return None
@@ -300,13 +319,18 @@ def _nchw_dims(shape, layout):
 
 
 def conv2d(x: QuantizedTensor, w: QuantizedTensor, stride: int = 1, pad: int = 0, *,
-           layout: str = "nchw", engine: str = "sequential", stream=None) -> torch.Tensor:
+           layout: str = "nchw", engine: str = "sequential", out_fmt: Optional[str] = None,
+           out_mode: str = "nearest-even", out_seed: int = 1, out_saturate: bool = False,
+           out_counters: Optional[Counters] = None, want_y: bool = True, stream=None):
     """fp8emu.conv2d (bindings.cpp:191-198 -> kernels.cpp:106-151): FP32 output.
 
     layout "nchw": x [N,C,H,W], w [F,C,kH,kW] -> y [N,F,OH,OW] (the reference);
     layout "nhwc": x [N,H,W,C], w [F,kH,kW,C] -> y [N,OH,OW,F].
     engine "sequential" is bitwise the reference; "tensor" runs tcgen05 implicit
-    GEMM where supported (NHWC E5M2 stride 1) within the GEMM tolerance."""
+    GEMM where supported (NHWC E5M2 stride 1) within the GEMM tolerance.
+    out_fmt: also emit the output's Q node (fused into the tensor epilogue);
+    returns (y or None, QuantizedTensor) then. out_mode "stochastic" uses
+    counter bits (seed out_seed)."""
     xd, wd = _nchw_dims(x.shape, layout), _nchw_dims(w.shape, layout)
     if xd is None or wd is None:
         raise ValueError("conv2d_fp8 expects [N,C,H,W] and [F,C,kH,kW]")
@@ -318,16 +342,22 @@ def conv2d(x: QuantizedTensor, w: QuantizedTensor, stride: int = 1, pad: int = 0
         raise ValueError("kernel operands must share one format")
     oh, ow = conv_out_dim(h, kh, stride, pad), conv_out_dim(wi, kw, stride, pad)
     shape = (n, f, oh, ow) if layout == "nchw" else (n, oh, ow, f)
-    y = torch.empty(shape, dtype=torch.float32, device=x.codes.device)
     g = _conv_geom(n, c, h, wi, f, kh, kw, stride, pad, layout, engine)
-    check(LIB.fp8b_conv2d_fprop(x.codes.data_ptr(), w.codes.data_ptr(), y.data_ptr(), x.fmt_id,
+    q, _ = _conv_out_q(g, shape, x.codes.device, out_fmt, out_mode, out_seed, out_saturate,
+                       out_counters)
+    keep = want_y or q is None
+    y = torch.empty(shape, dtype=torch.float32, device=x.codes.device) if keep else None
+    check(LIB.fp8b_conv2d_fprop(x.codes.data_ptr(), w.codes.data_ptr(), _ptr(y), x.fmt_id,
                                 g, _stream(stream)), "conv2d_fp8")
-    return y
+    return _conv_ret(y, q, keep)
 
 
 def conv2d_backward_data(e: QuantizedTensor, w: QuantizedTensor, stride: int, pad: int, h: int,
                          w_dim: int, *, layout: str = "nchw", engine: str = "sequential",
-                         stream=None) -> torch.Tensor:
+                         out_fmt: Optional[str] = None, out_mode: str = "nearest-even",
+                         out_seed: int = 1, out_saturate: bool = False,
+                         out_counters: Optional[Counters] = None, want_y: bool = True,
+                         stream=None):
     """conv2d_backward_data_fp8 (kernels.cpp:153-205): dx [N,C,H,W] (or NHWC)."""
     ed, wd = _nchw_dims(e.shape, layout), _nchw_dims(w.shape, layout)
     if ed is None or wd is None:
@@ -341,16 +371,22 @@ def conv2d_backward_data(e: QuantizedTensor, w: QuantizedTensor, stride: int, pa
     if conv_out_dim(h, kh, stride, pad) != oh or conv_out_dim(w_dim, kw, stride, pad) != ow:
         raise ValueError("conv backward geometry disagrees with error")
     shape = (n, c, h, w_dim) if layout == "nchw" else (n, h, w_dim, c)
-    dx = torch.empty(shape, dtype=torch.float32, device=e.codes.device)
     g = _conv_geom(n, c, h, w_dim, f, kh, kw, stride, pad, layout, engine)
-    check(LIB.fp8b_conv2d_dgrad(e.codes.data_ptr(), w.codes.data_ptr(), dx.data_ptr(), e.fmt_id,
+    q, _ = _conv_out_q(g, shape, e.codes.device, out_fmt, out_mode, out_seed, out_saturate,
+                       out_counters)
+    keep = want_y or q is None
+    dx = torch.empty(shape, dtype=torch.float32, device=e.codes.device) if keep else None
+    check(LIB.fp8b_conv2d_dgrad(e.codes.data_ptr(), w.codes.data_ptr(), _ptr(dx), e.fmt_id,
                                 g, _stream(stream)), "conv2d_backward_data_fp8")
-    return dx
+    return _conv_ret(dx, q, keep)
 
 
 def conv2d_backward_weights(x: QuantizedTensor, e: QuantizedTensor, kh: int, kw: int,
                             stride: int, pad: int, *, layout: str = "nchw",
-                            engine: str = "sequential", stream=None) -> torch.Tensor:
+                            engine: str = "sequential", out_fmt: Optional[str] = None,
+                            out_mode: str = "nearest-even", out_seed: int = 1,
+                            out_saturate: bool = False, out_counters: Optional[Counters] = None,
+                            want_y: bool = True, stream=None):
     """conv2d_backward_weights_fp8 (kernels.cpp:207-253): dw [F,C,kH,kW] (or [F,kH,kW,C])."""
     xd, ed = _nchw_dims(x.shape, layout), _nchw_dims(e.shape, layout)
     if xd is None or ed is None or xd[0] != ed[0]:
@@ -362,11 +398,14 @@ def conv2d_backward_weights(x: QuantizedTensor, e: QuantizedTensor, kh: int, kw:
     if conv_out_dim(h, kh, stride, pad) != oh or conv_out_dim(wi, kw, stride, pad) != ow:
         raise ValueError("conv backward geometry disagrees with error")
     shape = (f, c, kh, kw) if layout == "nchw" else (f, kh, kw, c)
-    dw = torch.empty(shape, dtype=torch.float32, device=x.codes.device)
     g = _conv_geom(n, c, h, wi, f, kh, kw, stride, pad, layout, engine)
-    check(LIB.fp8b_conv2d_wgrad(x.codes.data_ptr(), e.codes.data_ptr(), dw.data_ptr(), x.fmt_id,
+    q, _ = _conv_out_q(g, shape, x.codes.device, out_fmt, out_mode, out_seed, out_saturate,
+                       out_counters)
+    keep = want_y or q is None
+    dw = torch.empty(shape, dtype=torch.float32, device=x.codes.device) if keep else None
+    check(LIB.fp8b_conv2d_wgrad(x.codes.data_ptr(), e.codes.data_ptr(), _ptr(dw), x.fmt_id,
                                 g, _stream(stream)), "conv2d_backward_weights_fp8")
-    return dw
+    return _conv_ret(dw, q, keep)
 
 
 def conv2d_im2col(x: QuantizedTensor, w: QuantizedTensor, stride: int = 1, pad: int = 0, *,

@@ -71,7 +71,9 @@ class DenseStep(C.Structure):
 
 class ConvGeom(C.Structure):
     _fields_ = [("n", _i64), ("c", _i64), ("h", _i64), ("w", _i64), ("f", _i64), ("kh", _i64),
-                ("kw", _i64), ("stride", _i64), ("pad", _i64), ("layout", _i32), ("engine", _i32)]
+                ("kw", _i64), ("stride", _i64), ("pad", _i64), ("layout", _i32), ("engine", _i32),
+                ("yq", _vp), ("yq_fmt", _i32), ("yq_mode", _i32), ("yq_seed", _u64),
+                ("yq_saturate", _i32), ("reserved", _i32), ("yq_counters", _vp)]
 
 
 # every symbol include/fp8b200.h declares, with its ctypes signature

@@ -234,21 +234,60 @@ static int conv_common(int kind, const void* a, const void* b, float* out, int32
                        const fp8b_conv_t* g, void* stream, const char* who) {
     const int rc = conv_validate(g, fmt, who);
     if (rc) return rc;
+    if (g->yq) {
+        if (!valid_fmt(g->yq_fmt)) return fail(FP8B_EINVAL, "conv: bad yq_fmt");
+        if (!valid_mode(g->yq_mode)) return fail(FP8B_EINVAL, "conv: bad yq_mode");
+        if (g->yq_mode == FP8B_SR && g->yq_seed == 0)
+            return fail(FP8B_EINVAL, "QuantConfig.seed must be nonzero");
+    }
     const int64_t oh = (g->h + 2 * g->pad - g->kh) / g->stride + 1;
     const int64_t ow = (g->w + 2 * g->pad - g->kw) / g->stride + 1;
     const int64_t nout = kind == 0 ? g->n * g->f * oh * ow
                          : kind == 1 ? g->n * g->c * g->h * g->w
                                      : g->f * g->c * g->kh * g->kw;
     if (nout == 0) return FP8B_OK;
-    if (!out || !a || !b) return fail(FP8B_EINVAL, "conv: null tensor");
-    if (g->engine == FP8B_GEMM_TENSOR) {
+    if (!a || !b || (!out && !g->yq)) return fail(FP8B_EINVAL, "conv: null tensor");
+    cudaStream_t st = S(stream);
+    // fprop / dgrad on the tensor engine fuse the output Q node into the
+    // tcgen05 epilogue; every other case computes FP32 and quantizes after
+    if (g->engine == FP8B_GEMM_TENSOR && kind != 2) {
         int nl = 0;
-        const int r = fp8b::launch_conv_tc(kind, a, b, out, fmt, *g, S(stream), &nl);
+        const int r = fp8b::launch_conv_tc(kind, a, b, out, fmt, *g, st, &nl);
         if (r == FP8B_OK) return check_launch(nl);
         if (r != FP8B_ENOTSUP) return r;
     }
-    fp8b::launch_conv_seq(kind, a, b, out, fmt, *g, S(stream));
-    return check_launch(1);
+    float* tmp = nullptr;
+    if (!out) {
+        if (cudaMallocAsync(&tmp, sizeof(float) * (size_t)nout, st) != cudaSuccess)
+            return fail(FP8B_ECUDA, "conv: workspace allocation failed");
+        out = tmp;
+    }
+    fp8b_conv_t g2 = *g;
+    g2.yq = nullptr;
+    int nl = 0;
+    int r = FP8B_ENOTSUP;
+    if (g->engine == FP8B_GEMM_TENSOR) r = fp8b::launch_conv_tc(kind, a, b, out, fmt, g2, st, &nl);
+    if (r == FP8B_ENOTSUP) {
+        fp8b::launch_conv_seq(kind, a, b, out, fmt, g2, st);
+        nl = 1;
+        r = FP8B_OK;
+    }
+    if (r == FP8B_OK && g->yq) {
+        fp8b::LfsrTables tabs;
+        r = get_tables(&tabs);
+        if (r == FP8B_OK) {
+            fp8b_quant_config_t qc{};
+            qc.mode = g->yq_mode;
+            qc.bits = FP8B_BITS_COUNTER;
+            qc.seed = g->yq_seed;
+            qc.saturate = g->yq_saturate;
+            fp8b::launch_quantize(out, g->yq, nout, g->yq_fmt, qc, g->yq_counters, st, tabs);
+            nl += 1;
+        }
+    }
+    if (tmp) cudaFreeAsync(tmp, st);
+    if (r != FP8B_OK) return r;
+    return check_launch(nl);
 }
 
 int fp8b_conv2d_fprop(const void* x, const void* w, float* y, int32_t fmt, const fp8b_conv_t* g,

@@ -99,7 +99,7 @@ struct Geo {
     static constexpr uint32_t B_BYTES = MODE == 0 ? (uint32_t)BN * CB : (uint32_t)KPIX * CB;
     static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
     static constexpr int BUDGET = 232448 - (int)EPI_STAGE_BYTES - 1280;
-    static constexpr int STAGES = (BUDGET / (int)STAGE) > 8 ? 8 : (BUDGET / (int)STAGE);
+    static constexpr int STAGES = (BUDGET / (int)STAGE) > 16 ? 16 : (BUDGET / (int)STAGE);
     static constexpr uint32_t SMEM = STAGES * STAGE + EPI_STAGE_BYTES + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr uint32_t SWZ_LAYOUT = CB == 128 ? 2u : 4u;  // UMMA layout code
@@ -386,7 +386,7 @@ static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
 // fprop over NHWC x [n, h, w, c] and KRSC w [f, k, k, c] -> y [n, oh, ow, f]
 template <int ES>
 static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, int64_t wd,
-                 int64_t c, int64_t f, int k, int pad, cudaStream_t st) {
+                 int64_t c, int64_t f, int k, int pad, cudaStream_t st, const fp8b_conv_t& g) {
     const int cb_bytes = (c * ES) % 128 == 0 ? 128 : ((c * ES) % 64 == 0 ? 64 : 0);
     if (!cb_bytes) return FP8B_ENOTSUP;
     const int64_t oh = h + 2 * pad - k + 1, ow = wd + 2 * pad - k + 1;
@@ -399,7 +399,7 @@ static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, i
     if (!make_map(&tb, w, ES, (uint64_t)(k * k * c), (uint64_t)f, cbe, bn, swz)) return FP8B_ENOTSUP;
     CParams p{};
     p.M = P; p.N = f;
-    p.ep = EpiArgs{y, nullptr, nullptr, 0, 0, 0, 0, nullptr};
+    p.ep = EpiArgs{y, nullptr, g.yq, g.yq_fmt, g.yq_mode, g.yq_seed, g.yq_saturate, g.yq_counters};
     p.tiles_m = (int)((P + 127) / 128);
     p.tiles_n = (int)((f + bn - 1) / bn);
     p.cblocks = (int)(c / cbe);
@@ -408,7 +408,7 @@ static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, i
     p.C = (int)c; p.KW = k; p.pad = pad; p.OH = (int)oh; p.OW = (int)ow;
     CUtensorMap tcm;
     memset(&tcm, 0, sizeof(tcm));
-    p.c_tma = (epi_tma() && make_c_map(&tcm, y, P, f)) ? 1 : 0;
+    p.c_tma = (epi_tma() && y && make_c_map(&tcm, y, P, f)) ? 1 : 0;
     if (cb_bytes == 128) {
         if (bn == 64) return run<ES, 0, 64, 128>(ta, tb, tcm, p, st);
         if (bn == 128) return run<ES, 0, 128, 128>(ta, tb, tcm, p, st);
@@ -470,7 +470,8 @@ static int wgrad(const void* x, const void* e, float* dw, int64_t n, int64_t h, 
 
 template <int ES>
 static int dgrad(const void* e, const void* w, float* dx, int64_t n, int64_t h, int64_t wd,
-                 int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl) {
+                 int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl,
+                 const fp8b_conv_t& g) {
     // fprop of e [n, oh, ow, f] with W' [c, k, k, f] and pad' = k-1-pad -> [n, h, w, c]
     const int pad2 = k - 1 - pad;
     if (pad2 < 0 || (f * ES) % 64) return FP8B_ENOTSUP;
@@ -482,7 +483,7 @@ static int dgrad(const void* e, const void* w, float* dx, int64_t n, int64_t h, 
     if (b > 4 * num_sms()) b = 4 * num_sms();
     using T = typename std::conditional<ES == 1, uint8_t, uint16_t>::type;
     flip_kernel<T><<<(int)b, 256, 0, st>>>((const T*)w, (T*)wf, f, c, k, k);
-    const int rc = fprop<ES>(e, wf, dx, n, oh, ow, f, c, k, pad2, st);
+    const int rc = fprop<ES>(e, wf, dx, n, oh, ow, f, c, k, pad2, st, g);
     cudaFreeAsync(wf, st);
     *nl = 2;
     return rc;
@@ -513,12 +514,12 @@ int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
     const int k = (int)g.kh, pad = (int)g.pad;
     int rc;
     if (kind == 0) {
-        rc = fmt == FP8B_E5M2 ? tc::cv::fprop<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st)
-                              : tc::cv::fprop<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st);
+        rc = fmt == FP8B_E5M2 ? tc::cv::fprop<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, g)
+                              : tc::cv::fprop<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, g);
         if (rc == FP8B_OK) *nlaunch = 1;
     } else if (kind == 1) {
-        rc = fmt == FP8B_E5M2 ? tc::cv::dgrad<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch)
-                              : tc::cv::dgrad<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch);
+        rc = fmt == FP8B_E5M2 ? tc::cv::dgrad<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch, g)
+                              : tc::cv::dgrad<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch, g);
     } else {
         rc = fmt == FP8B_E5M2 ? tc::cv::wgrad<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch)
                               : tc::cv::wgrad<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch);

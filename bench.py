@@ -409,16 +409,41 @@ RESNET_LAYERS = [  # (name, C, F, H=W, k): BASELINE config 4, stride 1, pad k//2
 ]
 
 
-def bench_conv(F, args, reps=5, only=None):
-    """BASELINE config 4: ResNet-50-shaped conv layers, batch N NHWC, E5M2 codes,
-    implicit GEMM on tcgen05 for fprop / dgrad / wgrad (FP32 outputs). Inputs:
-    half-normal activations, He-init weights, N(0, 1e-5) errors x 2^13 loss
-    scale, quantized RNE to E5M2 by our own kernels."""
+def _graph_ms(fn, reps):
+    """Device time of one call captured in a CUDA graph (replays, events)."""
     import torch
-    from paper_1905_12334_b200 import _lib
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    del g
+    return a.elapsed_time(b) / reps
+
+
+def bench_conv(F, args, reps=5, only=None):
+    """BASELINE config 4: ResNet-50-shaped conv layers, batch N NHWC, E5M2 codes.
+
+    * ``passes_f32``: fprop / dgrad / wgrad with FP32 outputs (the reference
+      kernels' semantics), tcgen05 implicit GEMM, each a CUDA-graph replay.
+    * ``step``: the layer's FP8 training step as config 4 runs it -- fprop with
+      the fused E5M2 Q(y) epilogue, dgrad with fused Q(dx), wgrad -> Q(dW), the
+      SR FP16 master update (reference LFSR stream) writing next step's E5M2
+      weights, and the dynamic loss scaler (floor 2^13) -- one CUDA graph.
+    Inputs: half-normal activations, He-init weights, N(0, 1e-5) errors x 2^13,
+    quantized RNE to E5M2 by our own kernels."""
+    import torch
     nb = args.conv_batch
     res = {}
-    tot_flop = tot_ms = 0.0
+    tot_flop = tot_ms = tot_step = 0.0
     for name, c, f, hw, k in RESNET_LAYERS:
         if only and name not in only:
             continue
@@ -431,11 +456,13 @@ def bench_conv(F, args, reps=5, only=None):
         es = torch.empty(P * f, dtype=torch.float32, device="cuda")
         F.fill_synthetic(es, "normal", 13, 1e-5 * 8192.0)
         X = F.quantize(xs).reshaped([nb, hw, hw, c])
+        master = F.quantize(ws, "fp16").codes
         W = F.quantize(ws).reshaped([f, k, k, c])
         E = F.quantize(es).reshaped([nb, hw, hw, f])
         del xs, ws, es
+        mom = torch.zeros(f * k * k * c, dtype=torch.float32, device="cuda")
+        scaler = F.LossScaler("dynamic-backoff", 8192.0, min_threshold_schedule=[(0, 8192.0)])
         flop = 2.0 * P * f * k * k * c
-        row = {}
         calls = {
             "fprop": lambda: F.conv2d(X, W, 1, pad, layout="nhwc", engine="tensor"),
             "dgrad": lambda: F.conv2d_backward_data(E, W, 1, pad, hw, hw, layout="nhwc",
@@ -443,37 +470,41 @@ def bench_conv(F, args, reps=5, only=None):
             "wgrad": lambda: F.conv2d_backward_weights(X, E, k, k, 1, pad, layout="nhwc",
                                                        engine="tensor"),
         }
+        row = {}
         for kind, fn in calls.items():
             assert F.conv_tensor_supported(nb, c, hw, hw, f, k, 1, pad, "fp8", kind)
-            out = fn()
-            del out
-            torch.cuda.synchronize()
-            # one pass captured in a CUDA graph: replays measure device time only
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                out = fn()
-            g.replay()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            for _ in range(reps):
-                g.replay()
-            b.record()
-            torch.cuda.synchronize()
-            ms = a.elapsed_time(b) / reps
-            del g, out
+            ms = _graph_ms(fn, reps)
             row[kind] = {"ms": round(ms, 3), "tflops": round(flop / (ms * 1e-3) / 1e12, 1)}
             tot_flop += flop
             tot_ms += ms
-        res[name] = row
-        del X, W, E
+        bwd = F.Counters()
+
+        def step():
+            bwd.zero_()
+            F.conv2d(X, W, 1, pad, layout="nhwc", engine="tensor", out_fmt="fp8", want_y=False)
+            F.conv2d_backward_data(E, W, 1, pad, hw, hw, layout="nhwc", engine="tensor",
+                                   out_fmt="fp8", out_counters=bwd, want_y=False)
+            _, qdw = F.conv2d_backward_weights(X, E, k, k, 1, pad, layout="nhwc", engine="tensor",
+                                               out_fmt="fp8", out_counters=bwd, want_y=False)
+            F.sgd_momentum_update(qdw.codes, "fp8", master, mom, lr=0.1, mu=0.9, scaler=scaler,
+                                  skip_counters=bwd, master_mode="stochastic", seed=5,
+                                  w_e5m2=W.codes)
+            scaler.step_async(True, 0, counters=bwd)
+        sms = _graph_ms(step, reps)
+        tot_step += sms
+        res[name] = {"passes_f32": row,
+                     "step": {"ms": round(sms, 3), "tflops": round(3 * flop / (sms * 1e-3) / 1e12, 1)}}
+        del X, W, E, master, mom
         torch.cuda.empty_cache()
-    res["all_layers_fprop_dgrad_wgrad"] = {"ms": round(tot_ms, 3),
-                                           "tflops": round(tot_flop / (tot_ms * 1e-3) / 1e12, 1)}
-    res["config"] = {"batch": nb, "layout": "NHWC", "dtype": "e5m2 x e5m2 -> f32",
-                     "timing": "CUDA-graph replays of one pass (device time incl. dgrad's weight "
-                               "flip and wgrad's split-K sum)"}
-    _ = _lib
+    nl = sum(1 for L in RESNET_LAYERS if not only or L[0] in only)
+    res["all_layers_passes_f32"] = {"ms": round(tot_ms, 3),
+                                    "tflops": round(tot_flop / (tot_ms * 1e-3) / 1e12, 1)}
+    res["all_layers_step"] = {"ms": round(tot_step, 3),
+                              "tflops": round(tot_flop / (tot_step * 1e-3) / 1e12, 1),
+                              "layers": nl}
+    res["config"] = {"batch": nb, "layout": "NHWC", "dtype": "e5m2 x e5m2 -> f32 / e5m2",
+                     "timing": "CUDA-graph replays (device time incl. dgrad's weight flip, "
+                               "wgrad's split-K sum, Q(dW), update and scaler)"}
     return res
 
 

@@ -36,7 +36,9 @@ struct CParams {
     int cblocks;   // fprop: channel blocks per tap
     int C;         // channels of the im2col'd tensor
     int KW, pad, OH, OW;
-    int c_tma;     // outputs go through the TMA-store epilogue
+    int c_tma;     // FP32 output goes through the TMA-store epilogue
+    int q_tma;     // or the fused output codes (when no FP32 output is written)
+    int qg;        // code chunks per TMA store
     float* ws;     // wgrad: split-K partials [splits][M][N]
 };
 
@@ -111,7 +113,8 @@ struct Geo {
 template <int ES, int MODE, int BN, int CB>
 __global__ void __launch_bounds__(THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const CParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
+                   const CParams p) {
     using G = Geo<ES, MODE, BN, CB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -263,6 +266,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_wait(tfull_bar + acc, accphase);
             fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+            EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
+                      (int64_t)tm * 128 + quarter * 32, lane, -1, p.qg, 0, nullptr};
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
@@ -270,16 +275,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int64_t col0 = (int64_t)tn * BN + c * 32;
                 if (col0 >= p.N) continue;
                 const int64_t row0 = (int64_t)tm * 128 + quarter * 32;
-                if (p.c_tma) {
+                if (p.c_tma || p.q_tma) {
                     if (MODE == 0) {
-                        epilogue_chunk(p, row, col0, v, co, cu, cn, &tmC, sbuf + (nst++ & 1) * 4096,
-                                       row0, lane);
+                        const bool last = c == BN / 32 - 1 || col0 + 32 >= p.N;
+                        epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
                     } else {
-                        float y[32];
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]);
-                        stage_store_c(&tmC, sbuf + (nst++ & 1) * 4096, y, lane, (int32_t)col0,
-                                      (int32_t)row0, s);
+                        stage_store_f32(&tmC, sbuf, nst, v, lane, (int32_t)col0, (int32_t)row0, s);
                     }
                     continue;
                 }
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (++acc == 2) { acc = 0; accphase ^= 1; }
         }
     }
-    if (p.c_tma && warp >= 2 && lane == 0) bulk_wait_all();
+    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
     if (MODE == 0 && p.ep.cq_counters) flush_counters<THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     __syncthreads();
@@ -369,8 +370,8 @@ static int num_sms() {
 }
 
 template <int ES, int MODE, int BN, int CB>
-static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, const CParams& p,
-               cudaStream_t st) {
+static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm,
+               const CUtensorMap& tqm, const CParams& p, cudaStream_t st) {
     using G = Geo<ES, MODE, BN, CB>;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -379,7 +380,7 @@ static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
     });
     const int items = p.tiles_m * p.tiles_n * p.splits;
     const int grid = items < num_sms() ? items : num_sms();
-    conv_tc_kernel<ES, MODE, BN, CB><<<grid, THREADS, G::SMEM, st>>>(ta, tb, tcm, p);
+    conv_tc_kernel<ES, MODE, BN, CB><<<grid, THREADS, G::SMEM, st>>>(ta, tb, tcm, tqm, p);
     return FP8B_OK;
 }
 
@@ -409,14 +410,18 @@ static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, i
     CUtensorMap tcm;
     memset(&tcm, 0, sizeof(tcm));
     p.c_tma = (epi_tma() && y && make_c_map(&tcm, y, P, f)) ? 1 : 0;
+    CUtensorMap tqm;
+    memset(&tqm, 0, sizeof(tqm));
+    p.qg = code_group(g.yq_fmt, bn);
+    p.q_tma = (!p.c_tma && epi_tma() && g.yq && make_q_map(&tqm, g.yq, g.yq_fmt, P, f, bn)) ? 1 : 0;
     if (cb_bytes == 128) {
-        if (bn == 64) return run<ES, 0, 64, 128>(ta, tb, tcm, p, st);
-        if (bn == 128) return run<ES, 0, 128, 128>(ta, tb, tcm, p, st);
-        return run<ES, 0, 256, 128>(ta, tb, tcm, p, st);
+        if (bn == 64) return run<ES, 0, 64, 128>(ta, tb, tcm, tqm, p, st);
+        if (bn == 128) return run<ES, 0, 128, 128>(ta, tb, tcm, tqm, p, st);
+        return run<ES, 0, 256, 128>(ta, tb, tcm, tqm, p, st);
     }
-    if (bn == 64) return run<ES, 0, 64, 64>(ta, tb, tcm, p, st);
-    if (bn == 128) return run<ES, 0, 128, 64>(ta, tb, tcm, p, st);
-    return run<ES, 0, 256, 64>(ta, tb, tcm, p, st);
+    if (bn == 64) return run<ES, 0, 64, 64>(ta, tb, tcm, tqm, p, st);
+    if (bn == 128) return run<ES, 0, 128, 64>(ta, tb, tcm, tqm, p, st);
+    return run<ES, 0, 256, 64>(ta, tb, tcm, tqm, p, st);
 }
 
 // wgrad: dw [f, k, k, c] from x [n, h, w, c] and e [n, oh, ow, f]
@@ -454,9 +459,12 @@ static int wgrad(const void* x, const void* e, float* dw, int64_t n, int64_t h, 
     CUtensorMap tcm;
     memset(&tcm, 0, sizeof(tcm));
     p.c_tma = (epi_tma() && make_ws_map(&tcm, ws, splits, p.M, p.N)) ? 1 : 0;
+    CUtensorMap tqm;
+    memset(&tqm, 0, sizeof(tqm));
+    p.q_tma = 0;
     int rc;
-    if (cb_bytes == 128) rc = run<ES, 1, 128 / ES, 128>(ta, tb, tcm, p, st);
-    else rc = run<ES, 1, 64 / ES, 64>(ta, tb, tcm, p, st);
+    if (cb_bytes == 128) rc = run<ES, 1, 128 / ES, 128>(ta, tb, tcm, tqm, p, st);
+    else rc = run<ES, 1, 64 / ES, 64>(ta, tb, tcm, tqm, p, st);
     *nl = 1;
     if (splits > 1) {
         int64_t b = (mn + 255) / 256;

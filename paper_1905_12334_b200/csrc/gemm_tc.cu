@@ -46,13 +46,16 @@ struct Params {
     int a_mn, b_mn;
     int tiles_m, tiles_n, num_kb;
     int c_tma;  // FP32 C goes out through the TMA-store epilogue
+    int q_tma;  // or the fused output codes (when no FP32 C is written)
+    int qg;     // code chunks per TMA store
     EpiArgs ep;
 };
 
 template <int ES>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const Params p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
+                   const Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -178,16 +181,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(tfull_bar + acc, accphase);
             fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+            EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
+                      (int64_t)tm * BM + quarter * 32, lane, -1, p.qg, 0, nullptr};
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
                 tmem_ld32(taddr + c * 32, v);
                 const int64_t col0 = (int64_t)tn * BN + c * 32;
-                if (p.c_tma) {
-                    if (col0 < p.N)
-                        epilogue_chunk(p, row, col0, v, co, cu, cn, &tmC, sbuf + (nst++ & 1) * 4096,
-                                       (int64_t)tm * BM + quarter * 32, lane);
-                } else if (row < p.M && col0 < p.N) {
+                if (col0 >= p.N) continue;
+                if (p.c_tma || p.q_tma) {
+                    const bool last = c == BN / 32 - 1 || col0 + 32 >= p.N;
+                    epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
+                } else if (row < p.M) {
                     epilogue_chunk(p, row, col0, v, co, cu, cn);
                 }
             }
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (++acc == 2) { acc = 0; accphase ^= 1; }
         }
     }
-    if (p.c_tma && warp >= 2 && lane == 0) bulk_wait_all();
+    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
     if (p.ep.cq_counters) flush_counters<NUM_THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     __syncthreads();
@@ -275,7 +280,8 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
 template <int ES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmC, const Params p) {
+                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
+                   const Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -400,16 +406,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(tfull_bar + acc, accphase);
             fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN2);
+            EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
+                      (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane, -1, p.qg, 0, nullptr};
 #pragma unroll 1
             for (int c = 0; c < BN2 / 32; ++c) {
                 uint32_t v[32];
                 tmem_ld32(taddr + c * 32, v);
                 const int64_t col0 = (int64_t)tn * BN2 + c * 32;
-                if (p.c_tma) {
-                    if (col0 < p.N)
-                        epilogue_chunk(p, row, col0, v, co, cu, cn, &tmC, sbuf + (nst++ & 1) * 4096,
-                                       (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane);
-                } else if (row < p.M && col0 < p.N) {
+                if (col0 >= p.N) continue;
+                if (p.c_tma || p.q_tma) {
+                    const bool last = c == BN2 / 32 - 1 || col0 + 32 >= p.N;
+                    epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
+                } else if (row < p.M) {
                     epilogue_chunk(p, row, col0, v, co, cu, cn);
                 }
             }
@@ -419,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (++acc == 2) { acc = 0; accphase ^= 1; }
         }
     }
-    if (p.c_tma && warp >= 2 && lane == 0) bulk_wait_all();
+    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
     if (p.ep.cq_counters) flush_counters<NUM_THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     cluster_sync_all();
@@ -479,6 +487,10 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
     CUtensorMap tmC;
     memset(&tmC, 0, sizeof(tmC));
     p.c_tma = (use_epi_tma() && ep.c && make_c_map(&tmC, ep.c, m, n)) ? 1 : 0;
+    CUtensorMap tmQ;
+    memset(&tmQ, 0, sizeof(tmQ));
+    p.qg = code_group(ep.cq_fmt, BN);
+    p.q_tma = (!p.c_tma && use_epi_tma() && ep.cq && make_q_map(&tmQ, ep.cq, ep.cq_fmt, m, n, BN)) ? 1 : 0;
     static int num_sms = 0;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -508,13 +520,13 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
             int grid2 = 2 * ntiles2;
             const int maxg = num_sms & ~1;
             if (grid2 > maxg) grid2 = maxg;
-            gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, tmC, p2);
+            gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, tmC, tmQ, p2);
             return FP8B_OK;
         }
     }
     const int ntiles = p.tiles_m * p.tiles_n;
     const int grid = ntiles < num_sms ? ntiles : num_sms;
-    gemm_tc_kernel<ES><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(tmA, tmB, tmC, p);
+    gemm_tc_kernel<ES><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(tmA, tmB, tmC, tmQ, p);
     return FP8B_OK;
 }
 

@@ -121,12 +121,27 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
     tn = first_n + r % width;
 }
 
-// Epilogue for one 32-column chunk of one row held in registers.
-// TMA-store staging for the FP32 output: each epilogue warp owns two 4 KB
-// buffers (32 rows x 32 FP32, 128B-swizzled to match the C tensor map), fills
-// one per 32-column chunk with st.shared.v4 and hands it to the TMA engine with
-// one cp.async.bulk.tensor store (rows/cols outside C are clipped by TMA).
+// TMA-store epilogue. Each epilogue warp owns two 4 KB staging buffers used as
+// a ring: an output chunk (32 rows x 32 columns; FP32 = 128 B per row, FP16
+// codes 64 B, E5M2 codes 32 B) is written with st.shared.v4 in the swizzle of
+// its tensor map (span = row bytes) and handed to the TMA engine with one
+// cp.async.bulk.tensor store; rows/columns outside the tensor are clipped by
+// TMA. Before a buffer is refilled its previous store must have read it
+// (wait_group.read 1: only the other buffer's store may still be pending).
 constexpr uint32_t EPI_STAGE_BYTES = 4 * 2 * 4096;  // 4 warps x 2 buffers
+
+struct EpiTma {
+    const CUtensorMap* c;  // FP32 output map (32x32 boxes, 128B swizzle) or null
+    const CUtensorMap* q;  // code output map (qg*32 x 32 boxes, row-span swizzle) or null
+    uint8_t* sbuf;         // this warp's 8 KB of staging
+    uint32_t* nst;         // this warp's buffer counter
+    int64_t row0;          // first row of the warp's 32-row slab
+    int lane;
+    int z;                 // 3-D store coordinate (split index) or -1
+    int qg;                // code chunks per store (row span = qg * 32 * code bytes)
+    int qpos;              // chunks already staged in the open code group
+    uint8_t* qbuf;         // the open code group's buffer
+};
 
 __device__ __forceinline__ void bulk_wait_read1() {
     asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -135,60 +150,101 @@ __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-__device__ __forceinline__ void stage_store_c(const CUtensorMap* tmC, uint8_t* buf, const float (&y)[32],
-                                              int lane, int32_t col0, int32_t row0, int32_t z = -1) {
-    if (lane == 0) bulk_wait_read1();  // the buffer's previous store has read it
+// Next ring buffer, once its previous store has read it.
+__device__ __forceinline__ uint8_t* stage_acquire(uint8_t* sbuf, uint32_t& nst, int lane) {
+    uint8_t* buf = sbuf + (nst++ & 1) * 4096;
+    if (lane == 0) bulk_wait_read1();
     __syncwarp();
-    const uint32_t base = smem_u32(buf) + lane * 128;
+    return buf;
+}
+// NW words of this lane's row at byte offset OFF of a SPAN-byte row, in the
+// map's swizzle (16-byte chunk index XOR the row's phase).
+template <int SPAN, int NW>
+__device__ __forceinline__ void stage_write(uint8_t* buf, int off, const uint32_t* w, int lane) {
+    const uint32_t base = smem_u32(buf) + lane * SPAN;
+    const uint32_t x = (uint32_t)(lane / (128 / SPAN)) & (SPAN / 16 - 1);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint32_t a = base + ((uint32_t)(j ^ (lane & 7)) << 4);
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(y[4 * j]),
-                     "f"(y[4 * j + 1]), "f"(y[4 * j + 2]), "f"(y[4 * j + 3])
+    for (int j = 0; j < NW / 4; ++j) {
+        const uint32_t a = base + ((((uint32_t)off >> 4) + j) ^ x) * 16u;
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[4 * j]),
+                     "r"(w[4 * j + 1]), "r"(w[4 * j + 2]), "r"(w[4 * j + 3])
                      : "memory");
     }
+}
+// Hand the warp's staged box to the TMA engine.
+__device__ __forceinline__ void stage_flush(const CUtensorMap* tm, uint8_t* buf, int lane, int32_t col0,
+                                            int32_t row0, int32_t z = -1) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) {
         if (z < 0)
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                    reinterpret_cast<uint64_t>(tmC)),
+                    reinterpret_cast<uint64_t>(tm)),
                 "r"(smem_u32(buf)), "r"(col0), "r"(row0)
                 : "memory");
         else
             asm volatile(
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                    reinterpret_cast<uint64_t>(tmC)),
+                    reinterpret_cast<uint64_t>(tm)),
                 "r"(smem_u32(buf)), "r"(col0), "r"(row0), "r"(z)
                 : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
 }
+// One 32-row x 128-byte box (32 FP32 columns) per call.
+__device__ __forceinline__ void stage_store_f32(const CUtensorMap* tm, uint8_t* sbuf, uint32_t& nst,
+                                                const uint32_t* w, int lane, int32_t col0,
+                                                int32_t row0, int32_t z = -1) {
+    uint8_t* buf = stage_acquire(sbuf, nst, lane);
+    stage_write<128, 32>(buf, 0, w, lane);
+    stage_flush(tm, buf, lane, col0, row0, z);
+}
+// Codes: chunks accumulate into one box of qg*32 columns (a 64- or 128-byte row)
+// before one store; `last` closes a partial group at the end of a tile.
+template <int ES>
+__device__ __forceinline__ void stage_codes(EpiTma* t, const uint32_t* w, int64_t col0, bool last) {
+    constexpr int NW = 8 * ES;  // 32 codes of ES bytes
+    if (t->qpos == 0) t->qbuf = stage_acquire(t->sbuf, *t->nst, t->lane);
+    const int span = t->qg * 32 * ES;
+    if (span == 128) stage_write<128, NW>(t->qbuf, t->qpos * 32 * ES, w, t->lane);
+    else stage_write<64, NW>(t->qbuf, t->qpos * 32 * ES, w, t->lane);
+    if (++t->qpos == t->qg || last) {
+        stage_flush(t->q, t->qbuf, t->lane, (int32_t)(col0 - 32 * (t->qpos - 1)), (int32_t)t->row0);
+        t->qpos = 0;
+    }
+}
 
-// Epilogue of one 32-column chunk; one row per lane. With tmC set, the whole
-// warp must call it (rows >= M included: TMA clips them) and C goes out through
-// stage_store_c; otherwise rows >= M return early.
+// Epilogue of one 32-column chunk; one row per lane. With TMA stores active
+// (t.c or t.q set) the whole warp must call it -- rows >= M included, TMA clips
+// them and the counters skip them; otherwise rows >= M return early.
 template <class P>
 __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t col0,
                                                uint32_t (&v)[32], uint32_t& co, uint32_t& cu,
-                                               uint32_t& cn, const CUtensorMap* tmC = nullptr,
-                                               uint8_t* sbuf = nullptr, int64_t row0 = 0,
-                                               int lane = 0) {
+                                               uint32_t& cn, EpiTma* tm_ = nullptr,
+                                               bool last = false) {
     const EpiArgs& ep = p.ep;
     float y[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]);
     const bool full = col0 + 32 <= p.N;
+    const bool live = row < p.M;
     if (ep.bias) {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
             if (full || col0 + j < p.N) y[j] = __fadd_rn(y[j], __ldg(ep.bias + col0 + j));
     }
-    if (tmC) stage_store_c(tmC, sbuf, y, lane, (int32_t)col0, (int32_t)row0);
-    if (row >= p.M) return;
+    const bool c_tma = tm_ && tm_->c, q_tma = tm_ && tm_->q;
+    if (c_tma) {
+        uint32_t w[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(y[j]);
+        stage_store_f32(tm_->c, tm_->sbuf, *tm_->nst, w, tm_->lane, (int32_t)col0,
+                        (int32_t)tm_->row0, tm_->z);
+    }
+    if (!live && !q_tma) return;
     const int64_t base = row * p.N + col0;
-    if (ep.c && !tmC) {
+    if (ep.c && !c_tma && live) {
         if (full && (p.N % 4 == 0)) {
             float4* dst = reinterpret_cast<float4*>(ep.c + base);
 #pragma unroll
@@ -199,19 +255,68 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
                 if (col0 + j < p.N) ep.c[base + j] = y[j];
         }
     }
-    if (ep.cq) {
+    if (ep.cq && ep.cq_mode == FP8B_RNE && ep.cq_fmt == FP8B_E5M2) {
+        // Lean E5M2 RNE path: paired hardware cvt packed straight into words;
+        // one max.NaN per element screens for overflow / NaN (rare slow path
+        // applies the reference fix-ups and counts them); underflow = nonzero
+        // input whose magnitude rounds to zero, counted on real rows/columns.
+        const bool sat = ep.cq_sat != 0;
+        uint32_t w[8];
+        float amax = 0.0f;
+        uint32_t unf = 0;
+        const int nvalid = full ? 32 : (int)(p.N - col0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t lo = cvt_e5m2x2(y[4 * q], y[4 * q + 1]);
+            const uint32_t hi = cvt_e5m2x2(y[4 * q + 2], y[4 * q + 3]);
+            w[q] = __byte_perm(lo, hi, 0x5410);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            float m;
+            asm("max.NaN.f32 %0, %1, %2;" : "=f"(m) : "f"(amax), "f"(fabsf(y[j])));
+            amax = m;
+            unf += ((__float_as_uint(y[j]) & 0x7FFFFFFFu) - 1u < Fmt<2>::rne_unf_max) && j < nvalid;
+        }
+        if (!(amax <= 57344.0f)) {  // an overflowing or NaN output in this row chunk
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t hw = (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+                uint32_t b = 0, nn = 0, uu = 0;
+                const uint32_t c = fix_rne<2>(hw, __float_as_uint(y[j]), sat, b, nn, uu);
+                w[j >> 2] = (w[j >> 2] & ~(0xFFu << (8 * (j & 3)))) | (c << (8 * (j & 3)));
+                if (live && j < nvalid) { co += b - nn; cn += nn; }
+            }
+        }
+        if (live) cu += unf;
+        if (q_tma) {
+            stage_codes<1>(tm_, w, col0, last);
+        } else if (live) {
+            uint8_t* dst = reinterpret_cast<uint8_t*>(ep.cq) + base;
+            if (full && (p.N % 16 == 0)) {
+                uint4* d4 = reinterpret_cast<uint4*>(dst);
+                d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < nvalid) dst[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+            }
+        }
+    } else if (ep.cq) {
         uint32_t code[32];
         const bool sat = ep.cq_sat != 0;
+        const bool cnt = live && full;  // counters: real rows, whole chunk in range
         if (ep.cq_mode == FP8B_RNE && ep.cq_fmt == FP8B_E5M2) {
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
                 const uint32_t pr = cvt_e5m2x2(y[j], y[j + 1]);
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
+                for (int h = 0; h < 2; ++h) {
                     uint32_t b = 0, nn = 0, uu = 0;
-                    code[j + t] = fix_rne<2>(t ? (pr >> 8) : (pr & 0xFFu),
-                                             __float_as_uint(y[j + t]), sat, b, nn, uu);
-                    if (full || col0 + j + t < p.N) { co += b - nn; cn += nn; cu += uu; }
+                    code[j + h] = fix_rne<2>(h ? (pr >> 8) : (pr & 0xFFu),
+                                             __float_as_uint(y[j + h]), sat, b, nn, uu);
+                    if (cnt || (live && col0 + j + h < p.N)) { co += b - nn; cn += nn; cu += uu; }
                 }
             }
         } else {
@@ -224,40 +329,43 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
                     code[j] = encode_int<2>(__float_as_uint(y[j]), ep.cq_mode, r16, sat, o, u, na);
                 else
                     code[j] = encode_int<10>(__float_as_uint(y[j]), ep.cq_mode, r16, sat, o, u, na);
-                if (full || col0 + j < p.N) { co += o; cu += u; cn += na; }
+                if (cnt || (live && col0 + j < p.N)) { co += o; cu += u; cn += na; }
             }
         }
         if (ep.cq_fmt == FP8B_E5M2) {
-            uint8_t* dst = reinterpret_cast<uint8_t*>(ep.cq) + base;
-            if (full && (p.N % 16 == 0)) {
-                uint4* d4 = reinterpret_cast<uint4*>(dst);
+            uint32_t w[8];
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    uint32_t w[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int b = 16 * j + 4 * q;
-                        w[q] = code[b] | (code[b + 1] << 8) | (code[b + 2] << 16) | (code[b + 3] << 24);
-                    }
-                    d4[j] = make_uint4(w[0], w[1], w[2], w[3]);
+            for (int q = 0; q < 8; ++q)
+                w[q] = code[4 * q] | (code[4 * q + 1] << 8) | (code[4 * q + 2] << 16) | (code[4 * q + 3] << 24);
+            if (q_tma) {
+                stage_codes<1>(tm_, w, col0, last);
+            } else if (live) {
+                uint8_t* dst = reinterpret_cast<uint8_t*>(ep.cq) + base;
+                if (full && (p.N % 16 == 0)) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst);
+                    d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                    d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                } else {
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < p.N) dst[j] = (uint8_t)code[j];
                 }
-            } else {
-                for (int j = 0; j < 32; ++j)
-                    if (col0 + j < p.N) dst[j] = (uint8_t)code[j];
             }
         } else {
-            uint16_t* dst = reinterpret_cast<uint16_t*>(ep.cq) + base;
-            if (full && (p.N % 8 == 0)) {
-                uint4* d4 = reinterpret_cast<uint4*>(dst);
+            uint32_t w[16];
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    d4[j] = make_uint4(code[8 * j] | (code[8 * j + 1] << 16),
-                                       code[8 * j + 2] | (code[8 * j + 3] << 16),
-                                       code[8 * j + 4] | (code[8 * j + 5] << 16),
-                                       code[8 * j + 6] | (code[8 * j + 7] << 16));
-            } else {
-                for (int j = 0; j < 32; ++j)
-                    if (col0 + j < p.N) dst[j] = (uint16_t)code[j];
+            for (int q = 0; q < 16; ++q) w[q] = code[2 * q] | (code[2 * q + 1] << 16);
+            if (q_tma) {
+                stage_codes<2>(tm_, w, col0, last);
+            } else if (live) {
+                uint16_t* dst = reinterpret_cast<uint16_t*>(ep.cq) + base;
+                if (full && (p.N % 8 == 0)) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) d4[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+                } else {
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < p.N) dst[j] = (uint16_t)code[j];
+                }
             }
         }
     }
@@ -309,6 +417,26 @@ static inline bool make_c_map(CUtensorMap* tm, const float* c, int64_t m, int64_
     if (!c || (uintptr_t)c % 16 || (n * 4) % 16 || m <= 0 || n <= 0) return false;
     if (m > INT32_MAX || n > INT32_MAX) return false;
     return make_map(tm, c, 4, (uint64_t)n, (uint64_t)m, 32, 32);
+}
+
+// Store map for an [m, n] code output (E5M2 u8 / FP16 u16) whose boxes are 32
+// rows x qg*32 columns with the swizzle of that row span (64 or 128 bytes);
+// qg = min(tile_n / 32, 4 / code bytes). False when TMA cannot address it.
+static inline int code_group(int fmt, int tile_n) {
+    const int es = fmt == FP8B_E5M2 ? 1 : 2;
+    const int g = tile_n / 32 < 4 / es ? tile_n / 32 : 4 / es;
+    return g;
+}
+static inline bool make_q_map(CUtensorMap* tm, const void* q, int fmt, int64_t m, int64_t n,
+                              int tile_n) {
+    const int es = fmt == FP8B_E5M2 ? 1 : 2;
+    const int qg = code_group(fmt, tile_n);
+    const int span = qg * 32 * es;
+    if (span != 64 && span != 128) return false;
+    if (!q || (uintptr_t)q % 16 || (n * es) % 16 || m <= 0 || n <= 0) return false;
+    if (m > INT32_MAX || n > INT32_MAX) return false;
+    return make_map(tm, q, es, (uint64_t)n, (uint64_t)m, (uint32_t)(qg * 32), 32,
+                    span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 }  // namespace tc

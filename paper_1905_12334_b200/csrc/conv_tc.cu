@@ -27,7 +27,11 @@ namespace fp8b {
 namespace tc {
 namespace cv {
 
-constexpr int THREADS = 192;
+// 2 warps (TMA producer, MMA issuer) + EW epilogue warps; EW = 8 doubles the
+// epilogue's issue rate for short-K passes (1x1 convs), where the output Q node
+// and stores, not the MMAs, set the pace.
+template <int EW>
+constexpr int threads_of() { return 64 + 32 * EW; }
 
 struct CParams {
     int64_t M, N;  // output matrix (epilogue): fprop [P, F]; wgrad [F, taps*C]
@@ -94,15 +98,16 @@ __device__ __forceinline__ void tma_im2col_4d(const CUtensorMap* tm, void* dst, 
 }
 
 // Compile-time geometry of one kernel instance.
-template <int ES, int MODE, int BN, int CB>
+template <int ES, int MODE, int BN, int CB, int EW>
 struct Geo {
+    static constexpr uint32_t EPI_BYTES = (uint32_t)EW * 8192;  // 2 x 4 KB per epilogue warp
     static constexpr int KPIX = 128 / ES;            // wgrad: pixels per K block
     static constexpr uint32_t A_BYTES = MODE == 0 ? 128u * CB : 128u * 128u;
     static constexpr uint32_t B_BYTES = MODE == 0 ? (uint32_t)BN * CB : (uint32_t)KPIX * CB;
     static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
-    static constexpr int BUDGET = 232448 - (int)EPI_STAGE_BYTES - 1280;
+    static constexpr int BUDGET = 232448 - (int)EPI_BYTES - 1280;
     static constexpr int STAGES = (BUDGET / (int)STAGE) > 16 ? 16 : (BUDGET / (int)STAGE);
-    static constexpr uint32_t SMEM = STAGES * STAGE + EPI_STAGE_BYTES + 1024 + 256;
+    static constexpr uint32_t SMEM = STAGES * STAGE + EPI_BYTES + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr uint32_t SWZ_LAYOUT = CB == 128 ? 2u : 4u;  // UMMA layout code
     static constexpr uint32_t SBO = 8u * CB;                     // 8 rows of one swizzle atom
@@ -110,16 +115,16 @@ struct Geo {
 
 // MODE 0: fprop (A = im2col X, K-major; B = W [F, taps*C], K-major).
 // MODE 1: wgrad (A = E [P, F], MN-major; B = im2col X, MN-major), split-K.
-template <int ES, int MODE, int BN, int CB>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int ES, int MODE, int BN, int CB, int EW>
+__global__ void __launch_bounds__(threads_of<EW>(), 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
                    const CParams p) {
-    using G = Geo<ES, MODE, BN, CB>;
+    using G = Geo<ES, MODE, BN, CB, EW>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE + EPI_STAGE_BYTES);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE + G::EPI_BYTES);
     uint64_t* empty_bar = full_bar + G::STAGES;
     uint64_t* tfull_bar = empty_bar + G::STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar + a, 1);
-            mbar_init(tempty_bar + a, 4);
+            mbar_init(tempty_bar + a, EW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -254,8 +259,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        const int quarter = warp & 3;
-        uint8_t* sbuf = smem + G::STAGES * G::STAGE + quarter * 8192;
+        const int quarter = warp & 3;             // TMEM lanes 32*quarter .. +31
+        const int ew = warp - 2;                   // epilogue warp index
+        constexpr int NC = BN / 32;                // 32-column chunks per tile
+        constexpr int PER = NC / (EW / 4);         // chunks per warp (column halves when EW = 8)
+        const int c_lo = (ew / 4) * PER;
+        uint8_t* sbuf = smem + G::STAGES * G::STAGE + ew * 8192;
         uint32_t nst = 0;
         int acc = 0;
         uint32_t accphase = 0;
@@ -269,7 +278,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
                       (int64_t)tm * 128 + quarter * 32, lane, -1, p.qg, 0, nullptr};
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = c_lo; c < c_lo + PER; ++c) {
                 uint32_t v[32];
                 tmem_ld32(taddr + c * 32, v);
                 const int64_t col0 = (int64_t)tn * BN + c * 32;
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int64_t row0 = (int64_t)tm * 128 + quarter * 32;
                 if (p.c_tma || p.q_tma) {
                     if (MODE == 0) {
-                        const bool last = c == BN / 32 - 1 || col0 + 32 >= p.N;
+                        const bool last = c == c_lo + PER - 1 || col0 + 32 >= p.N;
                         epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
                     } else {
                         stage_store_f32(&tmC, sbuf, nst, v, lane, (int32_t)col0, (int32_t)row0, s);
@@ -303,7 +312,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
-    if (MODE == 0 && p.ep.cq_counters) flush_counters<THREADS>(co, cu, cn, p.ep.cq_counters);
+    if (MODE == 0 && p.ep.cq_counters) flush_counters<threads_of<EW>()>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -369,18 +378,18 @@ static int num_sms() {
     return v;
 }
 
-template <int ES, int MODE, int BN, int CB>
+template <int ES, int MODE, int BN, int CB, int EW = 4>
 static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm,
                const CUtensorMap& tqm, const CParams& p, cudaStream_t st) {
-    using G = Geo<ES, MODE, BN, CB>;
+    using G = Geo<ES, MODE, BN, CB, EW>;
     static std::once_flag once;
     std::call_once(once, [] {
-        cudaFuncSetAttribute(conv_tc_kernel<ES, MODE, BN, CB>,
+        cudaFuncSetAttribute(conv_tc_kernel<ES, MODE, BN, CB, EW>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     });
     const int items = p.tiles_m * p.tiles_n * p.splits;
     const int grid = items < num_sms() ? items : num_sms();
-    conv_tc_kernel<ES, MODE, BN, CB><<<grid, THREADS, G::SMEM, st>>>(ta, tb, tcm, tqm, p);
+    conv_tc_kernel<ES, MODE, BN, CB, EW><<<grid, threads_of<EW>(), G::SMEM, st>>>(ta, tb, tcm, tqm, p);
     return FP8B_OK;
 }
 
@@ -412,16 +421,24 @@ static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, i
     p.c_tma = (epi_tma() && y && make_c_map(&tcm, y, P, f)) ? 1 : 0;
     CUtensorMap tqm;
     memset(&tqm, 0, sizeof(tqm));
-    p.qg = code_group(g.yq_fmt, bn);
-    p.q_tma = (!p.c_tma && epi_tma() && g.yq && make_q_map(&tqm, g.yq, g.yq_fmt, P, f, bn)) ? 1 : 0;
+    // short K loops (1x1 convs): 8 epilogue warps split each tile's columns
+    const bool ew8 = p.num_kb <= 4 && bn >= 128;
+    const int cols_per_warp = ew8 ? bn / 2 : bn;
+    p.qg = code_group(g.yq_fmt, cols_per_warp);
+    p.q_tma = (!p.c_tma && epi_tma() && g.yq &&
+               make_q_map(&tqm, g.yq, g.yq_fmt, P, f, cols_per_warp)) ? 1 : 0;
     if (cb_bytes == 128) {
         if (bn == 64) return run<ES, 0, 64, 128>(ta, tb, tcm, tqm, p, st);
-        if (bn == 128) return run<ES, 0, 128, 128>(ta, tb, tcm, tqm, p, st);
-        return run<ES, 0, 256, 128>(ta, tb, tcm, tqm, p, st);
+        if (bn == 128) return ew8 ? run<ES, 0, 128, 128, 8>(ta, tb, tcm, tqm, p, st)
+                                  : run<ES, 0, 128, 128>(ta, tb, tcm, tqm, p, st);
+        return ew8 ? run<ES, 0, 256, 128, 8>(ta, tb, tcm, tqm, p, st)
+                   : run<ES, 0, 256, 128>(ta, tb, tcm, tqm, p, st);
     }
     if (bn == 64) return run<ES, 0, 64, 64>(ta, tb, tcm, tqm, p, st);
-    if (bn == 128) return run<ES, 0, 128, 64>(ta, tb, tcm, tqm, p, st);
-    return run<ES, 0, 256, 64>(ta, tb, tcm, tqm, p, st);
+    if (bn == 128) return ew8 ? run<ES, 0, 128, 64, 8>(ta, tb, tcm, tqm, p, st)
+                              : run<ES, 0, 128, 64>(ta, tb, tcm, tqm, p, st);
+    return ew8 ? run<ES, 0, 256, 64, 8>(ta, tb, tcm, tqm, p, st)
+               : run<ES, 0, 256, 64>(ta, tb, tcm, tqm, p, st);
 }
 
 // wgrad: dw [f, k, k, c] from x [n, h, w, c] and e [n, oh, ow, f]

@@ -17,7 +17,7 @@ import sys
 
 BENCH_KEYS = {
     "quant_elem_kernel<2, 0, 256>": "e5m2_rne",
-    "quant_lfsr_staged_kernel<2>": "e5m2_sr_lfsr",
+    "quant_lfsr_warp_kernel<2>": "e5m2_sr_lfsr",
     "quant_elem_kernel<10, 1, 256>": "fp16_sr_counter",
 }
 
@@ -42,45 +42,54 @@ def _short(name):
 
 
 def launches(csv_path, out_md):
+    """Per kernel, launches split into the full-size class (the bench's timed
+    2^28-element sweep: DRAM bytes >= 1/2 of the kernel's largest launch) and
+    the small rest (e2e chunks, warm-up of other sizes); the roofline traffic is
+    the full-size median."""
     text = open(csv_path).read()
     start = text.find('"ID"')
     rows = list(csv.DictReader(io.StringIO(text[start:])))
-    per = collections.defaultdict(lambda: {"n": 0, "us": [], "rd": [], "wr": []})
+    per_launch = collections.OrderedDict()
     order = []
+    scale_t = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+    scale_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for r in rows:
-        k = _short(r["Kernel Name"])
-        if k not in per:
-            order.append(k)
-        m, v = r["Metric Name"], r["Metric Value"].replace(",", "")
+        key = (r["ID"], _short(r["Kernel Name"]))
+        if key[1] not in order:
+            order.append(key[1])
+        d = per_launch.setdefault(key, {"us": 0.0, "rd": 0.0, "wr": 0.0})
+        m, v = r["Metric Name"], float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
-        d = per[k]
         if m == "gpu__time_duration.sum":
-            d["n"] += 1
-            d["us"].append(float(v) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0,
-                                       "ms": 1e3, "msecond": 1e3}.get(unit, 1.0))
+            d["us"] = v * scale_t.get(unit, 1.0)
         elif m == "dram__bytes_read.sum":
-            d["rd"].append(float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1))
+            d["rd"] = v * scale_b.get(unit, 1)
         elif m == "dram__bytes_write.sum":
-            d["wr"].append(float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1))
-    tot = sum(sum(d["us"]) for d in per.values())
+            d["wr"] = v * scale_b.get(unit, 1)
+    tot = sum(d["us"] for d in per_launch.values())
+    med = lambda a: sorted(a)[len(a) // 2] if a else 0.0  # noqa: E731
     lines = ["# ncu launch list (cold cache, serialised; compare shares, not absolutes)", "",
              f"source: `{csv_path}`", "",
-             "| kernel | launches | median us | share of kernel time | DRAM read MB/launch | DRAM write MB/launch |",
-             "|---|---|---|---|---|---|"]
+             "Per kernel: the full-size launches (DRAM bytes >= 1/2 of its largest launch: the",
+             "timed 2^28-element sweep) and the small ones (e2e chunks) separately.", "",
+             "| kernel | class | launches | median us | share of kernel time | DRAM read MB/launch | DRAM write MB/launch |",
+             "|---|---|---|---|---|---|---|"]
     traffic = {}
     for k in order:
-        d = per[k]
-        if not d["n"]:
-            continue
-        med = lambda a: sorted(a)[len(a) // 2] if a else 0.0
-        mean = med(d["us"])  # median launch (the list mixes the 2^28 sweep with small e2e runs)
-        rd = med(d["rd"])
-        wr = med(d["wr"])
-        lines.append(f"| `{k}` | {d['n']} | {mean:.1f} | {100 * sum(d['us']) / tot:.1f}% | "
-                     f"{rd / 1e6:.1f} | {wr / 1e6:.1f} |")
-        for pat, key in BENCH_KEYS.items():
-            if k.startswith(pat.split("<")[0]) and k.replace(" ", "") == pat.replace(" ", ""):
-                traffic[key] = round(rd + wr)
+        ls = [d for (i, kk), d in per_launch.items() if kk == k]
+        big = max(d["rd"] + d["wr"] for d in ls)
+        for cls, group in (("full", [d for d in ls if d["rd"] + d["wr"] >= 0.5 * big]),
+                           ("small", [d for d in ls if d["rd"] + d["wr"] < 0.5 * big])):
+            if not group:
+                continue
+            us = med([d["us"] for d in group])
+            rd, wr = med([d["rd"] for d in group]), med([d["wr"] for d in group])
+            lines.append(f"| `{k}` | {cls} | {len(group)} | {us:.1f} | "
+                         f"{100 * sum(d['us'] for d in group) / tot:.1f}% | {rd / 1e6:.1f} | {wr / 1e6:.1f} |")
+            if cls == "full":
+                for pat, key in BENCH_KEYS.items():
+                    if k.replace(" ", "") == pat.replace(" ", ""):
+                        traffic[key] = round(rd + wr)
     open(out_md, "w").write("\n".join(lines) + "\n")
     tj = os.path.join(os.path.dirname(out_md), "dram_traffic.json")
     json.dump(traffic, open(tj, "w"), indent=1)

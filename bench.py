@@ -208,7 +208,15 @@ def run_ours(args):
     if rank == 0 and not args.no_extras:
         result["update"] = bench_update(F, args)
         result["gemm"] = bench_gemm(F, args, bf16_peak)
+        result["dense_step"] = bench_dense_step(F, args)
         result["conv"] = bench_conv(F, args)
+    if not args.no_extras:
+        # collective workloads: every rank takes part
+        del x, c8a, c8b, c16
+        torch.cuda.empty_cache()
+        result["gemm_sharded"] = bench_gemm_sharded(F, args, world, rank, dist)
+        if args.tf_steps > 0:
+            result["transformer"] = bench_transformer(F, args, world, rank, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(x, args)
     if dist:
@@ -508,6 +516,169 @@ def bench_conv(F, args, reps=5, only=None):
     return res
 
 
+def bench_dense_step(F, args):
+    """BASELINE config 1: one Dense layer FP8 training step (X[512x1024],
+    W[1024x1024] ~ N(0, 1/1024), dY ~ N(0, 1e-4) x 2^13): Q(X), fprop + fused
+    Q(Y), Q(E), wgrad + Q(dW), bprop + fused Q(dX), gate, SR FP16 master update
+    writing the next E5M2 W, dynamic scaler -- fp8b_dense_step, one CUDA graph.
+    Launch-latency bound at this size; reported in microseconds."""
+    import torch
+    B, I, O_ = 512, 1024, 1024
+    x = torch.empty(B * I, dtype=torch.float32, device="cuda")
+    w = torch.empty(I * O_, dtype=torch.float32, device="cuda")
+    e = torch.empty(B * O_, dtype=torch.float32, device="cuda")
+    F.fill_synthetic(x, "normal", 0, 1.0)
+    F.fill_synthetic(w, "normal", 1, 1.0 / 32.0)
+    F.fill_synthetic(e, "normal", 2, 0.01 * 8192.0)
+    sc = F.LossScaler("dynamic-backoff", 8192.0, min_threshold_schedule=[(0, 8192.0)])
+    out = {}
+    for engine in ("tensor",):
+        L = F.DenseLayer(w.reshape(I, O_), batch=B, lr=0.1, mu=0.9, scaler=sc, engine=engine,
+                         master_mode="stochastic", seed=1)
+        l0 = F.launch_count()
+        L.step(x, e, 0)
+        torch.cuda.synchronize()
+        launches = F.launch_count() - l0
+        ms = _graph_ms(lambda: L.step(x, e, 0), 200)
+        flop = 3 * 2.0 * B * I * O_
+        out[engine] = {"us": round(ms * 1e3, 2), "tflops": round(flop / (ms * 1e-3) / 1e12, 1),
+                       "launches": launches, "grads_finite": L.grads_finite()}
+    out["config"] = {"workload": "config1: Dense 512x1024x1024 step", "timing":
+                     "CUDA-graph replays, device time per step (200 replays)",
+                     "master": "SR FP16 (reference LFSR stream)", "loss_scale": 8192}
+    return out
+
+
+def bench_gemm_sharded(F, args, world, rank, dist):
+    """BASELINE config 3's large shapes sharded over N: every rank
+    holds all of A and a K x N/g panel of B and computes its M x N/g panel of C.
+    No reduction; aggregate TFLOP/s = total FLOP / max-over-ranks time."""
+    import torch
+    res = {}
+    for (m, n, k) in [(16384, 16384, 16384), (16384, 1024, 16384)]:
+        ng = n // world
+        x = torch.empty(m * k + k * ng, dtype=torch.float32, device="cuda")
+        F.fill_synthetic(x, "normal", 3 + rank, 1.0)
+        qa = F.quantize(x[: m * k]).codes
+        qb = F.quantize(x[m * k:]).codes
+        del x
+        cq = torch.empty(m * ng, dtype=torch.uint8, device="cuda")
+        for _ in range(3):
+            F.gemm_codes(qa, qb, m, ng, k, "fp8", want_c=False, out_fmt="fp8", out_codes=cq)
+        reps = 5
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(reps):
+            F.gemm_codes(qa, qb, m, ng, k, "fp8", want_c=False, out_fmt="fp8", out_codes=cq)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        tf = 2.0 * m * n * k / (ms * 1e-3) / 1e12
+        res[f"{m}x{n}x{k}"] = {"ms": round(ms, 3), "tflops": round(tf, 1),
+                               "tflops_per_gpu": round(tf / world, 1),
+                               "per_rank_shape": f"{m}x{ng}x{k}", "out": "e5m2"}
+        del qa, qb, cq
+        torch.cuda.empty_cache()
+    res["config"] = {"parallelism": f"N-sharded x{world}, A replicated, no collective",
+                     "scaling": "strong"}
+    return res
+
+
+def bench_transformer(F, args, world, rank, dist):
+    """BASELINE config 5: Transformer-base linear layers (6 enc + 6 dec, d 512,
+    FFN 2048, vocab 32000), data-parallel FP8 training step over a global batch
+    of 4096 x 256 tokens split over the ranks (strong scaling): fprop + fused
+    Q(Y), dgrad + fused Q(dX), wgrad (fused Q(dW) at N=1; FP32 dW all-reduced
+    over NCCL before Q(dW) at N>1), one SR FP16 master update over all 60.5M
+    parameters writing next step's E5M2 weights, device dynamic loss scaler.
+    Attention / layernorm / embedding / loss are not in the reference and are
+    not run: every layer reads seeded synthetic E5M2 activations / errors."""
+    import torch
+    from paper_1905_12334_b200.stack import (LinearStack, linear_flops_per_token,
+                                             transformer_base_layers)
+    layers = transformer_base_layers()
+    T = args.tf_tokens // world
+    st_tmp = [(i * o + 4095) // 4096 * 4096 for _, i, o in layers]
+    w = torch.empty(sum(st_tmp), dtype=torch.float32, device="cuda")
+    off = 0
+    for (_, i, o), sz in zip(layers, st_tmp):
+        F.fill_synthetic(w[off:off + i * o], "normal", 100 + off, (1.0 / i) ** 0.5)
+        w[off + i * o:off + sz].zero_()
+        off += sz
+    max_in = max(i for _, i, _ in layers)
+    max_out = max(o for _, _, o in layers)
+
+    def codes(n, kind, seed, p):
+        buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+        tmp = torch.empty(min(n, 1 << 28), dtype=torch.float32, device="cuda")
+        for c0 in range(0, n, tmp.numel()):
+            c1 = min(n, c0 + tmp.numel())
+            F.fill_synthetic(tmp[: c1 - c0], kind, seed + c0, p)
+            F.quantize(tmp[: c1 - c0], out=buf[c0:c1])
+        del tmp
+        return buf
+
+    xbuf = codes(T * max_in, "halfnormal", 1000 * (rank + 1), 1.0)
+    ebuf = codes(T * max_out, "normal", 2000 * (rank + 1), 0.1)
+    ybuf = torch.empty(T * max_out, dtype=torch.uint8, device="cuda")
+    dxbuf = torch.empty(T * max_in, dtype=torch.uint8, device="cuda")
+    xs = [xbuf[: T * i] for _, i, _ in layers]
+    es = [ebuf[: T * o] for _, _, o in layers]
+    ys = [ybuf[: T * o] for _, _, o in layers]
+    dxs = [dxbuf[: T * i] for _, i, _ in layers]
+    scaler = F.LossScaler("dynamic-backoff", 8192.0, min_threshold_schedule=[(0, 8192.0)])
+    stack = LinearStack(layers, T, w, lr=1e-3, mu=0.9, scaler=scaler, master_mode="stochastic",
+                        seed=11)
+    del w
+    torch.cuda.empty_cache()
+    for it in range(args.tf_warmup):
+        stack.step(xs, es, it, ys=ys, dxs=dxs)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = F.launch_count()
+    gates = []
+    a.record()
+    for it in range(args.tf_steps):
+        _, bwd = stack.step(xs, es, args.tf_warmup + it, ys=ys, dxs=dxs)
+        gates.append(bwd)
+    b.record()
+    torch.cuda.synchronize()
+    launches = (F.launch_count() - l0) // args.tf_steps
+    ms = a.elapsed_time(b) / args.tf_steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flop = linear_flops_per_token(layers) * T * world
+    gate = [g.values() for g in gates]
+    res = {"ms_per_step": round(ms, 2), "tokens_per_s": round(T * world / (ms * 1e-3), 0),
+           "tflops": round(flop / (ms * 1e-3) / 1e12, 1),
+           "tflops_per_gpu": round(flop / world / (ms * 1e-3) / 1e12, 1),
+           "launches_per_step": launches, "update_skipped_steps": sum(1 for g in gate
+                                                                     if g[0] + g[2] > 0),
+           "config": {"workload": "config5: Transformer-base linear layers, FP8 E5M2 training step",
+                      "global_tokens": T * world, "tokens_per_gpu": T, "layers": len(layers),
+                      "params": stack.nparams, "linear_tflop_per_step": round(flop / 1e12, 1),
+                      "parallelism": f"dp{world}" + (", FP32 dW all-reduce (NCCL) before Q(dW)"
+                                                     if world > 1 else ", fused Q(dW)"),
+                      "scaling": "strong (global batch fixed)",
+                      "data": "synthetic E5M2 activations (half-normal) / errors N(0, 0.01)",
+                      "not_run": "attention, layernorm, embedding, loss (absent from reference)"}}
+    del stack, xbuf, ebuf, ybuf, dxbuf
+    torch.cuda.empty_cache()
+    return res
+
+
 def cpu_baseline(x_dev, args):
     """The reference's own quantize (oracle/_ref, compiled from /root/reference)
     on this host's cores, block-parallel (bit-identical to serial), over a bounded
@@ -585,6 +756,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--conv-batch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tf-tokens", type=int, default=4096 * 256)
+    ap.add_argument("--tf-steps", type=int, default=2)
+    ap.add_argument("--tf-warmup", type=int, default=1)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -79,6 +79,15 @@ int get_tables(fp8b::LfsrTables* out) {
         g_tabs[dev].tabx = dt;
         g_tabs[dev].pos = dp;
         g_tab_ok[dev] = true;
+        // Split-K workspaces (GEMM, conv wgrad) come from the device's default
+        // stream-ordered pool; keep freed blocks mapped across synchronisations
+        // so a hot call never pays for re-mapping them.
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
     }
     *out = g_tabs[dev];
     return FP8B_OK;

@@ -48,6 +48,8 @@ struct Params {
     int c_tma;  // FP32 C goes out through the TMA-store epilogue
     int q_tma;  // or the fused output codes (when no FP32 C is written)
     int qg;     // code chunks per TMA store
+    int dbg;    // 2-SM kernel diagnostics (FP8B_GEMM_DBG bits): 1 = no MMAs, 2 = no operand loads, 4 = no epilogue
+    int splits; // 2-SM kernel: split-K factor (>1: FP32 partials into the 3-D workspace map tmC)
     EpiArgs ep;
 };
 
@@ -295,7 +297,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t rank = cluster_rank();
     constexpr int BKE = BKB / ES, UK = 32 / ES, MN_CHUNK = 128 / ES;
     const int ntiles = p.tiles_m * p.tiles_n;  // 256x256 tiles
+    const int nitems = ntiles * p.splits;      // (tile, K-split) work items
     const int cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    (void)ntiles;
+    auto item_of = [&](int item, int& tm, int& tn, int& s, int& kb0, int& kb1) {
+        const int tile = item / p.splits;
+        s = item - tile * p.splits;
+        tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+        kb0 = (int)((int64_t)p.num_kb * s / p.splits);
+        kb1 = (int)((int64_t)p.num_kb * (s + 1) / p.splits);
+    };
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -326,13 +337,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
-                int tm, tn;
-                tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+            for (int item = cluster_id; item < nitems; item += nclusters) {
+                int tm, tn, s, kb0, kb1;
+                item_of(item, tm, tn, s, kb0, kb1);
                 const int32_t m0 = tm * BM2 + (int32_t)rank * 128, n0 = tn * BN2 + (int32_t)rank * 128;
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty_bar + stage, phase ^ 1);
                     const uint32_t fb = mapa_u32(smem_u32(full_bar + stage), 0);
+                    if (p.dbg & 2) {
+                        if (rank == 0) mbar_expect_tx(full_bar + stage, 0);
+                        if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     if (rank == 0) mbar_expect_tx(full_bar + stage, 2 * STAGE2_BYTES);
                     uint8_t* sA = smem + stage * STAGE2_BYTES;
                     uint8_t* sB = sA + A2_BYTES;
@@ -367,23 +383,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t accphase = 0;
-            for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+            for (int item = cluster_id; item < nitems; item += nclusters) {
+                int tm, tn, s, kb0, kb1;
+                item_of(item, tm, tn, s, kb0, kb1);
                 mbar_wait(tempty_bar + acc, accphase ^ 1);
                 fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(full_bar + stage, phase);
                     fence_after();
                     const uint32_t a_base = smem_u32(smem + stage * STAGE2_BYTES);
                     const uint32_t b_base = a_base + A2_BYTES;
 #pragma unroll
                     for (int k = 0; k < BKB / 32; ++k) {
+                        if (p.dbg & 1) break;
                         uint64_t ad, bd;
                         if (!p.a_mn) ad = umma_desc(a_base + 32 * k, 16, 1024);
                         else ad = umma_desc(a_base + k * UK * 128, BKE * 128, 1024);
                         if (!p.b_mn) bd = umma_desc(b_base + 32 * k, 16, 1024);
                         else bd = umma_desc(b_base + k * UK * 128, BKE * 128, 1024);
-                        mma2<ES>(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        mma2<ES>(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                     }
                     umma_commit_mc(empty_bar + stage);
                     if (++stage == STAGES2) { stage = 0; phase ^= 1; }
@@ -399,17 +418,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int acc = 0;
         uint32_t accphase = 0;
         const uint32_t te_leader = mapa_u32(smem_u32(tempty_bar), 0);
-        for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
-            int tm, tn;
-                tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+        for (int item = cluster_id; item < nitems; item += nclusters) {
+            int tm, tn, s, kb0, kb1;
+            item_of(item, tm, tn, s, kb0, kb1);
             const int64_t row = (int64_t)tm * BM2 + rank * 128 + quarter * 32 + lane;
             mbar_wait(tfull_bar + acc, accphase);
             fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN2);
             EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
-                      (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane, -1, p.qg, 0, nullptr};
+                      (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane, p.splits > 1 ? s : -1,
+                      p.qg, 0, nullptr};
 #pragma unroll 1
-            for (int c = 0; c < BN2 / 32; ++c) {
+            for (int c = 0; c < ((p.dbg & 4) ? 0 : BN2 / 32); ++c) {
                 uint32_t v[32];
                 tmem_ld32(taddr + c * 32, v);
                 const int64_t col0 = (int64_t)tn * BN2 + c * 32;
@@ -436,6 +456,99 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                      "r"(TMEM_COLS));
     }
+}
+
+// Split-K finish: C = sum_s ws[s] in split order (deterministic), then the
+// full epilogue (bias, FP32 C, fused output Q node and its counters) per
+// 32-column chunk, one chunk per thread.
+__global__ void __launch_bounds__(256)
+    splitk_finish_kernel(const float* __restrict__ ws, const Params p) {
+    uint32_t co = 0, cu = 0, cn = 0;
+    const int64_t cpr = (p.N + 31) / 32;  // chunks per row
+    const int64_t nch = p.M * cpr;
+    const int64_t mn = p.M * p.N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nch;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / cpr, col0 = (i - row * cpr) * 32;
+        const float* src = ws + row * p.N + col0;
+        float a[32];
+        if (col0 + 32 <= p.N && (p.N % 4) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(src) + j);
+                a[4 * j] = v.x; a[4 * j + 1] = v.y; a[4 * j + 2] = v.z; a[4 * j + 3] = v.w;
+            }
+            for (int s = 1; s < p.splits; ++s) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(src + s * mn) + j);
+                    a[4 * j] = __fadd_rn(a[4 * j], v.x);
+                    a[4 * j + 1] = __fadd_rn(a[4 * j + 1], v.y);
+                    a[4 * j + 2] = __fadd_rn(a[4 * j + 2], v.z);
+                    a[4 * j + 3] = __fadd_rn(a[4 * j + 3], v.w);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                float v = 0.0f;
+                if (col0 + j < p.N) {
+                    v = src[j];
+                    for (int s = 1; s < p.splits; ++s) v = __fadd_rn(v, src[s * mn + j]);
+                }
+                a[j] = v;
+            }
+        }
+        uint32_t v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(a[j]);
+        epilogue_chunk(p, row, col0, v, co, cu, cn);
+    }
+    if (p.ep.cq_counters) flush_counters<256>(co, cu, cn, p.ep.cq_counters);
+}
+
+// 3-D store map over the split-K workspace [splits][m][n] FP32 (32x32x1 boxes).
+static bool make_ws_map(CUtensorMap* tm, float* ws, int splits, int64_t m, int64_t n) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc || (uintptr_t)ws % 16 || (n * 4) % 16 || m > INT32_MAX || n > INT32_MAX) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)m, (cuuint64_t)splits};
+    cuuint64_t strides[2] = {(cuuint64_t)(n * 4), (cuuint64_t)(m * n * 4)};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ws, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Split-K factor for the 2-SM kernel: minimise (waves of work items) x (K-blocks
+// per item) plus the workspace round trip, over s <= num_kb / 4. Only taken
+// when it beats s = 1 by more than 5 %. FP8B_GEMM_SPLITK=<s> forces a factor
+// (tests), FP8B_GEMM_SPLITK=1 disables splitting.
+static int choose_splits(int tiles, int clusters, int num_kb, int64_t mn, int es) {
+    const char* e = getenv("FP8B_GEMM_SPLITK");
+    if (e && e[0]) {
+        int s = atoi(e);
+        if (s < 1) s = 1;
+        if (s > num_kb) s = num_kb;
+        return s;
+    }
+    const double t_kb = 0.4e-6 * (es == 2 ? 2.0 : 1.0);   // s per 256x256x128B stage (measured)
+    const double bw = 5.0e12;                             // B/s for the workspace round trip
+    auto cost = [&](int s) {
+        const double waves = (double)((tiles * (int64_t)s + clusters - 1) / clusters);
+        const double kbs = (double)((num_kb + s - 1) / s);
+        const double ws = s > 1 ? (double)mn * 4.0 * (2.0 * s + 1.0) / bw : 0.0;
+        return waves * kbs * t_kb + ws;
+    };
+    int best = 1;
+    double bc = cost(1);
+    const int smax = num_kb / 4 < 64 ? num_kb / 4 : 64;
+    for (int s = 2; s <= smax; ++s) {
+        if ((double)s * (double)mn * 4.0 > (double)(1ll << 30)) break;  // workspace <= 1 GiB
+        const double c = cost(s);
+        if (c < bc) { bc = c; best = s; }
+    }
+    return bc < 0.95 * cost(1) ? best : 1;
 }
 
 // ------------------------------------------------------------------ host side
@@ -483,6 +596,11 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
     p.tiles_m = (int)((m + BM - 1) / BM);
     p.tiles_n = (int)((n + BN - 1) / BN);
     p.num_kb = (int)((k + BKE - 1) / BKE);
+    p.splits = 1;
+    {
+        const char* e = getenv("FP8B_GEMM_DBG");
+        p.dbg = e ? atoi(e) : 0;
+    }
     p.ep = ep;
     CUtensorMap tmC;
     memset(&tmC, 0, sizeof(tmC));
@@ -517,8 +635,39 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
             p2.tiles_m = (int)((m + BM2 - 1) / BM2);
             p2.tiles_n = (int)((n + BN2 - 1) / BN2);
             const int ntiles2 = p2.tiles_m * p2.tiles_n;
-            int grid2 = 2 * ntiles2;
             const int maxg = num_sms & ~1;
+            const int splits = use_epi_tma() ? choose_splits(ntiles2, maxg / 2, p.num_kb, m * n, ES) : 1;
+            float* ws = nullptr;
+            CUtensorMap tmW;
+            if (splits > 1) {
+                // FP32 partials of each K range -> workspace; the finish kernel
+                // sums them in split order and runs the real epilogue.
+                if (cudaMallocAsync(&ws, (size_t)splits * m * n * sizeof(float), st) != cudaSuccess)
+                    return FP8B_ECUDA;
+                if (!make_ws_map(&tmW, ws, splits, m, n)) {
+                    cudaFreeAsync(ws, st);
+                    ws = nullptr;
+                }
+            }
+            if (ws) {
+                Params pk = p2;
+                pk.splits = splits;
+                pk.c_tma = 1;
+                pk.q_tma = 0;
+                pk.ep = EpiArgs{ws, nullptr, nullptr, 0, 0, 0, 0, nullptr};
+                int grid2 = 2 * ntiles2 * splits;
+                if (grid2 > maxg) grid2 = maxg;
+                gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, tmW, tmQ, pk);
+                Params pf = p2;
+                pf.splits = splits;
+                const int64_t nch = m * ((n + 31) / 32);
+                int64_t b = (nch + 255) / 256;
+                if (b > 8 * num_sms) b = 8 * num_sms;
+                splitk_finish_kernel<<<(int)b, 256, 0, st>>>(ws, pf);
+                cudaFreeAsync(ws, st);
+                return 2;  // launches
+            }
+            int grid2 = 2 * ntiles2;
             if (grid2 > maxg) grid2 = maxg;
             gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, tmC, tmQ, p2);
             return FP8B_OK;
@@ -539,6 +688,10 @@ int launch_gemm_tc(const void* a, const void* b, int64_t m, int64_t n, int64_t k
         return FP8B_ENOTSUP;
     const int rc = fmt == FP8B_E5M2 ? tc::launch_es<1>(a, b, m, n, k, a_mn, b_mn, ep, st)
                                     : tc::launch_es<2>(a, b, m, n, k, a_mn, b_mn, ep, st);
+    if (rc == 2) {  // split-K: GEMM + finish
+        *nlaunch = 2;
+        return FP8B_OK;
+    }
     if (rc == FP8B_OK) *nlaunch = 1;
     return rc;
 }

@@ -52,6 +52,11 @@ class GpuOps:
         self.engine = engine
         self.device = torch.device("cuda", torch.cuda.current_device())
 
+    def dequantize(self, codes, fmt="fp8"):
+        from . import QuantizedTensor, dequantize, _fmt
+        return dequantize(QuantizedTensor(codes.reshape(-1), [codes.numel()], _fmt(fmt), 0,
+                                          self.counters()))
+
     def counters(self):
         return self._C(self.device)
 
@@ -59,16 +64,20 @@ class GpuOps:
     def ctensor(c):
         return c.t
 
-    def quantize(self, x, fmt="fp8", mode="nearest-even", seed=1, block_offset=0, counters=None):
-        return self._q(x, fmt, mode, seed, block_offset=block_offset, counters=counters).codes
+    def quantize(self, x, fmt="fp8", mode="nearest-even", seed=1, block_offset=0, counters=None,
+                 out=None):
+        return self._q(x, fmt, mode, seed, block_offset=block_offset, counters=counters,
+                       out=out).codes
 
-    def gemm_f32(self, a, b, m, n, k, a_major="k", b_major="n"):
-        c, _ = self._g(a, b, m, n, k, "fp8", a_major=a_major, b_major=b_major, engine=self.engine)
+    def gemm_f32(self, a, b, m, n, k, a_major="k", b_major="n", out=None):
+        c, _ = self._g(a, b, m, n, k, "fp8", a_major=a_major, b_major=b_major, engine=self.engine,
+                       c=None if out is None else out.view(m, n))
         return c
 
-    def gemm_q(self, a, b, m, n, k, a_major="k", b_major="n", counters=None):
+    def gemm_q(self, a, b, m, n, k, a_major="k", b_major="n", counters=None, out=None):
         _, cq = self._g(a, b, m, n, k, "fp8", a_major=a_major, b_major=b_major,
-                        engine=self.engine, want_c=False, out_fmt="fp8", out_counters=counters)
+                        engine=self.engine, want_c=False, out_fmt="fp8", out_counters=counters,
+                        out_codes=out)
         return cq
 
     def update(self, qdw, master, momentum, *, lr, mu, two_lambda, scaler, skip_counters,

@@ -1,0 +1,7 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for d in 0 1 2; do
+FP8B_GEMM_DBG=$d timeout 120 python scripts/gemm_clock.py --shapes 8192x8192x8192 --cublas $((d==0)) --seconds 0.3 > gpurun_out/clock_dbg_$d.log 2>&1; echo "dbg=$d"; cat gpurun_out/clock_dbg_$d.log
+done
+timeout 120 python scripts/splitk_diag.py > gpurun_out/splitk_diag.log 2>&1; cat gpurun_out/splitk_diag.log

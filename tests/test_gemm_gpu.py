@@ -188,3 +188,66 @@ def test_tensor_vs_sequential_large(fp8):
         cg, cr = ct.reshape(-1)[idx].double(), cs.reshape(-1)[idx].double()
         assert bool((((cg - mid) * (cr - mid)) <= 0).all())
     assert nflip <= m * n * 1e-4
+
+
+@pytest.fixture
+def splitk_env():
+    old = os.environ.get("FP8B_GEMM_SPLITK")
+    yield
+    if old is None:
+        os.environ.pop("FP8B_GEMM_SPLITK", None)
+    else:
+        os.environ["FP8B_GEMM_SPLITK"] = old
+
+
+@pytest.mark.parametrize("splits", ["", "3", "7"])
+@pytest.mark.parametrize("out_mode,out_fmt", [("nearest-even", "fp8"), ("truncate", "fp8"),
+                                              ("stochastic", "fp8"), ("nearest-even", "fp16")])
+@pytest.mark.parametrize("a_major", ["k", "m"])
+def test_splitk_exact_grid(fp8, splitk_env, splits, out_mode, out_fmt, a_major):
+    """Split-K (FP32 partials per K range -> fixed-order sum -> bias / C / fused
+    Q node / counters): on a coarse operand grid every partial sum is exact, so
+    C, the codes and the counters must equal the exact result bit for bit, with
+    ragged K ranges (3, 7 splits) and the automatic choice (wgrad-like shape:
+    small M x N, long K)."""
+    import torch
+    os.environ["FP8B_GEMM_SPLITK"] = splits
+    rng = np.random.default_rng(31)
+    m, k, n = 512, 8192, 768
+    A = O.quantize((rng.integers(-4, 5, m * k) * 0.25).astype(np.float32))[0].reshape(m, k)
+    B = O.quantize((rng.integers(-4, 5, k * n) * 0.5).astype(np.float32))[0].reshape(k, n)
+    bias = (rng.integers(-8, 8, n) * 0.125).astype(np.float32)
+    a_st = A if a_major == "k" else A.T.copy()
+    cnt = fp8.Counters()
+    c, cq = fp8.gemm_codes(_codes_dev(a_st, "fp8"), _codes_dev(B, "fp8"), m, n, k, "fp8",
+                           a_major=a_major, engine="tensor", bias=torch.from_numpy(bias).cuda(),
+                           out_fmt=out_fmt, out_mode=out_mode, out_seed=9, out_counters=cnt)
+    da = O.dequantize(A).astype(np.float64).reshape(m, k)
+    db = O.dequantize(B).astype(np.float64).reshape(k, n)
+    y = ((da @ db).astype(np.float32) + bias[None, :]).astype(np.float32)
+    np.testing.assert_array_equal(c.cpu().numpy(), y)
+    codes, k_ = O.quantize(y, out_fmt, out_mode, 9, bits="counter")
+    got = cq.cpu().numpy()
+    got = got.view(np.uint16) if out_fmt == "fp16" else got
+    np.testing.assert_array_equal(got, codes.astype(got.dtype))
+    assert cnt.values() == tuple(int(v) for v in k_)
+
+
+@pytest.mark.parametrize("splits", ["", "5"])
+def test_splitk_tolerance_long_k(fp8, splitk_env, splits):
+    """Config-5 wgrad shape class (dW[512 x 1024] over 65536 tokens): split-K
+    result within tau of the exact sum."""
+    import torch
+    os.environ["FP8B_GEMM_SPLITK"] = splits
+    m, k, n = 512, 65536, 1024
+    x = torch.empty(m * k + k * n, dtype=torch.float32, device="cuda")
+    fp8.fill_synthetic(x, "normal", 41, 1.0)
+    qa = fp8.quantize(x[: m * k])
+    qb = fp8.quantize(x[m * k:])
+    # A stored [K, M] (MN-major): X^T of a [tokens, features] activation
+    c, _ = fp8.gemm_codes(qa.codes, qb.codes, m, n, k, "fp8", a_major="m", engine="tensor")
+    da = fp8.dequantize(qa).double().reshape(k, m).t()
+    db = fp8.dequantize(qb).double().reshape(k, n)
+    ex = da @ db
+    absdot = da.abs() @ db.abs()
+    assert bool(((c.double() - ex).abs() <= TAU * absdot + 1e-30).all())

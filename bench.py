@@ -210,6 +210,8 @@ def run_ours(args):
         result["gemm"] = bench_gemm(F, args, bf16_peak)
         result["dense_step"] = bench_dense_step(F, args)
         result["conv"] = bench_conv(F, args)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(x, args)
     if not args.no_extras:
         # collective workloads: every rank takes part
         del x, c8a, c8b, c16
@@ -217,8 +219,6 @@ def run_ours(args):
         result["gemm_sharded"] = bench_gemm_sharded(F, args, world, rank, dist)
         if args.tf_steps > 0:
             result["transformer"] = bench_transformer(F, args, world, rank, dist)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(x, args)
     if dist:
         dist.destroy_process_group()
     if rank == 0:

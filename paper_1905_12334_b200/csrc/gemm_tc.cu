@@ -48,7 +48,13 @@ struct Params {
     int c_tma;  // FP32 C goes out through the TMA-store epilogue
     int q_tma;  // or the fused output codes (when no FP32 C is written)
     int qg;     // code chunks per TMA store
-    int dbg;    // 2-SM kernel diagnostics (FP8B_GEMM_DBG bits): 1 = no MMAs, 2 = no operand loads, 4 = no epilogue
+    int stages; // 2-SM kernel: smem ring depth in use (FP8B_GEMM_STAGES, <= STAGES2)
+    int dbg;    // 2-SM kernel diagnostics (FP8B_GEMM_DBG bits): 1 = no MMAs, 2 = no operand loads, 4 = no epilogue,
+                // 8 = free-running MMAs (no stage barriers; with 2|4 only),
+                // 16 / 32 = busy-poll the full / empty barriers, 64 = EVICT_LAST operand
+                // loads (ES=1, 128-wide boxes), 128 = one tfull poller per CTA,
+                // 256 = A operand declared E4M3 (timing only), 512 = NB=2 without the
+                // split (lo/hi) accumulator release
     int splits; // 2-SM kernel: split-K factor (>1: FP32 partials into the 3-D workspace map tmC)
     EpiArgs ep;
 };
@@ -224,12 +230,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // leader's barrier; commits multicast to both CTAs' empty / tmem-full
 // barriers; both CTAs' epilogue warps release the leader's tmem-empty barrier.
 constexpr int BM2 = 256;
-constexpr int BN2 = 256;
-constexpr int STAGES2 = 6;
+constexpr int BN2 = 256;      // N per MMA instruction
 constexpr uint32_t A2_BYTES = 128 * BKB;  // per CTA
-constexpr uint32_t B2_BYTES = 128 * BKB;  // per CTA
-constexpr uint32_t STAGE2_BYTES = A2_BYTES + B2_BYTES;
-constexpr uint32_t SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 512;
+// NB = N=256 MMAs per pair tile: 1 -> 256x256 tile, 6-stage ring, TMEM double
+// buffered (epilogue overlaps the next tile); 2 -> 256x512 tile whose two MMAs
+// share A through the collector buffer (A read from smem once), 4-stage ring,
+// one 512-column accumulator: 25 % less L2->smem traffic and half the stage
+// barriers per FLOP, at the price of an epilogue that does not overlap.
+template <int NB>
+struct Geo2 {
+    static constexpr int STAGES = NB == 1 ? 6 : 4;
+    static constexpr int NACC = NB == 1 ? 2 : 1;
+    static constexpr int TN = NB * BN2;
+    static constexpr uint32_t B_BYTES = NB * 128 * BKB;  // per CTA
+    static constexpr uint32_t STAGE = A2_BYTES + B_BYTES;
+    static constexpr uint32_t SMEM = STAGES * STAGE + EPI_STAGE_BYTES + 1024 + 512;
+};
+constexpr int STAGES2 = Geo2<1>::STAGES;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -244,6 +261,14 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
 }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm_hint(const CUtensorMap* tm, void* dst, uint32_t bar_leader,
+                                                     int32_t c0, int32_t c1, uint64_t hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_leader), "r"(c0), "r"(c1), "l"(hint)
+        : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* tm, void* dst, uint32_t bar_leader,
                                                 int32_t c0, int32_t c1) {
@@ -268,6 +293,36 @@ __device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t ad, uint64_t bd, 
             "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
     }
 }
+// CU: 0 = none, 1 = collector::a::fill, 2 = collector::a::lastuse
+template <int ES, int CU>
+__device__ __forceinline__ void mma2c(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                      uint32_t accum) {
+    if (CU == 0) {
+        mma2<ES>(tmem_d, ad, bd, idesc, accum);
+    } else if (ES == 1) {
+        if (CU == 1)
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::f8f6f4.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+        else
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::f8f6f4.collector::a::lastuse [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+    } else {
+        if (CU == 1)
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+        else
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+    }
+}
 __device__ __forceinline__ void umma_commit_mc(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -279,7 +334,7 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
 
-template <int ES>
+template <int ES, int NB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
@@ -287,9 +342,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES + EPI_STAGE_BYTES);
-    uint64_t* empty_bar = full_bar + STAGES2;
-    uint64_t* tfull_bar = empty_bar + STAGES2;
+    using G = Geo2<NB>;
+    constexpr uint32_t STAGE2_BYTES = G::STAGE;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::STAGES * STAGE2_BYTES + EPI_STAGE_BYTES);
+    uint64_t* empty_bar = full_bar + G::STAGES;
+    uint64_t* tfull_bar = empty_bar + G::STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
@@ -298,6 +355,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     constexpr int BKE = BKB / ES, UK = 32 / ES, MN_CHUNK = 128 / ES;
     const int ntiles = p.tiles_m * p.tiles_n;  // 256x256 tiles
     const int nitems = ntiles * p.splits;      // (tile, K-split) work items
+    const int nst2 = NB == 1 ? p.stages : G::STAGES;  // ring depth in use
     const int cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
     (void)ntiles;
     auto item_of = [&](int item, int& tm, int& tn, int& s, int& kb0, int& kb1) {
@@ -311,7 +369,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-        for (int s = 0; s < STAGES2; ++s) {
+        for (int s = 0; s < G::STAGES; ++s) {
             mbar_init(full_bar + s, 1);
             mbar_init(empty_bar + s, 1);
         }
@@ -334,25 +392,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
     uint32_t co = 0, cu = 0, cn = 0;
     if (warp == 0) {
-        if (lane == 0) {
+        if (lane == 0 && !(p.dbg & 8)) {
             int stage = 0;
             uint32_t phase = 0;
             for (int item = cluster_id; item < nitems; item += nclusters) {
                 int tm, tn, s, kb0, kb1;
                 item_of(item, tm, tn, s, kb0, kb1);
-                const int32_t m0 = tm * BM2 + (int32_t)rank * 128, n0 = tn * BN2 + (int32_t)rank * 128;
+                const int32_t m0 = tm * BM2 + (int32_t)rank * 128, n0 = tn * G::TN + (int32_t)rank * 128;
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(empty_bar + stage, phase ^ 1);
+                    if (p.dbg & 32) mbar_wait_spin(empty_bar + stage, phase ^ 1);
+                    else mbar_wait(empty_bar + stage, phase ^ 1);
                     const uint32_t fb = mapa_u32(smem_u32(full_bar + stage), 0);
                     if (p.dbg & 2) {
                         if (rank == 0) mbar_expect_tx(full_bar + stage, 0);
-                        if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                        if (++stage == nst2) { stage = 0; phase ^= 1; }
                         continue;
                     }
                     if (rank == 0) mbar_expect_tx(full_bar + stage, 2 * STAGE2_BYTES);
                     uint8_t* sA = smem + stage * STAGE2_BYTES;
                     uint8_t* sB = sA + A2_BYTES;
                     const int32_t k0 = kb * BKE;
+                    if (NB == 1 && (p.dbg & 64)) {
+                        // operands are re-read by other tiles: keep them in L2
+                        const uint64_t hint = 0x14F0000000000000ull;  // EVICT_LAST
+                        if (!p.a_mn) tma_load_2d_2sm_hint(&tmA, sA, fb, k0, m0, hint);
+                        else tma_load_2d_2sm_hint(&tmA, sA, fb, m0, k0, hint);
+                        if (!p.b_mn) tma_load_2d_2sm_hint(&tmB, sB, fb, k0, n0, hint);
+                        else tma_load_2d_2sm_hint(&tmB, sB, fb, n0, k0, hint);
+                        if (++stage == nst2) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     if (!p.a_mn) {
                         tma_load_2d_2sm(&tmA, sA, fb, k0, m0);
                     } else {
@@ -360,14 +429,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         for (int j = 0; j < 128 / MN_CHUNK; ++j)
                             tma_load_2d_2sm(&tmA, sA + j * (BKE * 128), fb, m0 + j * MN_CHUNK, k0);
                     }
-                    if (!p.b_mn) {
-                        tma_load_2d_2sm(&tmB, sB, fb, k0, n0);
-                    } else {
 #pragma unroll
-                        for (int j = 0; j < 128 / MN_CHUNK; ++j)
-                            tma_load_2d_2sm(&tmB, sB + j * (BKE * 128), fb, n0 + j * MN_CHUNK, k0);
+                    for (int h = 0; h < NB; ++h) {  // B rows of MMA h: n0 + 256 h (this CTA's 128)
+                        uint8_t* sBh = sB + h * (128 * BKB);
+                        if (!p.b_mn) {
+                            tma_load_2d_2sm(&tmB, sBh, fb, k0, n0 + h * BN2);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 128 / MN_CHUNK; ++j)
+                                tma_load_2d_2sm(&tmB, sBh + j * (BKE * 128), fb,
+                                                n0 + h * BN2 + j * MN_CHUNK, k0);
+                        }
                     }
-                    if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                    if (++stage == nst2) { stage = 0; phase ^= 1; }
                 }
             }
         }
@@ -375,6 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0 && rank == 0) {
             uint32_t idesc = (1u << 4);
             if (ES == 1) idesc |= (1u << 7) | (1u << 10);
+            if (ES == 1 && (p.dbg & 256)) idesc &= ~(7u << 7);  // diagnostic: A read as E4M3
             idesc |= (uint32_t)p.a_mn << 15;
             idesc |= (uint32_t)p.b_mn << 16;
             idesc |= (uint32_t)(BN2 >> 3) << 17;
@@ -383,14 +458,92 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t accphase = 0;
+            // NB == 2: the epilogue frees the accumulator in two halves (lo =
+            // columns 0-255, hi = 256-511). The next tile starts as soon as lo
+            // is free, issuing lo MMAs only and keeping those stages resident
+            // until hi is free too; then their hi MMAs go out and the stages
+            // are released. This hides the hi half of the drain.
+            auto issue_half = [&](uint32_t a_base, uint32_t b_base, uint32_t d, int kb, int kb0_) {
+#pragma unroll
+                for (int k = 0; k < BKB / 32; ++k) {
+                    uint64_t ad, bd;
+                    if (!p.a_mn) ad = umma_desc(a_base + 32 * k, 16, 1024);
+                    else ad = umma_desc(a_base + k * UK * 128, BKE * 128, 1024);
+                    if (!p.b_mn) bd = umma_desc(b_base + 32 * k, 16, 1024);
+                    else bd = umma_desc(b_base + k * UK * 128, BKE * 128, 1024);
+                    mma2<ES>(d, ad, bd, idesc, (kb != kb0_ || k != 0) ? 1u : 0u);
+                }
+            };
             for (int item = cluster_id; item < nitems; item += nclusters) {
                 int tm, tn, s, kb0, kb1;
                 item_of(item, tm, tn, s, kb0, kb1);
                 mbar_wait(tempty_bar + acc, accphase ^ 1);
                 fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
+                if (NB == 2 && !(p.dbg & 512)) {
+                    bool hi_free = false;
+                    int npend = 0, pend_stage = 0, pend_kb = 0;
+                    auto flush = [&]() {
+                        int st = pend_stage;
+                        for (int j = 0; j < npend; ++j) {
+                            const uint32_t a_base = smem_u32(smem + st * STAGE2_BYTES);
+                            issue_half(a_base, a_base + A2_BYTES + 128 * BKB, d_tmem + BN2,
+                                       pend_kb + j, kb0);
+                            umma_commit_mc(empty_bar + st);
+                            if (++st == nst2) st = 0;
+                        }
+                        npend = 0;
+                    };
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(full_bar + stage, phase);
+                        fence_after();
+                        if (!hi_free && mbar_test(tempty_bar + 1, accphase ^ 1)) {
+                            hi_free = true;
+                            fence_after();
+                            flush();
+                        }
+                        const uint32_t a_base = smem_u32(smem + stage * STAGE2_BYTES);
+                        const uint32_t b_base = a_base + A2_BYTES;
+                        if (hi_free) {
+#pragma unroll
+                            for (int k = 0; k < BKB / 32; ++k) {
+                                uint64_t ad, bd;
+                                if (!p.a_mn) ad = umma_desc(a_base + 32 * k, 16, 1024);
+                                else ad = umma_desc(a_base + k * UK * 128, BKE * 128, 1024);
+                                const uint32_t acc_on = (kb != kb0 || k != 0) ? 1u : 0u;
+                                if (!p.b_mn) bd = umma_desc(b_base + 32 * k, 16, 1024);
+                                else bd = umma_desc(b_base + k * UK * 128, BKE * 128, 1024);
+                                mma2c<ES, 1>(d_tmem, ad, bd, idesc, acc_on);
+                                const uint32_t b2 = b_base + 128 * BKB;
+                                if (!p.b_mn) bd = umma_desc(b2 + 32 * k, 16, 1024);
+                                else bd = umma_desc(b2 + k * UK * 128, BKE * 128, 1024);
+                                mma2c<ES, 2>(d_tmem + BN2, ad, bd, idesc, acc_on);
+                            }
+                            umma_commit_mc(empty_bar + stage);
+                        } else {
+                            issue_half(a_base, b_base, d_tmem, kb, kb0);
+                            if (npend++ == 0) { pend_stage = stage; pend_kb = kb; }
+                            if (npend == nst2) {  // every ring slot waits on hi
+                                mbar_wait(tempty_bar + 1, accphase ^ 1);
+                                hi_free = true;
+                                fence_after();
+                                flush();
+                            }
+                        }
+                        if (++stage == nst2) { stage = 0; phase ^= 1; }
+                    }
+                    if (npend) {
+                        mbar_wait(tempty_bar + 1, accphase ^ 1);
+                        fence_after();
+                        flush();
+                    }
+                    umma_commit_mc(tfull_bar + acc);
+                    accphase ^= 1;
+                    continue;
+                }
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(full_bar + stage, phase);
+                    if (p.dbg & 16) mbar_wait_spin(full_bar + stage, phase);
+                    else if (!(p.dbg & 8)) mbar_wait(full_bar + stage, phase);
                     fence_after();
                     const uint32_t a_base = smem_u32(smem + stage * STAGE2_BYTES);
                     const uint32_t b_base = a_base + A2_BYTES;
@@ -400,20 +553,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         uint64_t ad, bd;
                         if (!p.a_mn) ad = umma_desc(a_base + 32 * k, 16, 1024);
                         else ad = umma_desc(a_base + k * UK * 128, BKE * 128, 1024);
+                        const uint32_t acc_on = (kb != kb0 || k != 0) ? 1u : 0u;
                         if (!p.b_mn) bd = umma_desc(b_base + 32 * k, 16, 1024);
                         else bd = umma_desc(b_base + k * UK * 128, BKE * 128, 1024);
-                        mma2<ES>(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                        if (NB == 1) {
+                            mma2<ES>(d_tmem, ad, bd, idesc, acc_on);
+                        } else {
+                            // same A for both halves of N: load it into the collector once
+                            mma2c<ES, 1>(d_tmem, ad, bd, idesc, acc_on);
+                            const uint32_t b2 = b_base + 128 * BKB;
+                            if (!p.b_mn) bd = umma_desc(b2 + 32 * k, 16, 1024);
+                            else bd = umma_desc(b2 + k * UK * 128, BKE * 128, 1024);
+                            mma2c<ES, 2>(d_tmem + BN2, ad, bd, idesc, acc_on);
+                        }
                     }
-                    umma_commit_mc(empty_bar + stage);
-                    if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                    if (!(p.dbg & 8)) umma_commit_mc(empty_bar + stage);
+                    if (++stage == nst2) { stage = 0; phase ^= 1; }
                 }
                 umma_commit_mc(tfull_bar + acc);
-                if (++acc == 2) { acc = 0; accphase ^= 1; }
+                if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
             }
         }
     } else {
         const int quarter = warp & 3;
-        uint8_t* sbuf = smem + STAGES2 * STAGE2_BYTES + quarter * 8192;
+        uint8_t* sbuf = smem + G::STAGES * STAGE2_BYTES + quarter * 8192;
         uint32_t nst = 0;
         int acc = 0;
         uint32_t accphase = 0;
@@ -422,29 +585,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             int tm, tn, s, kb0, kb1;
             item_of(item, tm, tn, s, kb0, kb1);
             const int64_t row = (int64_t)tm * BM2 + rank * 128 + quarter * 32 + lane;
-            mbar_wait(tfull_bar + acc, accphase);
+            if (p.dbg & 128) {
+                // one poller, the other epilogue warps park on a named barrier
+                if (warp == 2 && lane == 0) mbar_wait(tfull_bar + acc, accphase);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            } else {
+                mbar_wait(tfull_bar + acc, accphase);
+            }
             fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN2);
             EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
                       (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane, p.splits > 1 ? s : -1,
                       p.qg, 0, nullptr};
 #pragma unroll 1
-            for (int c = 0; c < ((p.dbg & 4) ? 0 : BN2 / 32); ++c) {
-                uint32_t v[32];
-                tmem_ld32(taddr + c * 32, v);
-                const int64_t col0 = (int64_t)tn * BN2 + c * 32;
-                if (col0 >= p.N) continue;
-                if (p.c_tma || p.q_tma) {
-                    const bool last = c == BN2 / 32 - 1 || col0 + 32 >= p.N;
-                    epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
-                } else if (row < p.M) {
-                    epilogue_chunk(p, row, col0, v, co, cu, cn);
+            for (int c = 0; c < ((p.dbg & 4) ? 0 : G::TN / 32); ++c) {
+                const int64_t col0 = (int64_t)tn * G::TN + c * 32;
+                if (col0 < p.N) {
+                    uint32_t v[32];
+                    tmem_ld32(taddr + c * 32, v);
+                    if (p.c_tma || p.q_tma) {
+                        const bool last = c == G::TN / 32 - 1 || col0 + 32 >= p.N;
+                        epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
+                    } else if (row < p.M) {
+                        epilogue_chunk(p, row, col0, v, co, cu, cn);
+                    }
                 }
+                if (NB == 2 && c == BN2 / 32 - 1 && !(p.dbg & 512)) {
+                    fence_before();  // lo half read out: the next tile may start
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(te_leader);
+                }
+            }
+            if (NB == 2 && (p.dbg & 4) && !(p.dbg & 512)) {
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(te_leader);
             }
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
-            if (++acc == 2) { acc = 0; accphase ^= 1; }
+            if (lane == 0) mbar_arrive_cluster(te_leader + (NB == 2 && !(p.dbg & 512) ? 8 : acc * 8));
+            if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
         }
     }
     if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
@@ -524,7 +704,7 @@ static bool make_ws_map(CUtensorMap* tm, float* ws, int splits, int64_t m, int64
 // per item) plus the workspace round trip, over s <= num_kb / 4. Only taken
 // when it beats s = 1 by more than 5 %. FP8B_GEMM_SPLITK=<s> forces a factor
 // (tests), FP8B_GEMM_SPLITK=1 disables splitting.
-static int choose_splits(int tiles, int clusters, int num_kb, int64_t mn, int es) {
+static int choose_splits(int tiles, int clusters, int num_kb, int64_t mn, int es, int nb = 1) {
     const char* e = getenv("FP8B_GEMM_SPLITK");
     if (e && e[0]) {
         int s = atoi(e);
@@ -532,7 +712,7 @@ static int choose_splits(int tiles, int clusters, int num_kb, int64_t mn, int es
         if (s > num_kb) s = num_kb;
         return s;
     }
-    const double t_kb = 0.4e-6 * (es == 2 ? 2.0 : 1.0);   // s per 256x256x128B stage (measured)
+    const double t_kb = 0.4e-6 * (es == 2 ? 2.0 : 1.0) * nb;  // s per 256x(256 nb)x128B stage
     const double bw = 5.0e12;                             // B/s for the workspace round trip
     auto cost = [&](int s) {
         const double waves = (double)((tiles * (int64_t)s + clusters - 1) / clusters);
@@ -572,6 +752,73 @@ static bool use_epi_tma() {
     return v == 1;
 }
 
+// Pair-tile width for the 2-SM kernel: FP8B_GEMM_NB=1|2 forces it; otherwise
+// the 256x512 tile (NB=2) when N allows it and it does not cost waves.
+static int pick_nb(int64_t m, int64_t n, int num_kb, int clusters) {
+    const char* e = getenv("FP8B_GEMM_NB");
+    if (e && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
+    (void)num_kb;
+    // waves x tile time; the 256x512 tile does a 256x256 tile's work ~12 %
+    // faster (measured at 8192^3: 0.370 vs 0.415 ms)
+    const int64_t tm = (m + BM2 - 1) / BM2;
+    const int64_t t1 = tm * ((n + 255) / 256), t2 = tm * ((n + 511) / 512);
+    const double c1 = (double)((t1 + clusters - 1) / clusters);
+    const double c2 = (double)((t2 + clusters - 1) / clusters) * 2.0 * 0.89;
+    return c2 < c1 ? 2 : 1;
+}
+
+template <int ES, int NB>
+static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUtensorMap& tmC,
+                      const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int num_sms,
+                      cudaStream_t st) {
+    using G = Geo2<NB>;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             G::SMEM);
+    });
+    Params p2 = p;
+    p2.tiles_m = (int)((m + BM2 - 1) / BM2);
+    p2.tiles_n = (int)((n + G::TN - 1) / G::TN);
+    const int ntiles2 = p2.tiles_m * p2.tiles_n;
+    const int maxg = num_sms & ~1;
+    const int splits = use_epi_tma() ? choose_splits(ntiles2, maxg / 2, p.num_kb, m * n, ES, NB) : 1;
+    float* ws = nullptr;
+    CUtensorMap tmW;
+    if (splits > 1) {
+        // FP32 partials of each K range -> workspace; the finish kernel sums
+        // them in split order and runs the real epilogue.
+        if (cudaMallocAsync(&ws, (size_t)splits * m * n * sizeof(float), st) != cudaSuccess)
+            return FP8B_ECUDA;
+        if (!make_ws_map(&tmW, ws, splits, m, n)) {
+            cudaFreeAsync(ws, st);
+            ws = nullptr;
+        }
+    }
+    if (ws) {
+        Params pk = p2;
+        pk.splits = splits;
+        pk.c_tma = 1;
+        pk.q_tma = 0;
+        pk.ep = EpiArgs{ws, nullptr, nullptr, 0, 0, 0, 0, nullptr};
+        int grid2 = 2 * ntiles2 * splits;
+        if (grid2 > maxg) grid2 = maxg;
+        gemm_tc2_kernel<ES, NB><<<grid2, NUM_THREADS, G::SMEM, st>>>(tA2, tB2, tmW, tmQ, pk);
+        Params pf = p2;
+        pf.splits = splits;
+        const int64_t nch = m * ((n + 31) / 32);
+        int64_t b = (nch + 255) / 256;
+        if (b > 8 * num_sms) b = 8 * num_sms;
+        splitk_finish_kernel<<<(int)b, 256, 0, st>>>(ws, pf);
+        cudaFreeAsync(ws, st);
+        return 2;  // launches
+    }
+    int grid2 = 2 * ntiles2;
+    if (grid2 > maxg) grid2 = maxg;
+    gemm_tc2_kernel<ES, NB><<<grid2, NUM_THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tmQ, p2);
+    return FP8B_OK;
+}
+
 template <int ES>
 static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t k, int a_mn,
                      int b_mn, const EpiArgs& ep, cudaStream_t st) {
@@ -600,6 +847,9 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
     {
         const char* e = getenv("FP8B_GEMM_DBG");
         p.dbg = e ? atoi(e) : 0;
+        const char* st_ = getenv("FP8B_GEMM_STAGES");
+        p.stages = st_ ? atoi(st_) : STAGES2;
+        if (p.stages < 2 || p.stages > STAGES2) p.stages = STAGES2;
     }
     p.ep = ep;
     CUtensorMap tmC;
@@ -617,8 +867,6 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
-        cudaFuncSetAttribute(gemm_tc2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
     });
     if (use_2sm() && m >= BM2) {
         // 2-SM path: tmA box is 128 rows of the pair's 256 (each CTA loads its half)
@@ -631,46 +879,9 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
             else ok2 = make_map(&tB2, b, ES, (uint64_t)n, (uint64_t)k, MN_CHUNK, BKE);
         }
         if (ok2) {
-            Params p2 = p;
-            p2.tiles_m = (int)((m + BM2 - 1) / BM2);
-            p2.tiles_n = (int)((n + BN2 - 1) / BN2);
-            const int ntiles2 = p2.tiles_m * p2.tiles_n;
-            const int maxg = num_sms & ~1;
-            const int splits = use_epi_tma() ? choose_splits(ntiles2, maxg / 2, p.num_kb, m * n, ES) : 1;
-            float* ws = nullptr;
-            CUtensorMap tmW;
-            if (splits > 1) {
-                // FP32 partials of each K range -> workspace; the finish kernel
-                // sums them in split order and runs the real epilogue.
-                if (cudaMallocAsync(&ws, (size_t)splits * m * n * sizeof(float), st) != cudaSuccess)
-                    return FP8B_ECUDA;
-                if (!make_ws_map(&tmW, ws, splits, m, n)) {
-                    cudaFreeAsync(ws, st);
-                    ws = nullptr;
-                }
-            }
-            if (ws) {
-                Params pk = p2;
-                pk.splits = splits;
-                pk.c_tma = 1;
-                pk.q_tma = 0;
-                pk.ep = EpiArgs{ws, nullptr, nullptr, 0, 0, 0, 0, nullptr};
-                int grid2 = 2 * ntiles2 * splits;
-                if (grid2 > maxg) grid2 = maxg;
-                gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, tmW, tmQ, pk);
-                Params pf = p2;
-                pf.splits = splits;
-                const int64_t nch = m * ((n + 31) / 32);
-                int64_t b = (nch + 255) / 256;
-                if (b > 8 * num_sms) b = 8 * num_sms;
-                splitk_finish_kernel<<<(int)b, 256, 0, st>>>(ws, pf);
-                cudaFreeAsync(ws, st);
-                return 2;  // launches
-            }
-            int grid2 = 2 * ntiles2;
-            if (grid2 > maxg) grid2 = maxg;
-            gemm_tc2_kernel<ES><<<grid2, NUM_THREADS, SMEM2_BYTES, st>>>(tA2, tB2, tmC, tmQ, p2);
-            return FP8B_OK;
+            const int nb = pick_nb(m, n, p.num_kb, num_sms / 2);
+            return nb == 2 ? launch_2sm<ES, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st)
+                           : launch_2sm<ES, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
         }
     }
     const int ntiles = p.tiles_m * p.tiles_n;

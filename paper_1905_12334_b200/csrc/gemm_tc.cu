@@ -237,14 +237,20 @@ constexpr uint32_t A2_BYTES = 128 * BKB;  // per CTA
 // share A through the collector buffer (A read from smem once), 4-stage ring,
 // one 512-column accumulator: 25 % less L2->smem traffic and half the stage
 // barriers per FLOP, at the price of an epilogue that does not overlap.
-template <int NB>
+// EW epilogue warps (4, or 8 = two per TMEM lane quarter splitting each
+// 256-column block), NBUF 4 KB staging buffers per epilogue warp; the ring
+// takes what shared memory is left (at most 6 stages).
+template <int NB, int EW = 4, int NBUF = 2>
 struct Geo2 {
-    static constexpr int STAGES = NB == 1 ? 6 : 4;
     static constexpr int NACC = NB == 1 ? 2 : 1;
     static constexpr int TN = NB * BN2;
     static constexpr uint32_t B_BYTES = NB * 128 * BKB;  // per CTA
     static constexpr uint32_t STAGE = A2_BYTES + B_BYTES;
-    static constexpr uint32_t SMEM = STAGES * STAGE + EPI_STAGE_BYTES + 1024 + 512;
+    static constexpr uint32_t EPI = (uint32_t)EW * NBUF * 4096;
+    static constexpr int FIT = (int)((232448u - EPI - 1536u) / STAGE);
+    static constexpr int STAGES = FIT < 6 ? FIT : 6;
+    static constexpr int THREADS = 64 + 32 * EW;
+    static constexpr uint32_t SMEM = STAGES * STAGE + EPI + 1024 + 512;
 };
 constexpr int STAGES2 = Geo2<1>::STAGES;
 
@@ -334,17 +340,17 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
 
-template <int ES, int NB>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+template <int ES, int NB, int EW, int NBUF>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
                    const Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    using G = Geo2<NB>;
+    using G = Geo2<NB, EW, NBUF>;
     constexpr uint32_t STAGE2_BYTES = G::STAGE;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::STAGES * STAGE2_BYTES + EPI_STAGE_BYTES);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::STAGES * STAGE2_BYTES + G::EPI);
     uint64_t* empty_bar = full_bar + G::STAGES;
     uint64_t* tfull_bar = empty_bar + G::STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -375,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar + a, 1);
-            mbar_init(tempty_bar + a, 8);  // 4 epilogue warps x 2 CTAs
+            mbar_init(tempty_bar + a, 2 * EW);  // EW epilogue warps x 2 CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -575,8 +581,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
         }
     } else {
-        const int quarter = warp & 3;
-        uint8_t* sbuf = smem + G::STAGES * STAGE2_BYTES + quarter * 8192;
+        const int quarter = warp & 3;            // TMEM lane quarter this warp may read
+        const int ehalf = (warp - 2) >> 2;       // EW = 8: which half of each 256-column block
+        constexpr int PERB = 8 / (EW / 4);       // chunks per 256-column block per warp
+        uint8_t* sbuf = smem + G::STAGES * STAGE2_BYTES + (warp - 2) * (NBUF * 4096);
         uint32_t nst = 0;
         int acc = 0;
         uint32_t accphase = 0;
@@ -596,21 +604,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN2);
             EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
                       (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane, p.splits > 1 ? s : -1,
-                      p.qg, 0, nullptr};
+                      p.qg, 0, nullptr, NBUF};
 #pragma unroll 1
-            for (int c = 0; c < ((p.dbg & 4) ? 0 : G::TN / 32); ++c) {
-                const int64_t col0 = (int64_t)tn * G::TN + c * 32;
-                if (col0 < p.N) {
-                    uint32_t v[32];
-                    tmem_ld32(taddr + c * 32, v);
-                    if (p.c_tma || p.q_tma) {
-                        const bool last = c == G::TN / 32 - 1 || col0 + 32 >= p.N;
-                        epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
-                    } else if (row < p.M) {
-                        epilogue_chunk(p, row, col0, v, co, cu, cn);
+            for (int b = 0; b < ((p.dbg & 4) ? 0 : NB); ++b) {
+#pragma unroll 1
+                for (int j = 0; j < PERB; ++j) {
+                    const int c = b * 8 + ehalf * PERB + j;
+                    const int64_t col0 = (int64_t)tn * G::TN + c * 32;
+                    if (col0 < p.N) {
+                        uint32_t v[32];
+                        tmem_ld32(taddr + c * 32, v);
+                        if (p.c_tma || p.q_tma) {
+                            const bool last = j == PERB - 1 || col0 + 32 >= p.N;
+                            epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
+                        } else if (row < p.M) {
+                            epilogue_chunk(p, row, col0, v, co, cu, cn);
+                        }
                     }
                 }
-                if (NB == 2 && c == BN2 / 32 - 1 && !(p.dbg & 512)) {
+                if (NB == 2 && b == 0 && !(p.dbg & 512)) {
                     fence_before();  // lo half read out: the next tile may start
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(te_leader);
@@ -628,7 +640,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
     }
     if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
-    if (p.ep.cq_counters) flush_counters<NUM_THREADS>(co, cu, cn, p.ep.cq_counters);
+    if (p.ep.cq_counters) flush_counters<G::THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     cluster_sync_all();
     if (warp == 1) {
@@ -767,15 +779,15 @@ static int pick_nb(int64_t m, int64_t n, int num_kb, int clusters) {
     return c2 < c1 ? 2 : 1;
 }
 
-template <int ES, int NB>
+template <int ES, int NB, int EW = 4, int NBUF = 2>
 static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUtensorMap& tmC,
                       const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int num_sms,
                       cudaStream_t st) {
-    using G = Geo2<NB>;
+    using G = Geo2<NB, EW, NBUF>;
     static std::once_flag once;
     std::call_once(once, [] {
-        cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             G::SMEM);
+        cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     });
     Params p2 = p;
     p2.tiles_m = (int)((m + BM2 - 1) / BM2);
@@ -803,7 +815,7 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
         pk.ep = EpiArgs{ws, nullptr, nullptr, 0, 0, 0, 0, nullptr};
         int grid2 = 2 * ntiles2 * splits;
         if (grid2 > maxg) grid2 = maxg;
-        gemm_tc2_kernel<ES, NB><<<grid2, NUM_THREADS, G::SMEM, st>>>(tA2, tB2, tmW, tmQ, pk);
+        gemm_tc2_kernel<ES, NB, EW, NBUF><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmW, tmQ, pk);
         Params pf = p2;
         pf.splits = splits;
         const int64_t nch = m * ((n + 31) / 32);
@@ -815,7 +827,7 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
     }
     int grid2 = 2 * ntiles2;
     if (grid2 > maxg) grid2 = maxg;
-    gemm_tc2_kernel<ES, NB><<<grid2, NUM_THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tmQ, p2);
+    gemm_tc2_kernel<ES, NB, EW, NBUF><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tmQ, p2);
     return FP8B_OK;
 }
 
@@ -880,8 +892,13 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
         }
         if (ok2) {
             const int nb = pick_nb(m, n, p.num_kb, num_sms / 2);
-            return nb == 2 ? launch_2sm<ES, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st)
-                           : launch_2sm<ES, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+            if (nb == 1) return launch_2sm<ES, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+            const char* ev = getenv("FP8B_GEMM_EPI");   // NB=2 epilogue: 4x2 (default), 8x1, 8x2
+            if (ev && ev[0] == '8' && ev[2] == '1')
+                return launch_2sm<ES, 2, 8, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+            if (ev && ev[0] == '8' && ev[2] == '2')
+                return launch_2sm<ES, 2, 8, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+            return launch_2sm<ES, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
         }
     }
     const int ntiles = p.tiles_m * p.tiles_n;

@@ -170,17 +170,27 @@ struct EpiTma {
     int qg;                // code chunks per store (row span = qg * 32 * code bytes)
     int qpos;              // chunks already staged in the open code group
     uint8_t* qbuf;         // the open code group's buffer
+    int nbuf = 2;          // staging buffers of this warp (2: ring of 4 KB buffers; 1: one)
 };
 
 __device__ __forceinline__ void bulk_wait_read1() {
     asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Next ring buffer, once its previous store has read it.
-__device__ __forceinline__ uint8_t* stage_acquire(uint8_t* sbuf, uint32_t& nst, int lane) {
+__device__ __forceinline__ uint8_t* stage_acquire(uint8_t* sbuf, uint32_t& nst, int lane,
+                                                  int nbuf = 2) {
+    if (nbuf == 1) {
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        return sbuf;
+    }
     uint8_t* buf = sbuf + (nst++ & 1) * 4096;
     if (lane == 0) bulk_wait_read1();
     __syncwarp();
@@ -224,8 +234,8 @@ __device__ __forceinline__ void stage_flush(const CUtensorMap* tm, uint8_t* buf,
 // One 32-row x 128-byte box (32 FP32 columns) per call.
 __device__ __forceinline__ void stage_store_f32(const CUtensorMap* tm, uint8_t* sbuf, uint32_t& nst,
                                                 const uint32_t* w, int lane, int32_t col0,
-                                                int32_t row0, int32_t z = -1) {
-    uint8_t* buf = stage_acquire(sbuf, nst, lane);
+                                                int32_t row0, int32_t z = -1, int nbuf = 2) {
+    uint8_t* buf = stage_acquire(sbuf, nst, lane, nbuf);
     stage_write<128, 32>(buf, 0, w, lane);
     stage_flush(tm, buf, lane, col0, row0, z);
 }
@@ -234,7 +244,7 @@ __device__ __forceinline__ void stage_store_f32(const CUtensorMap* tm, uint8_t* 
 template <int ES>
 __device__ __forceinline__ void stage_codes(EpiTma* t, const uint32_t* w, int64_t col0, bool last) {
     constexpr int NW = 8 * ES;  // 32 codes of ES bytes
-    if (t->qpos == 0) t->qbuf = stage_acquire(t->sbuf, *t->nst, t->lane);
+    if (t->qpos == 0) t->qbuf = stage_acquire(t->sbuf, *t->nst, t->lane, t->nbuf);
     const int span = t->qg * 32 * ES;
     if (span == 128) stage_write<128, NW>(t->qbuf, t->qpos * 32 * ES, w, t->lane);
     else stage_write<64, NW>(t->qbuf, t->qpos * 32 * ES, w, t->lane);
@@ -269,7 +279,7 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
 #pragma unroll
         for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(y[j]);
         stage_store_f32(tm_->c, tm_->sbuf, *tm_->nst, w, tm_->lane, (int32_t)col0,
-                        (int32_t)tm_->row0, tm_->z);
+                        (int32_t)tm_->row0, tm_->z, tm_->nbuf);
     }
     if (!live && !q_tma) return;
     const int64_t base = row * p.N + col0;

@@ -361,7 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
     constexpr int BKE = BKB / ES, UK = 32 / ES, MN_CHUNK = 128 / ES;
     const int ntiles = p.tiles_m * p.tiles_n;  // 256x256 tiles
     const int nitems = ntiles * p.splits;      // (tile, K-split) work items
-    const int nst2 = NB == 1 ? p.stages : G::STAGES;  // ring depth in use
+    const int nst2 = p.stages < G::STAGES ? p.stages : G::STAGES;  // ring depth in use
     const int cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
     (void)ntiles;
     auto item_of = [&](int item, int& tm, int& tn, int& s, int& kb0, int& kb1) {
@@ -769,9 +769,11 @@ static bool use_epi_tma() {
 static int pick_nb(int64_t m, int64_t n, int num_kb, int clusters) {
     const char* e = getenv("FP8B_GEMM_NB");
     if (e && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
-    (void)num_kb;
-    // waves x tile time; the 256x512 tile does a 256x256 tile's work ~12 %
-    // faster (measured at 8192^3: 0.370 vs 0.415 ms)
+    // The 256x512 tile's epilogue is only half hidden, so it pays off only on
+    // long K (measured: 8192^3 0.370 vs 0.415 ms; 4096^3 and every K <= 2048
+    // config-5 shape faster with NB = 1). Then waves x tile time, the 256x512
+    // tile doing a 256x256 tile's work ~12 % faster.
+    if (num_kb < 64) return 1;
     const int64_t tm = (m + BM2 - 1) / BM2;
     const int64_t t1 = tm * ((n + 255) / 256), t2 = tm * ((n + 511) / 512);
     const double c1 = (double)((t1 + clusters - 1) / clusters);
@@ -892,8 +894,14 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
         }
         if (ok2) {
             const int nb = pick_nb(m, n, p.num_kb, num_sms / 2);
-            if (nb == 1) return launch_2sm<ES, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
-            const char* ev = getenv("FP8B_GEMM_EPI");   // NB=2 epilogue: 4x2 (default), 8x1, 8x2
+            const char* ev = getenv("FP8B_GEMM_EPI");   // epilogue warps x buffers: 4x2, 8x1, 8x2
+            if (nb == 1) {
+                // short K: the epilogue, not the MMA, sets the pace -> two warps
+                // per TMEM lane quarter (each half of the tile's columns)
+                const bool ew8 = ev ? (ev[0] == '8') : p.num_kb <= 16;
+                return ew8 ? launch_2sm<ES, 1, 8, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st)
+                           : launch_2sm<ES, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+            }
             if (ev && ev[0] == '8' && ev[2] == '1')
                 return launch_2sm<ES, 2, 8, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
             if (ev && ev[0] == '8' && ev[2] == '2')

@@ -299,10 +299,14 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
         // one max.NaN per element screens for overflow / NaN (rare slow path
         // applies the reference fix-ups and counts them); underflow = nonzero
         // input whose magnitude rounds to zero, counted on real rows/columns.
+        // Screening on the packed codes, four at a time (magnitude bytes m <= 0x7F):
+        //   m >= 0x7B  <=>  bit 7 of m + 5: the max-normal code (possibly from
+        //                   an input above 57344, which the reference overflows),
+        //                   Inf or NaN -> per-element fix-ups below (rare);
+        //   m == 0     <=>  bit 7 of (m | 0x80) - 1 clear: the code rounded to
+        //                   zero; it is an underflow unless the input was +-0.
         const bool sat = ep.cq_sat != 0;
         uint32_t w[8];
-        float amax = 0.0f;
-        uint32_t unf = 0;
         const int nvalid = full ? 32 : (int)(p.N - col0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -310,14 +314,14 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
             const uint32_t hi = cvt_e5m2x2(y[4 * q + 2], y[4 * q + 3]);
             w[q] = __byte_perm(lo, hi, 0x5410);
         }
+        uint32_t big = 0, zero = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            float m;
-            asm("max.NaN.f32 %0, %1, %2;" : "=f"(m) : "f"(amax), "f"(fabsf(y[j])));
-            amax = m;
-            unf += ((__float_as_uint(y[j]) & 0x7FFFFFFFu) - 1u < Fmt<2>::rne_unf_max) && j < nvalid;
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t m = w[q] & 0x7F7F7F7Fu;
+            big |= (m + 0x05050505u) & 0x80808080u;
+            zero |= ~((m | 0x80808080u) - 0x01010101u) & 0x80808080u;
         }
-        if (!(amax <= 57344.0f)) {  // an overflowing or NaN output in this row chunk
+        if (big) {  // an output at the max code, overflowing or NaN in this row chunk
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const uint32_t hw = (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
@@ -327,7 +331,12 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
                 if (live && j < nvalid) { co += b - nn; cn += nn; }
             }
         }
-        if (live) cu += unf;
+        if (zero && live) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                cu += (((w[j >> 2] >> (8 * (j & 3))) & 0x7Fu) == 0u) &&
+                      (__float_as_uint(y[j]) & 0x7FFFFFFFu) != 0u && j < nvalid;
+        }
         if (q_tma) {
             stage_codes<1>(tm_, w, col0, last);
         } else if (live) {

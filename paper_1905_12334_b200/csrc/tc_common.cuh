@@ -137,6 +137,36 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Issue-only TMEM load (no wait): several chunks can be in flight before one
+// tmem_wait_regs(), which also ties the destination registers to the wait so
+// the compiler cannot hoist their uses above it.
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_regs_after_wait(uint32_t (&v)[32]) {
+    asm volatile(""
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                   "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                   "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]),
+                   "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                   "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                   "+r"(v[30]), "+r"(v[31])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // Grouped rasterisation: walk the tile grid in column bands of GROUP_N tiles so
 // the tiles in flight at once (one per SM / SM pair) share a few A row-panels
 // and B column-panels that stay resident in L2.
@@ -254,6 +284,49 @@ __device__ __forceinline__ void stage_codes(EpiTma* t, const uint32_t* w, int64_
     }
 }
 
+// Lean E5M2 RNE output node for one 32-column chunk (bias already added):
+// paired hardware cvt packed straight into words; overflow / NaN screened on
+// the packed codes, four at a time (magnitude bytes m <= 0x7F):
+//   m >= 0x7B  <=>  bit 7 of m + 5: the max-normal code (possibly from an input
+//                   above 57344, which the reference overflows), Inf or NaN ->
+//                   per-element fix-ups (rare);
+//   m == 0     <=>  bit 7 of (m | 0x80) - 1 clear: the code rounded to zero; an
+//                   underflow unless the input was +-0.
+// Counters cover real rows (live) and columns (< nvalid) only.
+__device__ __forceinline__ void lean_e5m2_codes(const float (&y)[32], uint32_t (&w)[8], bool sat,
+                                                bool live, int nvalid, uint32_t& co, uint32_t& cu,
+                                                uint32_t& cn) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t lo = cvt_e5m2x2(y[4 * q], y[4 * q + 1]);
+        const uint32_t hi = cvt_e5m2x2(y[4 * q + 2], y[4 * q + 3]);
+        w[q] = __byte_perm(lo, hi, 0x5410);
+    }
+    uint32_t big = 0, zero = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t m = w[q] & 0x7F7F7F7Fu;
+        big |= (m + 0x05050505u) & 0x80808080u;
+        zero |= ~((m | 0x80808080u) - 0x01010101u) & 0x80808080u;
+    }
+    if (big) {  // an output at the max code, overflowing or NaN in this row chunk
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t hw = (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+            uint32_t b = 0, nn = 0, uu = 0;
+            const uint32_t c = fix_rne<2>(hw, __float_as_uint(y[j]), sat, b, nn, uu);
+            w[j >> 2] = (w[j >> 2] & ~(0xFFu << (8 * (j & 3)))) | (c << (8 * (j & 3)));
+            if (live && j < nvalid) { co += b - nn; cn += nn; }
+        }
+    }
+    if (zero && live) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            cu += (((w[j >> 2] >> (8 * (j & 3))) & 0x7Fu) == 0u) &&
+                  (__float_as_uint(y[j]) & 0x7FFFFFFFu) != 0u && j < nvalid;
+    }
+}
+
 // Epilogue of one 32-column chunk; one row per lane. With TMA stores active
 // (t.c or t.q set) the whole warp must call it -- rows >= M included, TMA clips
 // them and the counters skip them; otherwise rows >= M return early.
@@ -295,48 +368,9 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
         }
     }
     if (ep.cq && ep.cq_mode == FP8B_RNE && ep.cq_fmt == FP8B_E5M2) {
-        // Lean E5M2 RNE path: paired hardware cvt packed straight into words;
-        // one max.NaN per element screens for overflow / NaN (rare slow path
-        // applies the reference fix-ups and counts them); underflow = nonzero
-        // input whose magnitude rounds to zero, counted on real rows/columns.
-        // Screening on the packed codes, four at a time (magnitude bytes m <= 0x7F):
-        //   m >= 0x7B  <=>  bit 7 of m + 5: the max-normal code (possibly from
-        //                   an input above 57344, which the reference overflows),
-        //                   Inf or NaN -> per-element fix-ups below (rare);
-        //   m == 0     <=>  bit 7 of (m | 0x80) - 1 clear: the code rounded to
-        //                   zero; it is an underflow unless the input was +-0.
-        const bool sat = ep.cq_sat != 0;
         uint32_t w[8];
         const int nvalid = full ? 32 : (int)(p.N - col0);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t lo = cvt_e5m2x2(y[4 * q], y[4 * q + 1]);
-            const uint32_t hi = cvt_e5m2x2(y[4 * q + 2], y[4 * q + 3]);
-            w[q] = __byte_perm(lo, hi, 0x5410);
-        }
-        uint32_t big = 0, zero = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t m = w[q] & 0x7F7F7F7Fu;
-            big |= (m + 0x05050505u) & 0x80808080u;
-            zero |= ~((m | 0x80808080u) - 0x01010101u) & 0x80808080u;
-        }
-        if (big) {  // an output at the max code, overflowing or NaN in this row chunk
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t hw = (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-                uint32_t b = 0, nn = 0, uu = 0;
-                const uint32_t c = fix_rne<2>(hw, __float_as_uint(y[j]), sat, b, nn, uu);
-                w[j >> 2] = (w[j >> 2] & ~(0xFFu << (8 * (j & 3)))) | (c << (8 * (j & 3)));
-                if (live && j < nvalid) { co += b - nn; cn += nn; }
-            }
-        }
-        if (zero && live) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                cu += (((w[j >> 2] >> (8 * (j & 3))) & 0x7Fu) == 0u) &&
-                      (__float_as_uint(y[j]) & 0x7FFFFFFFu) != 0u && j < nvalid;
-        }
+        lean_e5m2_codes(y, w, ep.cq_sat != 0, live, nvalid, co, cu, cn);
         if (q_tma) {
             stage_codes<1>(tm_, w, col0, last);
         } else if (live) {

@@ -14,6 +14,7 @@ qa = F.quantize(x[: m * k]).codes
 qb = F.quantize(x[m * k:]).codes
 qa0, qb0 = torch.zeros_like(qa), torch.zeros_like(qb)
 c = torch.empty((m, n), dtype=torch.float32, device="cuda")
+cq = torch.empty(m * n, dtype=torch.uint8, device="cuda")
 a8 = x[: m * k].reshape(m, k).to(torch.float8_e4m3fn)
 b8 = x[m * k:].reshape(n, k).to(torch.float8_e5m2)
 one = torch.ones((), device="cuda")
@@ -23,10 +24,13 @@ del x
 def run_ours(spec):
     env = dict(kv.split(":") for kv in spec.split(",") if kv)
     zeros = env.pop("zeros", None)
+    outq = env.pop("q", None)
     old = {kk: os.environ.get(kk) for kk in env}
     os.environ.update(env)
     try:
-        if zeros:
+        if outq:
+            F.gemm_codes(qa, qb, m, n, k, "fp8", want_c=False, out_fmt="fp8", out_codes=cq)
+        elif zeros:
             F.gemm_codes(qa0, qb0, m, n, k, "fp8", c=c)
         else:
             F.gemm_codes(qa, qb, m, n, k, "fp8", c=c)

@@ -8,12 +8,16 @@ m = n = k = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 F.init()
 x = torch.empty(m * k + k * n, dtype=torch.float32, device="cuda")
 F.fill_synthetic(x, "normal", 3, 1.0)
-if which == "ours":
+if which in ("ours", "ours_q"):
     qa = F.quantize(x[: m * k]).codes
     qb = F.quantize(x[m * k:]).codes
     c = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    cq = torch.empty(m * n, dtype=torch.uint8, device="cuda")
     for _ in range(3):
-        F.gemm_codes(qa, qb, m, n, k, "fp8", c=c)
+        if which == "ours":
+            F.gemm_codes(qa, qb, m, n, k, "fp8", c=c)
+        else:
+            F.gemm_codes(qa, qb, m, n, k, "fp8", want_c=False, out_fmt="fp8", out_codes=cq)
 else:
     a8 = x[: m * k].reshape(m, k).to(torch.float8_e4m3fn)
     b8 = x[m * k:].reshape(n, k).to(torch.float8_e5m2)

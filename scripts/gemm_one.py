@@ -5,6 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1905_12334_b200 as F
 which = sys.argv[1] if len(sys.argv) > 1 else "ours"
 m = n = k = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
+if len(sys.argv) > 4:  # explicit m n k
+    m, n, k = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
 F.init()
 x = torch.empty(m * k + k * n, dtype=torch.float32, device="cuda")
 F.fill_synthetic(x, "normal", 3, 1.0)

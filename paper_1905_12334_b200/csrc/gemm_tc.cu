@@ -27,6 +27,9 @@
 
 #include "tc_common.cuh"
 
+// LEAN kernels make the general epilogue loop unreachable (by design)
+#pragma nv_diag_suppress 128
+
 namespace fp8b {
 namespace tc {
 
@@ -341,7 +344,10 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
 
-template <int ES, int NB, int EW, int NBUF>
+// LEAN = 1: the epilogue is compiled for the fused E5M2 RNE output node only (no
+// FP32 C, no other Q modes, no diagnostics) -- a kernel a fraction of the general
+// one's size, for the instruction cache of epilogue-bound short-K shapes.
+template <int ES, int NB, int EW, int NBUF, int LEAN = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
@@ -591,8 +597,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
         uint32_t accphase = 0;
         const uint32_t te_leader = mapa_u32(smem_u32(tempty_bar), 0);
         const bool split_rel = NB == 2 && !(p.dbg & 512);
-        const bool lean_q = ES > 0 && p.ep.cq && !p.ep.c && p.splits == 1 && p.ep.cq_mode == FP8B_RNE &&
-                            p.ep.cq_fmt == FP8B_E5M2 && !(p.dbg & (4 | 1024 | 2048));
+        const bool lean_q = LEAN || (p.ep.cq && !p.ep.c && p.splits == 1 && p.ep.cq_mode == FP8B_RNE &&
+                                     p.ep.cq_fmt == FP8B_E5M2 && !(p.dbg & (4 | 1024 | 2048)));
         for (int item = cluster_id; item < nitems; item += nclusters) {
             int tm, tn, s, kb0, kb1;
             item_of(item, tm, tn, s, kb0, kb1);
@@ -842,14 +848,16 @@ static int pick_nb(int64_t m, int64_t n, int num_kb, int clusters) {
     return c2 < c1 ? 2 : 1;
 }
 
-template <int ES, int NB, int EW = 4, int NBUF = 2>
+template <int ES, int NB, int EW = 4, int NBUF = 2, int LEAN = 0>
 static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUtensorMap& tmC,
                       const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int num_sms,
                       cudaStream_t st) {
     using G = Geo2<NB, EW, NBUF>;
     static std::once_flag once;
     std::call_once(once, [] {
-        cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF>,
+        cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF, 0>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     });
     Params p2 = p;
@@ -878,7 +886,7 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
         pk.ep = EpiArgs{ws, nullptr, nullptr, 0, 0, 0, 0, nullptr};
         int grid2 = 2 * ntiles2 * splits;
         if (grid2 > maxg) grid2 = maxg;
-        gemm_tc2_kernel<ES, NB, EW, NBUF><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmW, tmQ, pk);
+        gemm_tc2_kernel<ES, NB, EW, NBUF, 0><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmW, tmQ, pk);
         Params pf = p2;
         pf.splits = splits;
         const int64_t nch = m * ((n + 31) / 32);
@@ -890,7 +898,7 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
     }
     int grid2 = 2 * ntiles2;
     if (grid2 > maxg) grid2 = maxg;
-    gemm_tc2_kernel<ES, NB, EW, NBUF><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tmQ, p2);
+    gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tmQ, p2);
     return FP8B_OK;
 }
 
@@ -956,10 +964,15 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
         if (ok2) {
             const int nb = pick_nb(m, n, p.num_kb, num_sms / 2);
             const char* ev = getenv("FP8B_GEMM_EPI");   // epilogue warps x buffers: 4x2, 8x1, 8x2
+            const bool lean = ES == 1 && ep.cq && !ep.c && ep.cq_mode == FP8B_RNE &&
+                              ep.cq_fmt == FP8B_E5M2 && p.dbg == 0;
             if (nb == 1) {
                 // short K: the epilogue, not the MMA, sets the pace -> two warps
                 // per TMEM lane quarter (each half of the tile's columns)
                 const bool ew8 = ev ? (ev[0] == '8') : p.num_kb <= 16;
+                if (lean)
+                    return ew8 ? launch_2sm<ES, 1, 8, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st)
+                               : launch_2sm<ES, 1, 4, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
                 return ew8 ? launch_2sm<ES, 1, 8, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st)
                            : launch_2sm<ES, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
             }
@@ -970,6 +983,7 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
                 return launch_2sm<ES, 2, 8, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
             if (ev && ev[0] == '4')
                 return launch_2sm<ES, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+            if (lean) return launch_2sm<ES, 2, 8, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
             return launch_2sm<ES, 2, 8, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
         }
     }

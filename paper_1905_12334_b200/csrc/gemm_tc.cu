@@ -340,6 +340,43 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar) {
         "h"((uint16_t)3)
         : "memory");
 }
+// One lane of the warp (elect.sync): 1 there, 0 elsewhere.
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t r;
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(r));
+    return r;
+}
+// tcgen05.mma.cta_group::2 issued only where `issue` != 0 (warp-uniform callers).
+// CU: 0 = none, 1 = collector::a::fill, 2 = collector::a::lastuse
+template <int ES, int CU>
+__device__ __forceinline__ void mma2p(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                      uint32_t accum, uint32_t issue) {
+#define FP8B_MMA2P(KIND, COL)                                                                      \
+    asm volatile("{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"           \
+                 "@q tcgen05.mma.cta_group::2.kind::" KIND COL " [%0], %1, %2, %3, p;\n}\n" ::"r"(  \
+                     tmem_d),                                                                      \
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(accum), "r"(issue))
+    if (ES == 1) {
+        if (CU == 0) FP8B_MMA2P("f8f6f4", "");
+        else if (CU == 1) FP8B_MMA2P("f8f6f4", ".collector::a::fill");
+        else FP8B_MMA2P("f8f6f4", ".collector::a::lastuse");
+    } else {
+        if (CU == 0) FP8B_MMA2P("f16", "");
+        else if (CU == 1) FP8B_MMA2P("f16", ".collector::a::fill");
+        else FP8B_MMA2P("f16", ".collector::a::lastuse");
+    }
+#undef FP8B_MMA2P
+}
+__device__ __forceinline__ void umma_commit_mc_p(uint64_t* bar, uint32_t issue) {
+    asm volatile(
+        "{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n"
+        "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3), "r"(issue)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
@@ -459,7 +496,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
+        if (rank == 0 && lane == 0) {
+            // One lane issues. Descriptors are precomputed once (stage 0 /
+            // k-step 0) and advanced by adding the byte offset >> 4 to their
+            // 14-bit address field, instead of being rebuilt per MMA with
+            // runtime layout selects (~25 instructions per MMA before); the
+            // issuer shares its SM sub-partition with epilogue warps, and its
+            // issue rate is what the tensor pipe waits on
+            // (profiles/ncu_gemm_epi_r01.md).
+            const uint32_t leader = 1u;
             uint32_t idesc = (1u << 4);
             if (ES == 1) idesc |= (1u << 7) | (1u << 10);
             if (ES == 1 && (p.dbg & 256)) idesc &= ~(7u << 7);  // diagnostic: A read as E4M3
@@ -467,24 +512,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
             idesc |= (uint32_t)p.b_mn << 16;
             idesc |= (uint32_t)(BN2 >> 3) << 17;
             idesc |= (uint32_t)(BM2 >> 4) << 24;
+            // descriptors of stage 0 / k-step 0; others add (byte offset >> 4) to
+            // the 14-bit address field (smem < 256 KB, so it never carries out)
+            const uint32_t s0 = smem_u32(smem);
+            const uint64_t dA0 = p.a_mn ? umma_desc(s0, BKE * 128, 1024) : umma_desc(s0, 16, 1024);
+            const uint64_t dB0 = p.b_mn ? umma_desc(s0 + A2_BYTES, BKE * 128, 1024)
+                                        : umma_desc(s0 + A2_BYTES, 16, 1024);
+            const uint32_t aLo = (uint32_t)dA0, aHi = (uint32_t)(dA0 >> 32);
+            const uint32_t bLo = (uint32_t)dB0, bHi = (uint32_t)(dB0 >> 32);
+            const uint32_t kA = p.a_mn ? (uint32_t)(UK * 128) >> 4 : 2u;  // per 32-byte K step
+            const uint32_t kB = p.b_mn ? (uint32_t)(UK * 128) >> 4 : 2u;
+            constexpr uint32_t ST16 = STAGE2_BYTES >> 4, BH16 = (128 * BKB) >> 4;
+            const bool issue = leader && !(p.dbg & 1);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t accphase = 0;
-            // NB == 2: the epilogue frees the accumulator in two halves (lo =
-            // columns 0-255, hi = 256-511). The next tile starts as soon as lo
-            // is free, issuing lo MMAs only and keeping those stages resident
-            // until hi is free too; then their hi MMAs go out and the stages
-            // are released. This hides the hi half of the drain.
-            auto issue_half = [&](uint32_t a_base, uint32_t b_base, uint32_t d, int kb, int kb0_) {
+            // one K-block of MMAs from `st` into accumulator column `d`; half 0 =
+            // B rows n0.., half 1 = n0 + 256.. (NB = 2); both = the pair sharing A
+            auto issue_kb = [&](int st, uint32_t d, int half, bool both, bool first) {
+                // only the low word of a descriptor moves (32-bit adds)
+                const uint32_t a_st = aLo + (uint32_t)st * ST16;
+                const uint32_t b_st = bLo + (uint32_t)st * ST16 + (uint32_t)half * BH16;
 #pragma unroll
                 for (int k = 0; k < BKB / 32; ++k) {
-                    uint64_t ad, bd;
-                    if (!p.a_mn) ad = umma_desc(a_base + 32 * k, 16, 1024);
-                    else ad = umma_desc(a_base + k * UK * 128, BKE * 128, 1024);
-                    if (!p.b_mn) bd = umma_desc(b_base + 32 * k, 16, 1024);
-                    else bd = umma_desc(b_base + k * UK * 128, BKE * 128, 1024);
-                    mma2<ES>(d, ad, bd, idesc, (kb != kb0_ || k != 0) ? 1u : 0u);
+                    const uint64_t ad = ((uint64_t)aHi << 32) | (a_st + (uint32_t)k * kA);
+                    const uint64_t bd = ((uint64_t)bHi << 32) | (b_st + (uint32_t)k * kB);
+                    const uint32_t acc_on = (first && k == 0) ? 0u : 1u;
+                    if (!both) {
+                        mma2p<ES, 0>(d, ad, bd, idesc, acc_on, issue);
+                    } else {
+                        const uint64_t bd2 = ((uint64_t)bHi << 32) | (b_st + (uint32_t)k * kB + BH16);
+                        mma2p<ES, 1>(d, ad, bd, idesc, acc_on, issue);
+                        mma2p<ES, 2>(d + BN2, ad, bd2, idesc, acc_on, issue);
+                    }
                 }
             };
             for (int item = cluster_id; item < nitems; item += nclusters) {
@@ -494,15 +555,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
                 fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
                 if (NB == 2 && !(p.dbg & 512)) {
+                    // The epilogue frees the accumulator in two halves (lo =
+                    // columns 0-255, hi = 256-511). The next tile starts as soon as
+                    // lo is free, issuing lo MMAs only and keeping those stages
+                    // resident until hi is free too; then their hi MMAs go out and
+                    // the stages are released. This hides the hi half of the drain.
                     bool hi_free = false;
                     int npend = 0, pend_stage = 0, pend_kb = 0;
                     auto flush = [&]() {
                         int st = pend_stage;
                         for (int j = 0; j < npend; ++j) {
-                            const uint32_t a_base = smem_u32(smem + st * STAGE2_BYTES);
-                            issue_half(a_base, a_base + A2_BYTES + 128 * BKB, d_tmem + BN2,
-                                       pend_kb + j, kb0);
-                            umma_commit_mc(empty_bar + st);
+                            issue_kb(st, d_tmem + BN2, 1, false, pend_kb + j == kb0);
+                            umma_commit_mc_p(empty_bar + st, leader);
                             if (++st == nst2) st = 0;
                         }
                         npend = 0;
@@ -515,26 +579,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
                             fence_after();
                             flush();
                         }
-                        const uint32_t a_base = smem_u32(smem + stage * STAGE2_BYTES);
-                        const uint32_t b_base = a_base + A2_BYTES;
                         if (hi_free) {
-#pragma unroll
-                            for (int k = 0; k < BKB / 32; ++k) {
-                                uint64_t ad, bd;
-                                if (!p.a_mn) ad = umma_desc(a_base + 32 * k, 16, 1024);
-                                else ad = umma_desc(a_base + k * UK * 128, BKE * 128, 1024);
-                                const uint32_t acc_on = (kb != kb0 || k != 0) ? 1u : 0u;
-                                if (!p.b_mn) bd = umma_desc(b_base + 32 * k, 16, 1024);
-                                else bd = umma_desc(b_base + k * UK * 128, BKE * 128, 1024);
-                                mma2c<ES, 1>(d_tmem, ad, bd, idesc, acc_on);
-                                const uint32_t b2 = b_base + 128 * BKB;
-                                if (!p.b_mn) bd = umma_desc(b2 + 32 * k, 16, 1024);
-                                else bd = umma_desc(b2 + k * UK * 128, BKE * 128, 1024);
-                                mma2c<ES, 2>(d_tmem + BN2, ad, bd, idesc, acc_on);
-                            }
-                            umma_commit_mc(empty_bar + stage);
+                            issue_kb(stage, d_tmem, 0, true, kb == kb0);
+                            umma_commit_mc_p(empty_bar + stage, leader);
                         } else {
-                            issue_half(a_base, b_base, d_tmem, kb, kb0);
+                            issue_kb(stage, d_tmem, 0, false, kb == kb0);
                             if (npend++ == 0) { pend_stage = stage; pend_kb = kb; }
                             if (npend == nst2) {  // every ring slot waits on hi
                                 mbar_wait(tempty_bar + 1, accphase ^ 1);
@@ -550,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
                         fence_after();
                         flush();
                     }
-                    umma_commit_mc(tfull_bar + acc);
+                    umma_commit_mc_p(tfull_bar + acc, leader);
                     accphase ^= 1;
                     continue;
                 }
@@ -558,32 +607,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
                     if (p.dbg & 16) mbar_wait_spin(full_bar + stage, phase);
                     else if (!(p.dbg & 8)) mbar_wait(full_bar + stage, phase);
                     fence_after();
-                    const uint32_t a_base = smem_u32(smem + stage * STAGE2_BYTES);
-                    const uint32_t b_base = a_base + A2_BYTES;
-#pragma unroll
-                    for (int k = 0; k < BKB / 32; ++k) {
-                        if (p.dbg & 1) break;
-                        uint64_t ad, bd;
-                        if (!p.a_mn) ad = umma_desc(a_base + 32 * k, 16, 1024);
-                        else ad = umma_desc(a_base + k * UK * 128, BKE * 128, 1024);
-                        const uint32_t acc_on = (kb != kb0 || k != 0) ? 1u : 0u;
-                        if (!p.b_mn) bd = umma_desc(b_base + 32 * k, 16, 1024);
-                        else bd = umma_desc(b_base + k * UK * 128, BKE * 128, 1024);
-                        if (NB == 1) {
-                            mma2<ES>(d_tmem, ad, bd, idesc, acc_on);
-                        } else {
-                            // same A for both halves of N: load it into the collector once
-                            mma2c<ES, 1>(d_tmem, ad, bd, idesc, acc_on);
-                            const uint32_t b2 = b_base + 128 * BKB;
-                            if (!p.b_mn) bd = umma_desc(b2 + 32 * k, 16, 1024);
-                            else bd = umma_desc(b2 + k * UK * 128, BKE * 128, 1024);
-                            mma2c<ES, 2>(d_tmem + BN2, ad, bd, idesc, acc_on);
-                        }
-                    }
-                    if (!(p.dbg & 8)) umma_commit_mc(empty_bar + stage);
+                    issue_kb(stage, d_tmem, 0, NB == 2, kb == kb0);
+                    if (!(p.dbg & 8)) umma_commit_mc_p(empty_bar + stage, leader);
                     if (++stage == nst2) { stage = 0; phase ^= 1; }
                 }
-                umma_commit_mc(tfull_bar + acc);
+                umma_commit_mc_p(tfull_bar + acc, leader);
                 if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
             }
         }

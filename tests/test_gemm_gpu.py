@@ -251,3 +251,44 @@ def test_splitk_tolerance_long_k(fp8, splitk_env, splits):
     ex = da @ db
     absdot = da.abs() @ db.abs()
     assert bool(((c.double() - ex).abs() <= TAU * absdot + 1e-30).all())
+
+
+@pytest.fixture
+def nb_env():
+    old = {k: os.environ.get(k) for k in ("FP8B_GEMM_NB",)}
+    yield
+    for k, v in old.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+@pytest.mark.parametrize("m,k,n,nb", [(512, 8192, 1024, "2"), (768, 512, 1280, ""),
+                                      (256, 2048, 512, "1")])
+def test_lean_codes_only_exact_grid(fp8, nb_env, m, k, n, nb):
+    """The LEAN kernels (fused E5M2 RNE output only, no FP32 C; 256x512 and
+    256x256 pair tiles): on an exact operand grid the codes and all three
+    counters must equal Q_RNE of the exact result, with bias columns that force
+    overflow (> 57344), underflow (tiny nonzero outputs) and NaN."""
+    import torch
+    os.environ["FP8B_GEMM_NB"] = nb
+    rng = np.random.default_rng(77)
+    A = O.quantize((rng.integers(-2, 3, m * k) * 0.5).astype(np.float32))[0].reshape(m, k)
+    B = O.quantize((rng.integers(-2, 3, k * n) * 0.25).astype(np.float32))[0].reshape(k, n)
+    B[:, 5::97] = 0  # zero columns: output = bias exactly
+    bias = (rng.integers(-8, 8, n) * 0.125).astype(np.float32)
+    bias[3::61] = 60000.0
+    bias[5::97] = 1e-6
+    bias[7::211] = np.nan
+    cnt = fp8.Counters()
+    _, cq = fp8.gemm_codes(_codes_dev(A, "fp8"), _codes_dev(B, "fp8"), m, n, k, "fp8",
+                           engine="tensor", want_c=False, bias=torch.from_numpy(bias).cuda(),
+                           out_fmt="fp8", out_mode="nearest-even", out_counters=cnt)
+    da = O.dequantize(A).astype(np.float64).reshape(m, k)
+    db = O.dequantize(B).astype(np.float64).reshape(k, n)
+    y = ((da @ db).astype(np.float32) + bias[None, :]).astype(np.float32)
+    codes, k_ = O.quantize(y, "fp8", "nearest-even", 1)
+    np.testing.assert_array_equal(cq.cpu().numpy(), codes.astype(np.uint8))
+    assert cnt.values() == tuple(int(v) for v in k_)
+    assert k_[0] > 0 and k_[1] > 0 and k_[2] > 0

@@ -410,6 +410,20 @@ template <int MB>
 __device__ __forceinline__ uint32_t special_packed(bool sat) {
     return (sat ? Fmt<MB>::maxcode : Fmt<MB>::infcode) << 16;
 }
+// NaN-propagating max (max.NaN): the screen of an overflow / NaN input.
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+// Number of code magnitudes equal to 0 in a packed word of codes (MASK = the
+// magnitude bits of each code: 0x7F7F7F7F for E5M2, 0x7FFF7FFF for FP16). A
+// magnitude m plus the all-but-top mask sets the code's top bit iff m != 0,
+// with no carry into the next code.
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t zero_mags(uint32_t w) {
+    return __popc(~((w & MASK) + MASK) & ~MASK);
+}
 // Gather the code bytes (E5M2) of four packed sums plus the four input signs.
 __device__ __forceinline__ uint32_t gather_e5m2(uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3,
                                                 uint32_t u0, uint32_t u1, uint32_t u2, uint32_t u3) {

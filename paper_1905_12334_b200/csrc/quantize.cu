@@ -73,36 +73,55 @@ __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict_
                 for (int k = 0; k < 4; ++k)
                     c[k] = fix_rne<MB>(c[k], __float_as_uint(f[k]), sat, c_big, c_nan, c_unf);
             } else {
+                // SR / TRUNC on the packed representation. Screens: amax
+                // (NaN-propagating) for overflow / NaN inputs, amin for an exact
+                // zero input; underflow = code magnitude 0 from a nonzero input,
+                // counted on the packed output words.
                 uint64_t word = 0;
                 if (MODE == 1) word = counter_word(seed, (uint64_t)((elem_offset >> 2) + g));
-                uint32_t sum[4];
-                float nanacc = 0.0f;
+                uint32_t r16[4] = {0u, 0u, 0u, 0u};  // TRUNC == SR with r16 = 0
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    uint32_t r16 = 0;  // TRUNC == SR with r16 = 0
-                    if (MODE == 1) r16 = (uint32_t)(word >> (16 * k)) & 0xFFFFu;
-                    if (MODE == 2) r16 = rb[j][k];
+                    if (MODE == 1) r16[k] = (uint32_t)(word >> (16 * k)) & 0xFFFFu;
+                    if (MODE == 2) r16[k] = rb[j][k];
+                }
+                const float amax = fmax_nan(fmax_nan(fabsf(f[0]), fabsf(f[1])), fmax_nan(fabsf(f[2]), fabsf(f[3])));
+                const float amin = fminf(fminf(fabsf(f[0]), fabsf(f[1])), fminf(fabsf(f[2]), fabsf(f[3])));
+                uint32_t sum[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {  // overflow (Inf / max code) or NaN: select, no branch
                     const bool big = big_or_nan<MB>(f[k]);
                     c_big += big;
-                    sum[k] = (big ? special_packed<MB>(sat) : packed_sr<MB>(f[k])) + r16;
-                    c_unf += (sum[k] < 0x10000u) & (fabsf(f[k]) != 0.0f);
-                    nanacc = fmaf(f[k], 0.0f, nanacc);
+                    sum[k] = (big ? special_packed<MB>(sat) : packed_sr<MB>(f[k])) + r16[k];
                 }
                 const uint32_t u[4] = {__float_as_uint(f[0]), __float_as_uint(f[1]),
                                        __float_as_uint(f[2]), __float_as_uint(f[3])};
+                uint32_t w0, w1 = 0;
                 if (MB == 2) {
-                    const uint32_t w = gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]);
-                    c[0] = w & 0xFFu; c[1] = (w >> 8) & 0xFFu; c[2] = (w >> 16) & 0xFFu; c[3] = w >> 24;
+                    w0 = gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]);
+                    c_unf += zero_mags<0x7F7F7F7Fu>(w0);
                 } else {
-                    const uint32_t w0 = gather_f16(sum[0], sum[1], u[0], u[1]);
-                    const uint32_t w1 = gather_f16(sum[2], sum[3], u[2], u[3]);
-                    c[0] = w0 & 0xFFFFu; c[1] = w0 >> 16; c[2] = w1 & 0xFFFFu; c[3] = w1 >> 16;
+                    w0 = gather_f16(sum[0], sum[1], u[0], u[1]);
+                    w1 = gather_f16(sum[2], sum[3], u[2], u[3]);
+                    c_unf += zero_mags<0x7FFF7FFFu>(w0) + zero_mags<0x7FFF7FFFu>(w1);
                 }
-                if (nanacc != nanacc) {  // rare: an Inf or NaN input; NaN -> canonical code
+                if (amin == 0.0f) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) c_unf -= (u[k] << 1) == 0u;
+                }
+                if (amax != amax) {  // rare: NaN -> canonical unsigned code (float_format.cpp:99)
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        if (f[k] != f[k]) { c[k] = Fmt<MB>::nancode; ++c_nan; }
+                        if (f[k] != f[k]) {
+                            ++c_nan;
+                            if (MB == 2) w0 = (w0 & ~(0xFFu << (8 * k))) | ((uint32_t)Fmt<MB>::nancode << (8 * k));
+                            else if (k < 2) w0 = (w0 & ~(0xFFFFu << (16 * k))) | ((uint32_t)Fmt<MB>::nancode << (16 * k));
+                            else w1 = (w1 & ~(0xFFFFu << (16 * (k - 2)))) | ((uint32_t)Fmt<MB>::nancode << (16 * (k - 2)));
+                        }
                 }
+                if (MB == 2) __stcs(reinterpret_cast<uint32_t*>(codes) + g, w0);
+                else __stcs(reinterpret_cast<uint2*>(codes) + g, make_uint2(w0, w1));
+                continue;
             }
             if (MB == 2) {
                 const uint32_t w = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
@@ -192,6 +211,7 @@ __device__ __forceinline__ void store4(void* codes, int64_t i0, const uint32_t (
 // reads its samples from the jump table kept in shared memory. The table copy
 // carries the 4096-entry wrap extension, so no modular addressing is needed.
 constexpr int kWarpLfsrThreads = 768;
+
 constexpr int kTabWrapBytes = ((kLfsrPeriod + kBlock) * 2 + 15) & ~15;  // 139264
 template <int MB>
 __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
@@ -201,7 +221,7 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t tab_bar;
     const bool sat = saturate != 0;
-    const uint32_t special = special_packed<MB>(sat);
+    const uint32_t special_code = special_packed<MB>(sat);
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * kWarpLfsrThreads + threadIdx.x) >> 5;
@@ -227,35 +247,32 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
         if (lane == 0 && b + wstride < nfull)
             p0_next = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b + wstride)));
         const float4* xb = reinterpret_cast<const float4*>(x + b * kBlock) + 2 * lane;
-        float4 va = __ldcs(xb), vb = __ldcs(xb + 1);
         uint32_t run = stab_addr + 2u * p0;  // table byte address of the chunk's first sample
-#pragma unroll 2
-        for (int c = 0; c < kBlock / 256; ++c) {
+        // one 256-element chunk: 8 consecutive elements per lane
+        auto chunk = [&](const float4& va, const float4& vb, int c) {
             const uint32_t u[8] = {__float_as_uint(va.x), __float_as_uint(va.y), __float_as_uint(va.z),
                                    __float_as_uint(va.w), __float_as_uint(vb.x), __float_as_uint(vb.y),
                                    __float_as_uint(vb.z), __float_as_uint(vb.w)};
-            if (c + 1 < kBlock / 256) {  // prefetch the next chunk
-                va = __ldcs(xb + 64 * (c + 1));
-                vb = __ldcs(xb + 64 * (c + 1) + 1);
-            }
             uint32_t P[8], inc[8], n = 0;
-            float nanacc = 0.0f, amax = 0.0f;
+            // screen: amax (NaN-propagating) catches overflow / NaN inputs
+            float amax = fabsf(__uint_as_float(u[0]));
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const float f = __uint_as_float(u[k]);
-                amax = fmaxf(amax, fabsf(f));
-                nanacc = fmaf(f, 0.0f, nanacc);  // NaN iff some input is NaN or +-Inf
+                if (k) amax = fmax_nan(amax, fabsf(f));
                 P[k] = packed_sr<MB>(f);
                 inc[k] = inexact_sr<MB>(f) ? 2u : 0u;  // byte stride in the table
             }
             // rare: an overflowing or NaN input in this lane -> the reference's
             // overflow code (Inf / max when saturating) and no sample taken
-            if (nanacc != nanacc || amax > (MB == 2 ? 57344.0f : 65504.0f)) {
+            bool has_nan = false;
+            if (!(amax <= (MB == 2 ? 57344.0f : 65504.0f))) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const bool big = big_or_nan<MB>(__uint_as_float(u[k]));
                     c_big += big;
-                    if (big) { P[k] = special; inc[k] = 0u; }
+                    has_nan |= (u[k] & 0x7FFFFFFFu) > 0x7F800000u;
+                    if (big) { P[k] = special_code; inc[k] = 0u; }
                 }
             }
 #pragma unroll
@@ -283,16 +300,18 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
             }
             const int64_t e0 = b * kBlock + 256 * c + 8 * lane;  // first element of this lane
             if (MB == 2) {
-                __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(codes) + e0),
-                       make_uint2(gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]),
-                                  gather_e5m2(sum[4], sum[5], sum[6], sum[7], u[4], u[5], u[6], u[7])));
+                const uint32_t w0 = gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]);
+                const uint32_t w1 = gather_e5m2(sum[4], sum[5], sum[6], sum[7], u[4], u[5], u[6], u[7]);
+                __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(codes) + e0), make_uint2(w0, w1));
             } else {
-                __stcs(reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(codes) + e0),
-                       make_uint4(gather_f16(sum[0], sum[1], u[0], u[1]), gather_f16(sum[2], sum[3], u[2], u[3]),
-                                  gather_f16(sum[4], sum[5], u[4], u[5]), gather_f16(sum[6], sum[7], u[6], u[7])));
+                const uint32_t w0 = gather_f16(sum[0], sum[1], u[0], u[1]);
+                const uint32_t w1 = gather_f16(sum[2], sum[3], u[2], u[3]);
+                const uint32_t w2 = gather_f16(sum[4], sum[5], u[4], u[5]);
+                const uint32_t w3 = gather_f16(sum[6], sum[7], u[6], u[7]);
+                __stcs(reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(codes) + e0), make_uint4(w0, w1, w2, w3));
             }
             // rare: NaN among the lane's inputs -> canonical unsigned NaN code (float_format.cpp:99)
-            if (nanacc != nanacc) {
+            if (has_nan) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     if ((u[k] & 0x7FFFFFFFu) > 0x7F800000u) {
@@ -301,6 +320,19 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
                         else reinterpret_cast<uint16_t*>(codes)[e0 + k] = 0x7E00;
                     }
             }
+        };
+        // two register sets in ping-pong, each chunk's loads issued one chunk
+        // ahead (no register copies between chunks)
+        float4 a0 = __ldcs(xb), a1 = __ldcs(xb + 1);
+#pragma unroll 1
+        for (int c = 0; c < kBlock / 256; c += 2) {
+            const float4 b0 = __ldcs(xb + 64 * (c + 1)), b1 = __ldcs(xb + 64 * (c + 1) + 1);
+            chunk(a0, a1, c);
+            if (c + 2 < kBlock / 256) {
+                a0 = __ldcs(xb + 64 * (c + 2));
+                a1 = __ldcs(xb + 64 * (c + 2) + 1);
+            }
+            chunk(b0, b1, c + 1);
         }
     }
     if (counters) flush_counters<kWarpLfsrThreads>(c_big - c_nan, c_unf, c_nan, counters);

@@ -244,17 +244,23 @@ constexpr uint32_t A2_BYTES = 128 * BKB;  // per CTA
 // EW epilogue warps (4, or 8 = two per TMEM lane quarter splitting each
 // 256-column block), NBUF 4 KB staging buffers per epilogue warp; the ring
 // takes what shared memory is left (at most 6 stages).
-template <int NB, int EW = 4, int NBUF = 2>
+template <int NB, int EW = 4, int NBUF = 2, int AST = 0>
 struct Geo2 {
     static constexpr int NACC = NB == 1 ? 2 : 1;
     static constexpr int TN = NB * BN2;
     static constexpr uint32_t B_BYTES = NB * 128 * BKB;  // per CTA
-    static constexpr uint32_t STAGE = A2_BYTES + B_BYTES;
+    // AST > 0 (A-stationary, short K): the CTA's A rows for all AST k-blocks stay
+    // resident at the start of shared memory while the pair walks every N tile
+    // of its M block; the ring stages then carry B only.
+    static constexpr uint32_t RING_OFF = (uint32_t)AST * A2_BYTES;
+    static constexpr uint32_t STAGE = AST ? B_BYTES : A2_BYTES + B_BYTES;
     static constexpr uint32_t EPI = (uint32_t)EW * NBUF * 4096;
-    static constexpr int FIT = (int)((232448u - EPI - 1536u) / STAGE);
-    static constexpr int STAGES = FIT < 6 ? FIT : 6;
+    static constexpr int FIT = (int)((232448u - RING_OFF - EPI - 1536u) / STAGE);
+    static constexpr int CAP = AST ? 8 : 6;
+    static constexpr int STAGES = FIT < CAP ? FIT : CAP;
+    static constexpr uint32_t EPI_OFF = RING_OFF + STAGES * STAGE;
     static constexpr int THREADS = 64 + 32 * EW;
-    static constexpr uint32_t SMEM = STAGES * STAGE + EPI + 1024 + 512;
+    static constexpr uint32_t SMEM = EPI_OFF + EPI + 1024 + 512;
 };
 constexpr int STAGES2 = Geo2<1>::STAGES;
 
@@ -384,31 +390,45 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
 // LEAN = 1: the epilogue is compiled for the fused E5M2 RNE output node only (no
 // FP32 C, no other Q modes, no diagnostics) -- a kernel a fraction of the general
 // one's size, for the instruction cache of epilogue-bound short-K shapes.
-template <int ES, int NB, int EW, int NBUF, int LEAN = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::THREADS, 1)
+template <int ES, int NB, int EW, int NBUF, int LEAN = 0, int AST = 0>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, AST>::THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
                    const Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    using G = Geo2<NB, EW, NBUF>;
+    using G = Geo2<NB, EW, NBUF, AST>;
+    static_assert(AST == 0 || NB == 1, "A-stationary runs the 256x256 pair tile");
     constexpr uint32_t STAGE2_BYTES = G::STAGE;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::STAGES * STAGE2_BYTES + G::EPI);
+    uint8_t* const ring = smem + G::RING_OFF;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::EPI_OFF + G::EPI);
     uint64_t* empty_bar = full_bar + G::STAGES;
     uint64_t* tfull_bar = empty_bar + G::STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* afull_bar = tempty_bar + 2;   // AST: resident A loaded (leader CTA)
+    uint64_t* aempty_bar = afull_bar + 1;   // AST: the M block's last MMAs done (both CTAs)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty_bar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     constexpr int BKE = BKB / ES, UK = 32 / ES, MN_CHUNK = 128 / ES;
     const int ntiles = p.tiles_m * p.tiles_n;  // 256x256 tiles
-    const int nitems = ntiles * p.splits;      // (tile, K-split) work items
+    // AST: cluster c walks M blocks c, c + nclusters, ... and, for each, every N
+    // tile in order (items beyond tiles_m are skipped by every role alike)
+    const int nitems = AST ? ((p.tiles_m + (gridDim.x >> 1) - 1) / (gridDim.x >> 1)) * (gridDim.x >> 1) * p.tiles_n
+                           : ntiles * p.splits;  // (tile, K-split) work items
     const int nst2 = p.stages < G::STAGES ? p.stages : G::STAGES;  // ring depth in use
     const int cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
     (void)ntiles;
     auto item_of = [&](int item, int& tm, int& tn, int& s, int& kb0, int& kb1) {
+        if (AST) {
+            const int r = item / nclusters;
+            tn = r % p.tiles_n;
+            tm = (r / p.tiles_n) * nclusters + (item - r * nclusters);
+            s = 0; kb0 = 0; kb1 = p.num_kb;
+            return;
+        }
         const int tile = item / p.splits;
         s = item - tile * p.splits;
         tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
@@ -427,6 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
             mbar_init(tfull_bar + a, 1);
             mbar_init(tempty_bar + a, 2 * EW);  // EW epilogue warps x 2 CTAs
         }
+        mbar_init(afull_bar, 1);
+        mbar_init(aempty_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -444,11 +466,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
     if (warp == 0) {
         if (lane == 0 && !(p.dbg & 8)) {
             int stage = 0;
-            uint32_t phase = 0;
+            uint32_t phase = 0, aphase = 0;
             for (int item = cluster_id; item < nitems; item += nclusters) {
                 int tm, tn, s, kb0, kb1;
                 item_of(item, tm, tn, s, kb0, kb1);
+                if (AST && tm >= p.tiles_m) continue;
                 const int32_t m0 = tm * BM2 + (int32_t)rank * 128, n0 = tn * G::TN + (int32_t)rank * 128;
+                if (AST) {
+                    if (tn == 0) {  // a new M block: its A rows, all k-blocks, once
+                        mbar_wait(aempty_bar, aphase ^ 1);
+                        const uint32_t fa = mapa_u32(smem_u32(afull_bar), 0);
+                        if (rank == 0) mbar_expect_tx(afull_bar, 2u * (uint32_t)p.num_kb * A2_BYTES);
+                        for (int kb = 0; kb < p.num_kb; ++kb)
+                            tma_load_2d_2sm(&tmA, smem + kb * A2_BYTES, fa, kb * BKE, m0);
+                        aphase ^= 1;
+                    }
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(empty_bar + stage, phase ^ 1);
+                        const uint32_t fb = mapa_u32(smem_u32(full_bar + stage), 0);
+                        if (rank == 0) mbar_expect_tx(full_bar + stage, 2 * STAGE2_BYTES);
+                        uint8_t* sB = ring + stage * STAGE2_BYTES;
+                        const int32_t k0 = kb * BKE;
+                        if (!p.b_mn) {
+                            tma_load_2d_2sm(&tmB, sB, fb, k0, n0);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 128 / MN_CHUNK; ++j)
+                                tma_load_2d_2sm(&tmB, sB + j * (BKE * 128), fb, n0 + j * MN_CHUNK, k0);
+                        }
+                        if (++stage == nst2) { stage = 0; phase ^= 1; }
+                    }
+                    continue;
+                }
                 for (int kb = kb0; kb < kb1; ++kb) {
                     if (p.dbg & 32) mbar_wait_spin(empty_bar + stage, phase ^ 1);
                     else mbar_wait(empty_bar + stage, phase ^ 1);
@@ -459,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
                         continue;
                     }
                     if (rank == 0) mbar_expect_tx(full_bar + stage, 2 * STAGE2_BYTES);
-                    uint8_t* sA = smem + stage * STAGE2_BYTES;
+                    uint8_t* sA = ring + stage * STAGE2_BYTES;
                     uint8_t* sB = sA + A2_BYTES;
                     const int32_t k0 = kb * BKE;
                     if (NB == 1 && (p.dbg & 64)) {
@@ -516,8 +565,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
             // the 14-bit address field (smem < 256 KB, so it never carries out)
             const uint32_t s0 = smem_u32(smem);
             const uint64_t dA0 = p.a_mn ? umma_desc(s0, BKE * 128, 1024) : umma_desc(s0, 16, 1024);
-            const uint64_t dB0 = p.b_mn ? umma_desc(s0 + A2_BYTES, BKE * 128, 1024)
-                                        : umma_desc(s0 + A2_BYTES, 16, 1024);
+            const uint32_t b_off = AST ? G::RING_OFF : A2_BYTES;  // B of stage 0
+            const uint64_t dB0 = p.b_mn ? umma_desc(s0 + b_off, BKE * 128, 1024)
+                                        : umma_desc(s0 + b_off, 16, 1024);
             const uint32_t aLo = (uint32_t)dA0, aHi = (uint32_t)(dA0 >> 32);
             const uint32_t bLo = (uint32_t)dB0, bHi = (uint32_t)(dB0 >> 32);
             const uint32_t kA = p.a_mn ? (uint32_t)(UK * 128) >> 4 : 2u;  // per 32-byte K step
@@ -530,9 +580,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
             uint32_t accphase = 0;
             // one K-block of MMAs from `st` into accumulator column `d`; half 0 =
             // B rows n0.., half 1 = n0 + 256.. (NB = 2); both = the pair sharing A
-            auto issue_kb = [&](int st, uint32_t d, int half, bool both, bool first) {
-                // only the low word of a descriptor moves (32-bit adds)
-                const uint32_t a_st = aLo + (uint32_t)st * ST16;
+            auto issue_kb = [&](int st, uint32_t d, int half, bool both, bool first, int akb = 0) {
+                // only the low word of a descriptor moves (32-bit adds); AST: A
+                // is the resident k-block akb
+                const uint32_t a_st = AST ? aLo + (uint32_t)akb * (A2_BYTES >> 4) : aLo + (uint32_t)st * ST16;
                 const uint32_t b_st = bLo + (uint32_t)st * ST16 + (uint32_t)half * BH16;
 #pragma unroll
                 for (int k = 0; k < BKB / 32; ++k) {
@@ -548,9 +599,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
                     }
                 }
             };
+            uint32_t aphase = 0;
             for (int item = cluster_id; item < nitems; item += nclusters) {
                 int tm, tn, s, kb0, kb1;
                 item_of(item, tm, tn, s, kb0, kb1);
+                if (AST) {
+                    if (tm >= p.tiles_m) continue;
+                    if (tn == 0) {
+                        mbar_wait(afull_bar, aphase);
+                        fence_after();
+                    }
+                    mbar_wait(tempty_bar + acc, accphase ^ 1);
+                    fence_after();
+                    const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(full_bar + stage, phase);
+                        fence_after();
+                        issue_kb(stage, d_tmem, 0, false, kb == kb0, kb);
+                        umma_commit_mc_p(empty_bar + stage, leader);
+                        if (++stage == nst2) { stage = 0; phase ^= 1; }
+                    }
+                    umma_commit_mc_p(tfull_bar + acc, leader);
+                    if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
+                    if (tn == p.tiles_n - 1) {  // the M block's A may be replaced
+                        umma_commit_mc_p(aempty_bar, leader);
+                        aphase ^= 1;
+                    }
+                    continue;
+                }
                 mbar_wait(tempty_bar + acc, accphase ^ 1);
                 fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
@@ -617,9 +693,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
         }
     } else {
         const int quarter = warp & 3;            // TMEM lane quarter this warp may read
-        const int ehalf = (warp - 2) >> 2;       // EW = 8: which half of each 256-column block
+        const int ehalf = (warp - 2) >> 2;       // EW = 8 / 16: which half / quarter of each 256-column block
         constexpr int PERB = 8 / (EW / 4);       // chunks per 256-column block per warp
-        uint8_t* sbuf = smem + G::STAGES * STAGE2_BYTES + (warp - 2) * (NBUF * 4096);
+        uint8_t* sbuf = smem + G::EPI_OFF + (warp - 2) * (NBUF * 4096);
         uint32_t nst = 0;
         int acc = 0;
         uint32_t accphase = 0;
@@ -630,6 +706,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF>::
         for (int item = cluster_id; item < nitems; item += nclusters) {
             int tm, tn, s, kb0, kb1;
             item_of(item, tm, tn, s, kb0, kb1);
+            if (AST && tm >= p.tiles_m) continue;
             const int64_t row = (int64_t)tm * BM2 + rank * 128 + quarter * 32 + lane;
             if (p.dbg & 128) {
                 // one poller, the other epilogue warps park on a named barrier
@@ -876,6 +953,37 @@ static int pick_nb(int64_t m, int64_t n, int num_kb, int clusters) {
     return c2 < c1 ? 2 : 1;
 }
 
+// A-stationary pair kernel (short K, many M blocks, several N tiles): A is read
+// into shared memory once per M block instead of once per tile, halving the
+// L2 -> SMEM operand stream that bounds short-K shapes.
+template <int ES, int EW, int NBUF, int LEAN, int AST>
+static int launch_2sm_ast(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUtensorMap& tmC,
+                          const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int num_sms,
+                          cudaStream_t st) {
+    using G = Geo2<1, EW, NBUF, AST>;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(gemm_tc2_kernel<ES, 1, EW, NBUF, LEAN, AST>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    });
+    Params p2 = p;
+    p2.tiles_m = (int)((m + BM2 - 1) / BM2);
+    p2.tiles_n = (int)((n + G::TN - 1) / G::TN);
+    p2.splits = 1;
+    // each epilogue warp stores 256 / (EW / 4) columns of a tile: code boxes of that width
+    CUtensorMap tq2 = tmQ;
+    constexpr int cols_per_warp = 256 / (EW / 4);
+    if (p2.q_tma && cols_per_warp < 128) {
+        p2.qg = code_group(p.ep.cq_fmt, cols_per_warp);
+        if (!make_q_map(&tq2, p.ep.cq, p.ep.cq_fmt, m, n, cols_per_warp)) p2.q_tma = 0;
+    }
+    int grid2 = 2 * p2.tiles_m;
+    const int maxg = num_sms & ~1;
+    if (grid2 > maxg) grid2 = maxg;
+    gemm_tc2_kernel<ES, 1, EW, NBUF, LEAN, AST><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tq2, p2);
+    return FP8B_OK;
+}
+
 template <int ES, int NB, int EW = 4, int NBUF = 2, int LEAN = 0>
 static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUtensorMap& tmC,
                       const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int num_sms,
@@ -998,6 +1106,21 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
                 // short K: the epilogue, not the MMA, sets the pace -> two warps
                 // per TMEM lane quarter (each half of the tile's columns)
                 const bool ew8 = ev ? (ev[0] == '8') : p.num_kb <= 16;
+                // K <= 512 bytes, K-major A, >= 2 N tiles and >= 4 M blocks per
+                // cluster: A-stationary (FP8B_GEMM_AST=0 disables, =1 forces)
+                const char* ea = getenv("FP8B_GEMM_AST");
+                const int64_t tiles_m2 = (m + BM2 - 1) / BM2, tiles_n2 = (n + BN2 - 1) / BN2;
+                if constexpr (ES == 1) {
+                    const bool force = ea && ea[0] == '1';  // tests: any shape it can run
+                    if (lean && ew8 && !a_mn && p.num_kb <= 4 && !(ea && ea[0] == '0') &&
+                        (force || (tiles_n2 >= 2 && tiles_m2 >= 4 * (num_sms / 2))))
+                    {
+                        const char* ee = getenv("FP8B_GEMM_AST_EW");
+                        if (ee && ee[0] == '8')
+                            return launch_2sm_ast<ES, 8, 2, 1, 4>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+                        return launch_2sm_ast<ES, 16, 1, 1, 4>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+                    }
+                }
                 if (lean)
                     return ew8 ? launch_2sm<ES, 1, 8, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st)
                                : launch_2sm<ES, 1, 4, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);

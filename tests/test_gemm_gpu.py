@@ -292,3 +292,41 @@ def test_lean_codes_only_exact_grid(fp8, nb_env, m, k, n, nb):
     np.testing.assert_array_equal(cq.cpu().numpy(), codes.astype(np.uint8))
     assert cnt.values() == tuple(int(v) for v in k_)
     assert k_[0] > 0 and k_[1] > 0 and k_[2] > 0
+
+
+@pytest.mark.parametrize("b_major", ["n", "k"])
+@pytest.mark.parametrize("m,k,n", [(40000, 320, 1000), (5000, 512, 256)])
+def test_astat_codes_exact_grid(fp8, nb_env, b_major, m, k, n):
+    """The A-stationary short-K pair kernel (resident A k-blocks, B-only ring;
+    forced with FP8B_GEMM_AST=1): ragged M / N / K, several M blocks per cluster,
+    both B layouts; codes and counters equal Q_RNE of the exact result, with
+    overflow / underflow / NaN bias columns."""
+    import torch
+    old = os.environ.get("FP8B_GEMM_AST")
+    os.environ["FP8B_GEMM_AST"] = "1"
+    try:
+        rng = np.random.default_rng(91)
+        A = O.quantize((rng.integers(-2, 3, m * k) * 0.5).astype(np.float32))[0].reshape(m, k)
+        B = O.quantize((rng.integers(-2, 3, k * n) * 0.25).astype(np.float32))[0].reshape(k, n)
+        B[:, 5::97] = 0
+        bias = (rng.integers(-8, 8, n) * 0.125).astype(np.float32)
+        bias[3::61] = 60000.0
+        bias[5::97] = 1e-6
+        bias[7::211] = np.nan
+        bdev = B if b_major == "n" else np.ascontiguousarray(B.T)
+        cnt = fp8.Counters()
+        _, cq = fp8.gemm_codes(_codes_dev(A, "fp8"), _codes_dev(bdev, "fp8"), m, n, k, "fp8",
+                               b_major=b_major, engine="tensor", want_c=False,
+                               bias=torch.from_numpy(bias).cuda(), out_fmt="fp8",
+                               out_mode="nearest-even", out_counters=cnt)
+        da = O.dequantize(A).astype(np.float64).reshape(m, k)
+        db = O.dequantize(B).astype(np.float64).reshape(k, n)
+        y = ((da @ db).astype(np.float32) + bias[None, :]).astype(np.float32)
+        codes, k_ = O.quantize(y, "fp8", "nearest-even", 1)
+        np.testing.assert_array_equal(cq.cpu().numpy().reshape(-1), codes.astype(np.uint8).reshape(-1))
+        assert cnt.values() == tuple(int(v) for v in k_)
+    finally:
+        if old is None:
+            os.environ.pop("FP8B_GEMM_AST", None)
+        else:
+            os.environ["FP8B_GEMM_AST"] = old

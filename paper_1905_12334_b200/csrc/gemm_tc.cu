@@ -254,7 +254,10 @@ struct Geo2 {
     // of its M block; the ring stages then carry B only.
     static constexpr uint32_t RING_OFF = (uint32_t)AST * A2_BYTES;
     static constexpr uint32_t STAGE = AST ? B_BYTES : A2_BYTES + B_BYTES;
-    static constexpr uint32_t EPI = (uint32_t)EW * NBUF * 4096;
+    // staging buffer per epilogue warp: 4 KB, or 2 KB for the A-stationary
+    // 16-warp epilogue (32 rows x 64 code bytes per store), two more B stages
+    static constexpr uint32_t BUF = (AST && EW == 16) ? 2048u : 4096u;
+    static constexpr uint32_t EPI = (uint32_t)EW * NBUF * BUF;
     static constexpr int FIT = (int)((232448u - RING_OFF - EPI - 1536u) / STAGE);
     static constexpr int CAP = AST ? 8 : 6;
     static constexpr int STAGES = FIT < CAP ? FIT : CAP;
@@ -293,6 +296,13 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* tm, void* dst
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_leader), "r"(c0), "r"(c1)
         : "memory");
+}
+// L2 prefetch of a 2-D box (no shared memory, no barrier).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* tm, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
 }
 template <int ES>
 __device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
@@ -400,15 +410,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                                                ~uintptr_t(1023));
     using G = Geo2<NB, EW, NBUF, AST>;
     static_assert(AST == 0 || NB == 1, "A-stationary runs the 256x256 pair tile");
+    static_assert(G::BUF == 4096 || (LEAN && NBUF == 1), "2 KB staging holds one 32x64 code box");
     constexpr uint32_t STAGE2_BYTES = G::STAGE;
     uint8_t* const ring = smem + G::RING_OFF;
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + G::EPI_OFF + G::EPI);
     uint64_t* empty_bar = full_bar + G::STAGES;
     uint64_t* tfull_bar = empty_bar + G::STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint64_t* afull_bar = tempty_bar + 2;   // AST: resident A loaded (leader CTA)
-    uint64_t* aempty_bar = afull_bar + 1;   // AST: the M block's last MMAs done (both CTAs)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty_bar + 1);
+    // AST, per resident k-block: loaded (leader CTA) / the M block's last MMAs
+    // reading it are done (both CTAs), so the next M block's k-block kb reloads
+    // while the last tile's later k-blocks still run
+    uint64_t* afull_bar = tempty_bar + 2;
+    uint64_t* aempty_bar = afull_bar + (AST ? AST : 1);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty_bar + (AST ? AST : 1));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -447,8 +461,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
             mbar_init(tfull_bar + a, 1);
             mbar_init(tempty_bar + a, 2 * EW);  // EW epilogue warps x 2 CTAs
         }
-        mbar_init(afull_bar, 1);
-        mbar_init(aempty_bar, 1);
+        for (int a = 0; a < (AST ? AST : 1); ++a) {
+            mbar_init(afull_bar + a, 1);
+            mbar_init(aempty_bar + a, 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -474,12 +490,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                 const int32_t m0 = tm * BM2 + (int32_t)rank * 128, n0 = tn * G::TN + (int32_t)rank * 128;
                 if (AST) {
                     if (tn == 0) {  // a new M block: its A rows, all k-blocks, once
-                        mbar_wait(aempty_bar, aphase ^ 1);
-                        const uint32_t fa = mapa_u32(smem_u32(afull_bar), 0);
-                        if (rank == 0) mbar_expect_tx(afull_bar, 2u * (uint32_t)p.num_kb * A2_BYTES);
-                        for (int kb = 0; kb < p.num_kb; ++kb)
+                        for (int kb = 0; kb < p.num_kb; ++kb) {
+                            mbar_wait(aempty_bar + kb, aphase ^ 1);
+                            const uint32_t fa = mapa_u32(smem_u32(afull_bar + kb), 0);
+                            if (rank == 0) mbar_expect_tx(afull_bar + kb, 2u * A2_BYTES);
                             tma_load_2d_2sm(&tmA, smem + kb * A2_BYTES, fa, kb * BKE, m0);
+                        }
                         aphase ^= 1;
+                        // warm L2 with the next M block's A rows (read at the next switch)
+                        if (tm + nclusters < p.tiles_m)
+                            for (int kb = 0; kb < p.num_kb; ++kb)
+                                tma_prefetch_2d(&tmA, kb * BKE, m0 + nclusters * BM2);
                     }
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(empty_bar + stage, phase ^ 1);
@@ -545,15 +566,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
             }
         }
     } else if (warp == 1) {
-        if (rank == 0 && lane == 0) {
-            // One lane issues. Descriptors are precomputed once (stage 0 /
-            // k-step 0) and advanced by adding the byte offset >> 4 to their
+        if (rank == 0) {
+            // The whole warp runs the issue loop in uniform control flow, so the
+            // descriptors live in uniform registers; one elected lane issues.
+            // Descriptors are precomputed once (stage 0 / k-step 0) and advanced by adding the byte offset >> 4 to their
             // 14-bit address field, instead of being rebuilt per MMA with
             // runtime layout selects (~25 instructions per MMA before); the
             // issuer shares its SM sub-partition with epilogue warps, and its
             // issue rate is what the tensor pipe waits on
             // (profiles/ncu_gemm_epi_r01.md).
-            const uint32_t leader = 1u;
+            uint32_t leader;
+            asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(leader));
             uint32_t idesc = (1u << 4);
             if (ES == 1) idesc |= (1u << 7) | (1u << 10);
             if (ES == 1 && (p.dbg & 256)) idesc &= ~(7u << 7);  // diagnostic: A read as E4M3
@@ -605,26 +628,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                 item_of(item, tm, tn, s, kb0, kb1);
                 if (AST) {
                     if (tm >= p.tiles_m) continue;
-                    if (tn == 0) {
-                        mbar_wait(afull_bar, aphase);
-                        fence_after();
-                    }
                     mbar_wait(tempty_bar + acc, accphase ^ 1);
                     fence_after();
                     const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
+                    const bool last_n = tn == p.tiles_n - 1;
                     for (int kb = kb0; kb < kb1; ++kb) {
+                        if (tn == 0) mbar_wait(afull_bar + kb, aphase);
                         mbar_wait(full_bar + stage, phase);
                         fence_after();
                         issue_kb(stage, d_tmem, 0, false, kb == kb0, kb);
                         umma_commit_mc_p(empty_bar + stage, leader);
+                        // the M block's k-block kb may be replaced
+                        if (last_n) umma_commit_mc_p(aempty_bar + kb, leader);
                         if (++stage == nst2) { stage = 0; phase ^= 1; }
                     }
                     umma_commit_mc_p(tfull_bar + acc, leader);
                     if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
-                    if (tn == p.tiles_n - 1) {  // the M block's A may be replaced
-                        umma_commit_mc_p(aempty_bar, leader);
-                        aphase ^= 1;
-                    }
+                    if (last_n) aphase ^= 1;
                     continue;
                 }
                 mbar_wait(tempty_bar + acc, accphase ^ 1);
@@ -650,7 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(full_bar + stage, phase);
                         fence_after();
-                        if (!hi_free && mbar_test(tempty_bar + 1, accphase ^ 1)) {
+                        if (!hi_free && __shfl_sync(0xFFFFFFFFu, (int)mbar_test(tempty_bar + 1, accphase ^ 1), 0)) {
                             hi_free = true;
                             fence_after();
                             flush();
@@ -695,7 +715,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
         const int quarter = warp & 3;            // TMEM lane quarter this warp may read
         const int ehalf = (warp - 2) >> 2;       // EW = 8 / 16: which half / quarter of each 256-column block
         constexpr int PERB = 8 / (EW / 4);       // chunks per 256-column block per warp
-        uint8_t* sbuf = smem + G::EPI_OFF + (warp - 2) * (NBUF * 4096);
+        uint8_t* sbuf = smem + G::EPI_OFF + (warp - 2) * (NBUF * G::BUF);
         uint32_t nst = 0;
         int acc = 0;
         uint32_t accphase = 0;

@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // whole warp in uniform control flow; one elected lane issues
+            const uint32_t leader = elect_one();
             uint32_t idesc = (1u << 4);
             if (ES == 1) idesc |= (1u << 7) | (1u << 10);
             if (MODE == 1) idesc |= (1u << 15) | (1u << 16);  // A and B MN-major
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
                         for (int k = 0; k < CB / 32; ++k) {
                             const uint64_t ad = umma_desc(a_base + 32 * k, 16, G::SBO, G::SWZ_LAYOUT);
                             const uint64_t bd = umma_desc(b_base + 32 * k, 16, G::SBO, G::SWZ_LAYOUT);
-                            mma<ES>(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u);
+                            mma_p<ES>(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u, leader);
                         }
                     } else {
 #pragma unroll
@@ -248,13 +249,13 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
                             const uint64_t ad = umma_desc(a_base + k * UK * 128, G::KPIX * 128, 1024);
                             const uint64_t bd = umma_desc(b_base + k * UK * CB, G::KPIX * CB, G::SBO,
                                                           G::SWZ_LAYOUT);
-                            mma<ES>(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u);
+                            mma_p<ES>(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u, leader);
                         }
                     }
-                    umma_commit(empty_bar + stage);
+                    umma_commit_p(empty_bar + stage, leader);
                     if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
                 }
-                umma_commit(tfull_bar + acc);
+                umma_commit_p(tfull_bar + acc, leader);
                 if (++acc == 2) { acc = 0; accphase ^= 1; }
             }
         }

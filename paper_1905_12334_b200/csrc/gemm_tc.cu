@@ -356,14 +356,6 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar) {
         "h"((uint16_t)3)
         : "memory");
 }
-// One lane of the warp (elect.sync): 1 there, 0 elsewhere.
-__device__ __forceinline__ uint32_t elect_one() {
-    uint32_t r;
-    asm volatile(
-        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
-        : "=r"(r));
-    return r;
-}
 // tcgen05.mma.cta_group::2 issued only where `issue` != 0 (warp-uniform callers).
 // CU: 0 = none, 1 = collector::a::fill, 2 = collector::a::lastuse
 template <int ES, int CU>
@@ -575,8 +567,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
             // issuer shares its SM sub-partition with epilogue warps, and its
             // issue rate is what the tensor pipe waits on
             // (profiles/ncu_gemm_epi_r01.md).
-            uint32_t leader;
-            asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(leader));
+            const uint32_t leader = elect_one();
             uint32_t idesc = (1u << 4);
             if (ES == 1) idesc |= (1u << 7) | (1u << 10);
             if (ES == 1 && (p.dbg & 256)) idesc &= ~(7u << 7);  // diagnostic: A read as E4M3

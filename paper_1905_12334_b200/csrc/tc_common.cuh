@@ -117,6 +117,38 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t ad, uint64_t bd, u
     }
 }
 
+// Predicated forms for an issue loop run by the whole warp (operands uniform,
+// one elected lane issuing).
+template <int ES>
+__device__ __forceinline__ void mma_p(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                      uint32_t accum, uint32_t issue) {
+    if (ES == 1) {
+        asm volatile(
+            "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
+            "@q tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(accum), "r"(issue));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
+            "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(accum), "r"(issue));
+    }
+}
+__device__ __forceinline__ void umma_commit_p(uint64_t* bar, uint32_t issue) {
+    asm volatile(
+        "{\n.reg .pred q;\nsetp.ne.b32 q, %1, 0;\n"
+        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(issue)
+        : "memory");
+}
+// One lane of the warp (elect.sync): 1 there, 0 elsewhere.
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t e;
+    asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(e));
+    return e;
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))

@@ -322,7 +322,7 @@ __device__ __forceinline__ void stage_codes(EpiTma* t, const uint32_t* w, int64_
 //   m >= 0x7B  <=>  bit 7 of m + 5: the max-normal code (possibly from an input
 //                   above 57344, which the reference overflows), Inf or NaN ->
 //                   per-element fix-ups (rare);
-//   m == 0     <=>  bit 7 of (m | 0x80) - 1 clear: the code rounded to zero; an
+//   m == 0     <=>  bit 7 of m + 0x7F clear: the code rounded to zero; an
 //                   underflow unless the input was +-0.
 // Counters cover real rows (live) and columns (< nvalid) only.
 __device__ __forceinline__ void lean_e5m2_codes(const float (&y)[32], uint32_t (&w)[8], bool sat,
@@ -334,12 +334,21 @@ __device__ __forceinline__ void lean_e5m2_codes(const float (&y)[32], uint32_t (
         const uint32_t hi = cvt_e5m2x2(y[4 * q + 2], y[4 * q + 3]);
         w[q] = __byte_perm(lo, hi, 0x5410);
     }
+    // one screen for both: bit 7 of m + 5 is set iff m >= 0x7B, bit 7 of m + 0x7F
+    // is clear iff m == 0 (no carries between bytes: m <= 0x7F); 4 ops per word
+    uint32_t flag = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t m = w[q] & 0x7F7F7F7Fu;
+        flag |= (m + 0x05050505u) | ~(m + 0x7F7F7F7Fu);
+    }
+    if (!(flag & 0x80808080u)) return;
     uint32_t big = 0, zero = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const uint32_t m = w[q] & 0x7F7F7F7Fu;
         big |= (m + 0x05050505u) & 0x80808080u;
-        zero |= ~((m | 0x80808080u) - 0x01010101u) & 0x80808080u;
+        zero |= ~(m + 0x7F7F7F7Fu) & 0x80808080u;
     }
     if (big) {  // an output at the max code, overflowing or NaN in this row chunk
 #pragma unroll

@@ -741,12 +741,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
 #pragma unroll 1
                 for (int b = 0; b < NB; ++b) {
                     uint32_t w[PERB][8];
+                    // LDP chunks' TMEM loads in flight before one wait
+                    constexpr int LDP = PERB >= 4 ? 2 : 1;
 #pragma unroll
-                    for (int j = 0; j < PERB; ++j) {
+                    for (int j0 = 0; j0 < PERB; j0 += LDP) {
+                      uint32_t vv[LDP][32];
+#pragma unroll
+                      for (int q = 0; q < LDP; ++q)
+                          tmem_ld32_nowait(taddr + (b * 8 + ehalf * PERB + j0 + q) * 32, vv[q]);
+                      tmem_wait_ld();
+#pragma unroll
+                      for (int q = 0; q < LDP; ++q) {
+                        const int j = j0 + q;
                         const int c = b * 8 + ehalf * PERB + j;
                         const int64_t col0 = (int64_t)tn * G::TN + c * 32;
-                        uint32_t v[32];
-                        tmem_ld32(taddr + c * 32, v);
+                        uint32_t (&v)[32] = vv[q];
+                        tmem_regs_after_wait(v);
                         float y[32];
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) y[jj] = __uint_as_float(v[jj]);
@@ -757,6 +767,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                         }
                         const int nvalid = col0 >= p.N ? 0 : (col0 + 32 <= p.N ? 32 : (int)(p.N - col0));
                         lean_e5m2_codes(y, w[j], p.ep.cq_sat != 0, live, nvalid, co, cu, cn);
+                      }
                     }
                     if (b == NB - 1 || split_rel) {
                         fence_before();

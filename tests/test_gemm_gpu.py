@@ -330,3 +330,36 @@ def test_astat_codes_exact_grid(fp8, nb_env, b_major, m, k, n):
             os.environ.pop("FP8B_GEMM_AST", None)
         else:
             os.environ["FP8B_GEMM_AST"] = old
+
+
+@pytest.mark.parametrize("n,b_major", [(2048, "n"), (1536, "k"), (32000, "n")])
+def test_astat_equals_streaming_at_config5_size(fp8, n, b_major):
+    """Config-5 fprop shapes at full size (2^20 tokens x 512 -> n): the
+    A-stationary kernel and the streaming pair kernel issue the same MMAs in the
+    same K order, so codes and counters must be identical bit for bit."""
+    import torch
+    T, k = 1 << 20, 512
+    if n == 32000:
+        T = 1 << 17  # 4 GB of output codes per run otherwise
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    a = torch.randint(0, 256, (T * k,), dtype=torch.uint8, device="cuda", generator=g)
+    a[(a & 0x7F) >= 0x7C] = 0x3C  # finite codes only
+    b = torch.randint(0, 0x40, (k * n,), dtype=torch.uint8, device="cuda", generator=g)
+    b |= (torch.randint(0, 2, (k * n,), dtype=torch.uint8, device="cuda", generator=g) << 7)
+    outs = []
+    old = os.environ.get("FP8B_GEMM_AST")
+    try:
+        for mode in ("2", "0"):  # default selection (A-stationary here), streaming
+            os.environ["FP8B_GEMM_AST"] = mode
+            cnt = fp8.Counters()
+            _, cq = fp8.gemm_codes(a, b, T, n, k, "fp8", b_major=b_major, engine="tensor",
+                                   want_c=False, out_fmt="fp8", out_counters=cnt)
+            outs.append((cq, cnt.values()))
+    finally:
+        if old is None:
+            os.environ.pop("FP8B_GEMM_AST", None)
+        else:
+            os.environ["FP8B_GEMM_AST"] = old
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]

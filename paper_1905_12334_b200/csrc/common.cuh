@@ -267,8 +267,10 @@ __device__ __forceinline__ void flush_counters(uint32_t c0, uint32_t c1, uint32_
     __syncthreads();
     if (threadIdx.x < 3) {
         unsigned long long s = 0;
+        const int nw = (int)(blockDim.x >> 5);  // <= NT / 32 (launch bound)
 #pragma unroll
-        for (int i = 0; i < NT / 32; ++i) s += red[threadIdx.x][i];
+        for (int i = 0; i < NT / 32; ++i)
+            if (i < nw) s += red[threadIdx.x][i];
         if (s) atomicAdd(reinterpret_cast<unsigned long long*>(counters) + threadIdx.x, s);
     }
 }

@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
     const uint32_t special_code = special_packed<MB>(sat);
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * kWarpLfsrThreads + threadIdx.x) >> 5;
-    const int64_t wstride = ((int64_t)gridDim.x * kWarpLfsrThreads) >> 5;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     if (threadIdx.x == 0) {
         mbar_init(&tab_bar, 1);
         mbar_fence_init();
@@ -516,10 +516,13 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
                 int num_sms = 0, dev = 0;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+                // one warp per 4096-block, spread over every SM for small tensors
                 int64_t g = num_sms;
-                const int64_t need = (nfull + kWarpLfsrThreads / 32 - 1) / (kWarpLfsrThreads / 32);
+                int64_t wpc = (nfull + g - 1) / g;
+                if (wpc > kWarpLfsrThreads / 32) wpc = kWarpLfsrThreads / 32;
+                const int64_t need = (nfull + wpc - 1) / wpc;
                 if (need < g) g = need;
-                fn<<<(int)g, kWarpLfsrThreads, smem, st>>>(x, codes, nfull, cfg.seed, cfg.saturate,
+                fn<<<(int)g, (int)(32 * wpc), smem, st>>>(x, codes, nfull, cfg.seed, cfg.saturate,
                                                           cfg.block_offset, tabs, counters);
                 begin = nfull;
             }

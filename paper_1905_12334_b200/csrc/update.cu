@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(kWarpUpdThreads, 1)
     const bool wsat = a.w_sat != 0;
     uint32_t mb = 0, mn = 0, mu_ = 0, wb = 0, wn = 0, wu = 0;
     const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * kWarpUpdThreads + threadIdx.x) >> 5;
-    const int64_t wstride = ((int64_t)gridDim.x * kWarpUpdThreads) >> 5;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     if (threadIdx.x == 0) {
         mbar_init(&tab_bar, 1);
         mbar_fence_init();
@@ -468,10 +468,14 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
             constexpr int smem = kUpdTabBytes;
             auto fn = cnt ? sgd_lfsr_warp_kernel<GFMT, true> : sgd_lfsr_warp_kernel<GFMT, false>;
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            // one warp per 4096-block: a small tensor (config 1: 256 blocks)
+            // spreads its warps over every SM instead of filling a few CTAs
             int64_t g = sm_count();
-            const int64_t need = (nfull + kWarpUpdThreads / 32 - 1) / (kWarpUpdThreads / 32);
+            int64_t wpc = (nfull + g - 1) / g;
+            if (wpc > kWarpUpdThreads / 32) wpc = kWarpUpdThreads / 32;
+            const int64_t need = (nfull + wpc - 1) / wpc;
             if (need < g) g = need;
-            fn<<<(int)g, kWarpUpdThreads, smem, st>>>(grad, master, mom, nfull, a, args.block_offset,
+            fn<<<(int)g, (int)(32 * wpc), smem, st>>>(grad, master, mom, nfull, a, args.block_offset,
                                                       tabs);
             begin = nfull;
         }

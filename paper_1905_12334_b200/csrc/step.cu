@@ -17,6 +17,30 @@ namespace fp8b {
 __global__ void merge_gate_kernel(const int64_t* c, int64_t* gate) {
     if (threadIdx.x < 3) gate[threadIdx.x] = c[threadIdx.x] + c[3 + threadIdx.x];
 }
+
+// Side stream for the step's independent branches (Q(E) beside Q(X) + fprop;
+// bprop beside wgrad): fork / join through events, which CUDA-graph capture
+// turns into parallel graph branches. One set per host thread and device, so
+// concurrent callers on different streams never share events.
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    int dev = -1;
+};
+static SideStream* side_stream() {
+    thread_local SideStream ss[16];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    SideStream& x = ss[dev];
+    if (x.dev != dev) {
+        if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+        x.dev = dev;
+    }
+    return &x;
+}
 }  // namespace fp8b
 
 extern "C" {
@@ -43,6 +67,24 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     rne.mode = FP8B_RNE;
     rne.seed = 1;
     rne.saturate = s->saturate;
+    fp8b::SideStream* ss = fp8b::side_stream();
+    if (!ss) return FP8B_ECUDA;
+    void* side = ss->s;
+    auto fork = [&]() {
+        return cudaEventRecord(ss->fork, st) == cudaSuccess &&
+               cudaStreamWaitEvent(ss->s, ss->fork, 0) == cudaSuccess;
+    };
+    auto join = [&]() {
+        return cudaEventRecord(ss->join, ss->s) == cudaSuccess &&
+               cudaStreamWaitEvent(st, ss->join, 0) == cudaSuccess;
+    };
+    // ---- Q(E) on the side stream, beside the forward (it depends on nothing there)
+    if (!fork()) return FP8B_ECUDA;
+    FP8B_TRY(fp8b_quantize(s->e, s->qe, B * O, FP8B_E5M2, &rne, s->counters, side));
+    if (s->b_master) {
+        FP8B_TRY(fp8b_bias_grad(s->qe, FP8B_E5M2, B, O, s->db, side));
+        FP8B_TRY(fp8b_count_nonfinite(s->db, O, s->counters, side));
+    }
     // ---- forward (nn.cpp:187-203): qx = Q(x); y = qx . w_q (+ b); qy = Q(y)
     if (s->b_master) FP8B_TRY(fp8b_dequantize(s->b_master, s->b_value, O, FP8B_FP16, stream));
     FP8B_TRY(fp8b_quantize(s->x, s->qx, B * I, FP8B_E5M2, &rne, s->fwd_counters, stream));
@@ -59,12 +101,8 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     g.cq = s->qy;
     g.cq_counters = s->fwd_counters;
     FP8B_TRY(fp8b_gemm(s->qx, s->w_q, B, O, I, FP8B_E5M2, &g, stream));
-    // ---- backward (nn.cpp:294-326)
-    FP8B_TRY(fp8b_quantize(s->e, s->qe, B * O, FP8B_E5M2, &rne, s->counters, stream));
-    if (s->b_master) {
-        FP8B_TRY(fp8b_bias_grad(s->qe, FP8B_E5M2, B, O, s->db, stream));
-        FP8B_TRY(fp8b_count_nonfinite(s->db, O, s->counters, stream));
-    }
+    // ---- backward (nn.cpp:294-326); Q(E) ran on the side stream
+    if (!join()) return FP8B_ECUDA;
     // wgrad: dW[I,O] = qx^T . qe  (qx read M-major, qe N-major; no transpose pass)
     g.a_major = FP8B_MN_MAJOR;
     g.b_major = FP8B_MN_MAJOR;
@@ -72,15 +110,19 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     g.bias = nullptr;
     g.cq = s->qdw;
     g.cq_counters = s->counters + 3;
-    FP8B_TRY(fp8b_gemm(s->qx, s->qe, I, O, B, FP8B_E5M2, &g, stream));
-    // bprop: dX[B,I] = qe . w_q^T  (w_q [I,O] read as the K-major [N=I, K=O] operand)
+    // bprop: dX[B,I] = qe . w_q^T  (w_q [I,O] read as the K-major [N=I, K=O]
+    // operand) on the side stream, beside wgrad (both only read qx / qe / w_q)
     if (s->qdx) {
-        g.a_major = FP8B_K_MAJOR;
-        g.b_major = FP8B_K_MAJOR;
-        g.cq = s->qdx;
-        g.cq_counters = s->counters;
-        FP8B_TRY(fp8b_gemm(s->qe, s->w_q, B, I, O, FP8B_E5M2, &g, stream));
+        fp8b_gemm_args_t gb = g;
+        gb.a_major = FP8B_K_MAJOR;
+        gb.b_major = FP8B_K_MAJOR;
+        gb.cq = s->qdx;
+        gb.cq_counters = s->counters;
+        if (!fork()) return FP8B_ECUDA;
+        FP8B_TRY(fp8b_gemm(s->qe, s->w_q, B, I, O, FP8B_E5M2, &gb, side));
     }
+    FP8B_TRY(fp8b_gemm(s->qx, s->qe, I, O, B, FP8B_E5M2, &g, stream));
+    if (s->qdx && !join()) return FP8B_ECUDA;
     // grads_finite gate (nn.cpp:401-411): overflow of qe/qdw/qdx, NaN in qdw, non-finite db
     fp8b::merge_gate_kernel<<<1, 32, 0, st>>>(s->counters, s->gate);
     if (cudaGetLastError() != cudaSuccess) return FP8B_ECUDA;

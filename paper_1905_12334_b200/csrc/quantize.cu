@@ -210,7 +210,16 @@ __device__ __forceinline__ void store4(void* codes, int64_t i0, const uint32_t (
 // a 5-step shuffle scan of the per-lane counts on top of a running count, and
 // reads its samples from the jump table kept in shared memory. The table copy
 // carries the 4096-entry wrap extension, so no modular addressing is needed.
-constexpr int kWarpLfsrThreads = 768;
+// Elements per lane per chunk and CTA size (compile-time knobs). Measured on
+// the B200: 16 per lane at 512 threads is -1.6 % (E5M2) / +1.3 % (FP16), and
+// spills at 768 threads; 8 per lane at 768 threads is the default.
+#ifndef FP8B_LFSR_EPL
+#define FP8B_LFSR_EPL 8
+#endif
+#ifndef FP8B_LFSR_THREADS
+#define FP8B_LFSR_THREADS 768
+#endif
+constexpr int kWarpLfsrThreads = FP8B_LFSR_THREADS;
 
 constexpr int kTabWrapBytes = ((kLfsrPeriod + kBlock) * 2 + 15) & ~15;  // 139264
 template <int MB>
@@ -246,18 +255,26 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
         const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, p0_next, 0);
         if (lane == 0 && b + wstride < nfull)
             p0_next = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + b + wstride)));
-        const float4* xb = reinterpret_cast<const float4*>(x + b * kBlock) + 2 * lane;
+        constexpr int EPL = FP8B_LFSR_EPL;  // consecutive elements per lane per chunk
+        constexpr int NV = EPL / 4;         // float4 loads per lane per chunk
+        constexpr int CH = 32 * EPL;        // chunk size
+        const float4* xb = reinterpret_cast<const float4*>(x + b * kBlock) + NV * lane;
         uint32_t run = stab_addr + 2u * p0;  // table byte address of the chunk's first sample
-        // one 256-element chunk: 8 consecutive elements per lane
-        auto chunk = [&](const float4& va, const float4& vb, int c) {
-            const uint32_t u[8] = {__float_as_uint(va.x), __float_as_uint(va.y), __float_as_uint(va.z),
-                                   __float_as_uint(va.w), __float_as_uint(vb.x), __float_as_uint(vb.y),
-                                   __float_as_uint(vb.z), __float_as_uint(vb.w)};
-            uint32_t P[8], inc[8], n = 0;
+        // one chunk: EPL consecutive elements per lane
+        auto chunk = [&](const float4 (&v)[NV], int c) {
+            uint32_t u[EPL];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                u[4 * q] = __float_as_uint(v[q].x);
+                u[4 * q + 1] = __float_as_uint(v[q].y);
+                u[4 * q + 2] = __float_as_uint(v[q].z);
+                u[4 * q + 3] = __float_as_uint(v[q].w);
+            }
+            uint32_t P[EPL], inc[EPL], n = 0;
             // screen: amax (NaN-propagating) catches overflow / NaN inputs
             float amax = fabsf(__uint_as_float(u[0]));
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < EPL; ++k) {
                 const float f = __uint_as_float(u[k]);
                 if (k) amax = fmax_nan(amax, fabsf(f));
                 P[k] = packed_sr<MB>(f);
@@ -268,7 +285,7 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
             bool has_nan = false;
             if (!(amax <= (MB == 2 ? 57344.0f : 65504.0f))) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
+                for (int k = 0; k < EPL; ++k) {
                     const bool big = big_or_nan<MB>(__uint_as_float(u[k]));
                     c_big += big;
                     has_nan |= (u[k] & 0x7FFFFFFFu) > 0x7F800000u;
@@ -276,7 +293,7 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
                 }
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) n += inc[k];
+            for (int k = 0; k < EPL; ++k) n += inc[k];
             // inclusive warp scan of the lanes' sample bytes
             uint32_t incl = n;
 #pragma unroll
@@ -287,33 +304,43 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
             const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
             uint32_t addr = run + incl - n;
             run += total;
-            uint32_t sum[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < EPL; ++k) {
                 uint32_t r16;
                 asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r16) : "r"(addr));
                 addr += inc[k];
-                sum[k] = P[k] + r16;  // exact lanes ignore their sample
+                P[k] += r16;  // exact lanes ignore their sample
                 // underflow: inexact and rounded to zero; exact lanes pushed out of range
-                const uint32_t chk = sum[k] + (2u - inc[k]) * 0x8000u;
+                const uint32_t chk = P[k] + (2u - inc[k]) * 0x8000u;
                 c_unf += (chk - 0x10000u) >> 31;
             }
-            const int64_t e0 = b * kBlock + 256 * c + 8 * lane;  // first element of this lane
+            const int64_t e0 = b * kBlock + CH * c + EPL * lane;  // first element of this lane
             if (MB == 2) {
-                const uint32_t w0 = gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]);
-                const uint32_t w1 = gather_e5m2(sum[4], sum[5], sum[6], sum[7], u[4], u[5], u[6], u[7]);
-                __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(codes) + e0), make_uint2(w0, w1));
+                uint32_t w[EPL / 4];
+#pragma unroll
+                for (int q = 0; q < EPL / 4; ++q)
+                    w[q] = gather_e5m2(P[4 * q], P[4 * q + 1], P[4 * q + 2], P[4 * q + 3], u[4 * q],
+                                       u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+                uint8_t* dst = reinterpret_cast<uint8_t*>(codes) + e0;
+                if (EPL == 8) __stcs(reinterpret_cast<uint2*>(dst), make_uint2(w[0], w[1]));
+                else
+#pragma unroll
+                    for (int q = 0; q < EPL / 16; ++q)
+                        __stcs(reinterpret_cast<uint4*>(dst) + q,
+                               make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
             } else {
-                const uint32_t w0 = gather_f16(sum[0], sum[1], u[0], u[1]);
-                const uint32_t w1 = gather_f16(sum[2], sum[3], u[2], u[3]);
-                const uint32_t w2 = gather_f16(sum[4], sum[5], u[4], u[5]);
-                const uint32_t w3 = gather_f16(sum[6], sum[7], u[6], u[7]);
-                __stcs(reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(codes) + e0), make_uint4(w0, w1, w2, w3));
+                uint32_t w[EPL / 2];
+#pragma unroll
+                for (int q = 0; q < EPL / 2; ++q) w[q] = gather_f16(P[2 * q], P[2 * q + 1], u[2 * q], u[2 * q + 1]);
+                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(codes) + e0);
+#pragma unroll
+                for (int q = 0; q < EPL / 8; ++q)
+                    __stcs(dst + q, make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
             }
             // rare: NaN among the lane's inputs -> canonical unsigned NaN code (float_format.cpp:99)
             if (has_nan) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < EPL; ++k)
                     if ((u[k] & 0x7FFFFFFFu) > 0x7F800000u) {
                         ++c_nan;
                         if (MB == 2) reinterpret_cast<uint8_t*>(codes)[e0 + k] = 0x7E;
@@ -323,16 +350,19 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
         };
         // two register sets in ping-pong, each chunk's loads issued one chunk
         // ahead (no register copies between chunks)
-        float4 a0 = __ldcs(xb), a1 = __ldcs(xb + 1);
+        float4 va[NV], vb[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) va[q] = __ldcs(xb + q);
 #pragma unroll 1
-        for (int c = 0; c < kBlock / 256; c += 2) {
-            const float4 b0 = __ldcs(xb + 64 * (c + 1)), b1 = __ldcs(xb + 64 * (c + 1) + 1);
-            chunk(a0, a1, c);
-            if (c + 2 < kBlock / 256) {
-                a0 = __ldcs(xb + 64 * (c + 2));
-                a1 = __ldcs(xb + 64 * (c + 2) + 1);
+        for (int c = 0; c < kBlock / CH; c += 2) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) vb[q] = __ldcs(xb + (CH / 4) * (c + 1) + q);
+            chunk(va, c);
+            if (c + 2 < kBlock / CH) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) va[q] = __ldcs(xb + (CH / 4) * (c + 2) + q);
             }
-            chunk(b0, b1, c + 1);
+            chunk(vb, c + 1);
         }
     }
     if (counters) flush_counters<kWarpLfsrThreads>(c_big - c_nan, c_unf, c_nan, counters);

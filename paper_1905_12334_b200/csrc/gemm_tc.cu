@@ -732,11 +732,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                       (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane, p.splits > 1 ? s : -1,
                       p.qg, 0, nullptr, NBUF};
             if (lean_q) {
-                // Fused E5M2 RNE output only: a 256-column block is drained and
-                // quantised into registers (8 words per chunk), the accumulator
-                // block is released to the MMA warp, and only then are the codes
-                // stored -- the stores overlap the next tile's MMAs instead of
-                // holding the accumulator.
+                // Fused E5M2 RNE output only: a 256-column block is drained into
+                // registers and quantised (8 words per chunk); the accumulator
+                // block is released to the MMA warp as soon as its last TMEM
+                // loads land, and the codes are stored after -- the stores
+                // overlap the next tile's MMAs instead of holding the accumulator.
                 const bool live = row < p.M;
 #pragma unroll 1
                 for (int b = 0; b < NB; ++b) {
@@ -750,6 +750,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                       for (int q = 0; q < LDP; ++q)
                           tmem_ld32_nowait(taddr + (b * 8 + ehalf * PERB + j0 + q) * 32, vv[q]);
                       tmem_wait_ld();
+                      // the block's last TMEM loads have landed: release it to
+                      // the MMA warp before quantising the last chunks
+                      if (j0 + LDP >= PERB && (b == NB - 1 || split_rel)) {
+                          fence_before();
+                          __syncwarp();
+                          if (lane == 0) mbar_arrive_cluster(te_leader + (split_rel ? b * 8 : acc * 8));
+                      }
 #pragma unroll
                       for (int q = 0; q < LDP; ++q) {
                         const int j = j0 + q;
@@ -768,11 +775,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                         const int nvalid = col0 >= p.N ? 0 : (col0 + 32 <= p.N ? 32 : (int)(p.N - col0));
                         lean_e5m2_codes(y, w[j], p.ep.cq_sat != 0, live, nvalid, co, cu, cn);
                       }
-                    }
-                    if (b == NB - 1 || split_rel) {
-                        fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_cluster(te_leader + (split_rel ? b * 8 : acc * 8));
                     }
 #pragma unroll
                     for (int j = 0; j < PERB; ++j) {

@@ -254,9 +254,9 @@ struct Geo2 {
     // of its M block; the ring stages then carry B only.
     static constexpr uint32_t RING_OFF = (uint32_t)AST * A2_BYTES;
     static constexpr uint32_t STAGE = AST ? B_BYTES : A2_BYTES + B_BYTES;
-    // staging buffer per epilogue warp: 4 KB, or 2 KB for the A-stationary
-    // 16-warp epilogue (32 rows x 64 code bytes per store), two more B stages
-    static constexpr uint32_t BUF = (AST && EW == 16) ? 2048u : 4096u;
+    // staging buffer per epilogue warp: 4 KB, or 2 KB for the 16-warp (codes
+    // only) epilogue: 32 rows x 64 code bytes per store
+    static constexpr uint32_t BUF = EW == 16 ? 2048u : 4096u;
     static constexpr uint32_t EPI = (uint32_t)EW * NBUF * BUF;
     static constexpr int FIT = (int)((232448u - RING_OFF - EPI - 1536u) / STAGE);
     static constexpr int CAP = AST ? 8 : 6;
@@ -977,6 +977,17 @@ static int pick_nb(int64_t m, int64_t n, int num_kb, int clusters) {
     return c2 < c1 ? 2 : 1;
 }
 
+// Each epilogue warp stores 256 / (EW / 4) columns of a 256-column block: with
+// 16 warps (64 columns each) the code store boxes are 64 columns wide.
+template <int EW>
+static void code_boxes_for_ew(Params& p2, CUtensorMap& tq2, const Params& p, int64_t m, int64_t n) {
+    constexpr int cols_per_warp = 256 / (EW / 4);
+    if (p2.q_tma && cols_per_warp < 128) {
+        p2.qg = code_group(p.ep.cq_fmt, cols_per_warp);
+        if (!make_q_map(&tq2, p.ep.cq, p.ep.cq_fmt, m, n, cols_per_warp)) p2.q_tma = 0;
+    }
+}
+
 // A-stationary pair kernel (short K, many M blocks, several N tiles): A is read
 // into shared memory once per M block instead of once per tile, halving the
 // L2 -> SMEM operand stream that bounds short-K shapes.
@@ -994,13 +1005,8 @@ static int launch_2sm_ast(const CUtensorMap& tA2, const CUtensorMap& tB2, const 
     p2.tiles_m = (int)((m + BM2 - 1) / BM2);
     p2.tiles_n = (int)((n + G::TN - 1) / G::TN);
     p2.splits = 1;
-    // each epilogue warp stores 256 / (EW / 4) columns of a tile: code boxes of that width
     CUtensorMap tq2 = tmQ;
-    constexpr int cols_per_warp = 256 / (EW / 4);
-    if (p2.q_tma && cols_per_warp < 128) {
-        p2.qg = code_group(p.ep.cq_fmt, cols_per_warp);
-        if (!make_q_map(&tq2, p.ep.cq, p.ep.cq_fmt, m, n, cols_per_warp)) p2.q_tma = 0;
-    }
+    code_boxes_for_ew<EW>(p2, tq2, p, m, n);
     int grid2 = 2 * p2.tiles_m;
     const int maxg = num_sms & ~1;
     if (grid2 > maxg) grid2 = maxg;
@@ -1014,18 +1020,20 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
                       cudaStream_t st) {
     using G = Geo2<NB, EW, NBUF>;
     static std::once_flag once;
+    static_assert(EW != 16 || LEAN, "16 epilogue warps: codes-only (LEAN) kernels");
     std::call_once(once, [] {
         cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF, 0>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        if constexpr (EW != 16)
+            cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF, 0>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     });
     Params p2 = p;
     p2.tiles_m = (int)((m + BM2 - 1) / BM2);
     p2.tiles_n = (int)((n + G::TN - 1) / G::TN);
     const int ntiles2 = p2.tiles_m * p2.tiles_n;
     const int maxg = num_sms & ~1;
-    const int splits = use_epi_tma() ? choose_splits(ntiles2, maxg / 2, p.num_kb, m * n, ES, NB) : 1;
+    const int splits = (EW != 16 && use_epi_tma()) ? choose_splits(ntiles2, maxg / 2, p.num_kb, m * n, ES, NB) : 1;
     float* ws = nullptr;
     CUtensorMap tmW;
     if (splits > 1) {
@@ -1038,7 +1046,7 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
             ws = nullptr;
         }
     }
-    if (ws) {
+    if constexpr (EW != 16) if (ws) {
         Params pk = p2;
         pk.splits = splits;
         pk.c_tma = 1;
@@ -1058,7 +1066,9 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
     }
     int grid2 = 2 * ntiles2;
     if (grid2 > maxg) grid2 = maxg;
-    gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tmQ, p2);
+    CUtensorMap tq2 = tmQ;
+    code_boxes_for_ew<EW>(p2, tq2, p, m, n);
+    gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tq2, p2);
     return FP8B_OK;
 }
 
@@ -1158,7 +1168,12 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
                 return launch_2sm<ES, 2, 8, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
             if (ev && ev[0] == '4')
                 return launch_2sm<ES, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
-            if (lean) return launch_2sm<ES, 2, 8, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+            // codes only: 16 epilogue warps (64 columns each, 2 KB staging) drain
+            // the lo half sooner; cooled interleaved A/B vs 8 warps: 8192^3
+            // 0.3575 vs ~0.359 ms, 16384^3 2.828 vs 2.843 ms, 4096^3 equal
+            if (lean && ev && ev[0] == '8')
+                return launch_2sm<ES, 2, 8, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
+            if (lean) return launch_2sm<ES, 2, 16, 1, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
             return launch_2sm<ES, 2, 8, 2>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
         }
     }

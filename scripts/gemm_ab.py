@@ -57,11 +57,17 @@ def timed(fn, reps=20):
 
 res = {lab: [] for lab, _ in variants}
 res["cublas"] = []
-for rnd in range(5):
+import time  # noqa: E402
+ROUNDS = int(os.environ.get("AB_ROUNDS", "5"))
+REPS = int(os.environ.get("AB_REPS", "20"))
+COOL = float(os.environ.get("AB_SLEEP", "0"))  # seconds idle before each timing (power state)
+for rnd in range(ROUNDS):
     for lab, spec in variants:
-        res[lab].append(timed(lambda: run_ours(spec)))
+        time.sleep(COOL)
+        res[lab].append(timed(lambda: run_ours(spec), REPS))
+    time.sleep(COOL)
     res["cublas"].append(timed(lambda: torch._scaled_mm(a8, b8.t(), scale_a=one, scale_b=one,
-                                                        out_dtype=torch.bfloat16)))
+                                                        out_dtype=torch.bfloat16), REPS))
 base = statistics.median(res["cublas"])
 for lab, v in res.items():
     md = statistics.median(v)

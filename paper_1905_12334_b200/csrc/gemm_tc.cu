@@ -1155,6 +1155,7 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
                         return launch_2sm_ast<ES, 16, 1, 1, 4>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
                     }
                 }
+                // (16 warps measured slower here: 1M x 512 x 1536 0.698 -> 0.707 ms)
                 if (lean)
                     return ew8 ? launch_2sm<ES, 1, 8, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st)
                                : launch_2sm<ES, 1, 4, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);

@@ -7,6 +7,9 @@ import paper_1905_12334_b200 as F
 
 variants = [v.split("=", 1) for v in sys.argv[1:]]  # label=ENVSPEC (k:v,k:v)
 m = n = k = int(os.environ.get("AB_N", "8192"))
+m = int(os.environ.get("AB_M", m))
+n = int(os.environ.get("AB_NN", n))
+k = int(os.environ.get("AB_K", k))
 F.init()
 x = torch.empty(m * k + k * n, dtype=torch.float32, device="cuda")
 F.fill_synthetic(x, "normal", 3, 1.0)

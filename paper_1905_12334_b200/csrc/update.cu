@@ -200,7 +200,14 @@ __global__ void __launch_bounds__(NT, MINB) sgd_elem_kernel(const void* __restri
 // on top of a running count -- no CTA barrier. Samples come from the
 // wrap-extended jump table in shared memory; exact lanes add their sample to a
 // zero remainder, which never carries, so no select is needed.
-constexpr int kWarpUpdThreads = 512;
+// CTA size = the SM's warp count (the 139 KB table allows one CTA per SM).
+// The kernel is latency-bound: A/B on one box, 512 -> 768 threads took the LFSR
+// SR master 5.59 -> 6.02 TB/s (with the fused E5M2 W 5.46 -> 5.95); 640 gave
+// 5.98, and 1024 (64 registers) spills and gave 5.65.
+#ifndef FP8B_UPD_THREADS
+#define FP8B_UPD_THREADS 768
+#endif
+constexpr int kWarpUpdThreads = FP8B_UPD_THREADS;
 constexpr int kUpdTabBytes = ((kLfsrPeriod + kBlock) * 2 + 15) & ~15;
 template <int GFMT, bool CNT>
 __global__ void __launch_bounds__(kWarpUpdThreads, 1)

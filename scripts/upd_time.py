@@ -10,7 +10,9 @@ master = torch.randint(0, 0x3C00, (n,), dtype=torch.int16, device="cuda")
 mom = torch.zeros(n, dtype=torch.float32, device="cuda")
 w8 = torch.empty(n, dtype=torch.uint8, device="cuda")
 res = []
-for md, kw, bpe in [("rne", dict(master_mode="nearest-even"), 13),
+for md, kw, bpe in [("lfsr", dict(master_mode="stochastic", bits="lfsr", seed=1), 13),
+                    ("lfsr_w8", dict(master_mode="stochastic", bits="lfsr", seed=1, w_e5m2=w8), 14),
+                    ("rne", dict(master_mode="nearest-even"), 13),
                     ("counter", dict(master_mode="stochastic", bits="counter", seed=1), 13),
                     ("counter_w8", dict(master_mode="stochastic", bits="counter", seed=1, w_e5m2=w8), 14),
                     ("rne_w8", dict(master_mode="nearest-even", w_e5m2=w8), 14)]:

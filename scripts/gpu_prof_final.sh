@@ -15,9 +15,10 @@ cap lfsr quant_lfsr_warp_kernel python scripts/prof.py lfsr 3
 cap fp16ctr quant_elem_kernel python scripts/prof.py fp16ctr 3
 cap gemm_e5m2 gemm_tc2 python scripts/prof.py gemm_e5m2 3
 cap gemm_ast gemm_tc2 python scripts/gemm_one.py ours_q 1048576 2048 512
+cap upd_lfsr sgd_lfsr_warp_kernel python scripts/prof.py upd_lfsr 3
 bash scripts/gpu_launches.sh
 # summaries on the box (the reports themselves exceed gpurun's copy-back limit)
-for name in lfsr fp16ctr gemm_e5m2 gemm_ast; do
+for name in lfsr fp16ctr gemm_e5m2 gemm_ast upd_lfsr; do
   [ -f gpurun_out/prof_$name.ncu-rep ] || continue
   python scripts/summarize_ncu.py report gpurun_out/prof_$name.ncu-rep gpurun_out/ncu_${name}_r01.md > /dev/null 2>&1
   $NCU -i gpurun_out/prof_$name.ncu-rep --page source --csv --print-source sass > gpurun_out/src_$name.csv 2>/dev/null

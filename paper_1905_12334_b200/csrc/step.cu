@@ -27,12 +27,18 @@ struct SideStream {
     cudaEvent_t fork = nullptr, join = nullptr;
     int dev = -1;
 };
-static SideStream* side_stream() {
+// nullptr -> run both branches on the caller's stream (no fork). That is also
+// the path when the first call of a thread is inside a stream capture, where
+// creating the stream / events is not allowed.
+static SideStream* side_stream(cudaStream_t caller) {
     thread_local SideStream ss[16];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
     SideStream& x = ss[dev];
     if (x.dev != dev) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(caller, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+            return nullptr;
         if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess)
@@ -67,16 +73,15 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     rne.mode = FP8B_RNE;
     rne.seed = 1;
     rne.saturate = s->saturate;
-    fp8b::SideStream* ss = fp8b::side_stream();
-    if (!ss) return FP8B_ECUDA;
-    void* side = ss->s;
+    fp8b::SideStream* ss = fp8b::side_stream(st);
+    void* side = ss ? (void*)ss->s : stream;
     auto fork = [&]() {
-        return cudaEventRecord(ss->fork, st) == cudaSuccess &&
-               cudaStreamWaitEvent(ss->s, ss->fork, 0) == cudaSuccess;
+        return !ss || (cudaEventRecord(ss->fork, st) == cudaSuccess &&
+                       cudaStreamWaitEvent(ss->s, ss->fork, 0) == cudaSuccess);
     };
     auto join = [&]() {
-        return cudaEventRecord(ss->join, ss->s) == cudaSuccess &&
-               cudaStreamWaitEvent(st, ss->join, 0) == cudaSuccess;
+        return !ss || (cudaEventRecord(ss->join, ss->s) == cudaSuccess &&
+                       cudaStreamWaitEvent(st, ss->join, 0) == cudaSuccess);
     };
     // ---- Q(E) on the side stream, beside the forward (it depends on nothing there)
     if (!fork()) return FP8B_ECUDA;

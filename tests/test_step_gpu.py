@@ -201,3 +201,37 @@ def test_checkpoint_resume_is_exact(fp8, inputs, tmp_path):
     assert torch.equal(A.w_master, B.w_master) and torch.equal(A.w_momentum, B.w_momentum)
     assert torch.equal(A.b_master, B.b_master) and torch.equal(A.w_q, B.w_q)
     assert sa.scale == sb.scale
+
+
+def test_step_first_call_inside_capture(fp8, inputs):
+    """A host thread whose first step is captured into a CUDA graph (no side
+    stream may be created during capture) runs both branches on the caller's
+    stream; replays equal eager steps."""
+    import threading
+
+    import torch
+    X, W, E = inputs
+    xs, es = torch.from_numpy(X).cuda(), torch.from_numpy(E).cuda()
+    La = _layer(fp8, W, "tensor", "stochastic")
+    Lb = _layer(fp8, W, "tensor", "stochastic")
+    La.step(xs, es, 0)  # warms the process-wide state (TMA descriptors, LFSR tables)
+    torch.cuda.synchronize()
+    err = []
+
+    def worker():
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                Lb.step(xs, es, 0)
+            g.replay()
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    t = threading.Thread(target=worker)
+    t.start()
+    t.join()
+    assert not err, err
+    assert torch.equal(La.w_master, Lb.w_master) and torch.equal(La.w_q, Lb.w_q)

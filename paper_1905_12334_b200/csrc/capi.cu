@@ -7,7 +7,9 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -102,6 +104,33 @@ bool valid_bits(int32_t b) { return b == FP8B_BITS_LFSR || b == FP8B_BITS_COUNTE
 namespace fp8b {
 void note_launches(int n) { g_launches += n; }
 void set_error(const std::string& msg) { g_err = msg; }
+
+// Per-device launch setup. A process may drive several GPUs (one thread per
+// device, or cudaSetDevice between calls), and both the SM count and the
+// >48 KB dynamic shared memory opt-in belong to the current device's context.
+static std::mutex g_dev_mu;
+int device_sm_count() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+    static std::map<int, int> sms;
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = sms.find(dev);
+    if (it != sms.end()) return it->second;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1)
+        return 1;
+    sms[dev] = v;
+    return v;
+}
+void ensure_smem_attr(const void* fn, int bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (done.count({fn, dev})) return;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
+        done.insert({fn, dev});
+}
 }  // namespace fp8b
 
 extern "C" {

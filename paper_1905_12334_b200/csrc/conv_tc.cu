@@ -368,26 +368,13 @@ static bool make_ws_map(CUtensorMap* tm, float* ws, int splits, int64_t m, int64
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int num_sms() {
-    static int v = 0;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    });
-    return v;
-}
+static int num_sms() { return device_sm_count(); }
 
 template <int ES, int MODE, int BN, int CB, int EW = 4>
 static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm,
                const CUtensorMap& tqm, const CParams& p, cudaStream_t st) {
     using G = Geo<ES, MODE, BN, CB, EW>;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(conv_tc_kernel<ES, MODE, BN, CB, EW>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    });
+    ensure_smem_attr((const void*)conv_tc_kernel<ES, MODE, BN, CB, EW>, G::SMEM);
     const int items = p.tiles_m * p.tiles_n * p.splits;
     const int grid = items < num_sms() ? items : num_sms();
     conv_tc_kernel<ES, MODE, BN, CB, EW><<<grid, threads_of<EW>(), G::SMEM, st>>>(ta, tb, tcm, tqm, p);

@@ -1,7 +1,9 @@
 // fp8t_io.cu -- host-side FP8T container I/O (tensor_io.cpp:47-187), the format
 // the reference uses for golden vectors and checkpoints. No device code: the
 // callers move tensors between HBM and these host buffers.
+#include <cstdint>
 #include <cstdio>
+#include <exception>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -57,10 +59,19 @@ int read_header(std::FILE* f, const std::string& path, Header& h) {
         uint64_t v = 0;
         for (int i = 0; i < 8; ++i) v = (v << 8) | b[i];
         d = (int64_t)v;
+        // shape_numel (tensor.cpp:9-16) throws invalid_argument here
+        if (d < 0) return io_fail("negative dimension");
+    }
+    int64_t n = 1;
+    for (int64_t d : h.dims) {
+        if (d != 0 && n > INT64_MAX / 4 / d) return io_fail(path + ": dimension product overflows");
+        n *= d;
     }
     return FP8B_OK;
 }
 
+// Dims are non-negative and their product (times 4 bytes) fits int64: checked
+// by read_header / fp8b_fp8t_save before this is called.
 int64_t numel(const std::vector<int64_t>& dims) {
     int64_t n = 1;
     for (int64_t d : dims) n *= d;
@@ -79,8 +90,13 @@ int fp8b_fp8t_save(const char* path, int32_t dtype, int32_t mode_tag, int32_t ra
         return io_fail(std::string(path) + ": bad rank");
     if (mode_tag < 0 || mode_tag > 3) return io_fail(std::string(path) + ": unknown rounding mode tag");
     std::vector<int64_t> d(dims, dims + rank);
-    for (int64_t v : d)
+    int64_t prod = 1;
+    for (int64_t v : d) {
         if (v < 0) return io_fail(std::string(path) + ": negative dimension");
+        if (v != 0 && prod > INT64_MAX / 4 / v)
+            return io_fail(std::string(path) + ": dimension product overflows");
+        prod *= v;
+    }
     const int64_t n = numel(d);
     if (n > 0 && !data) return io_fail(std::string(path) + ": null payload");
     File out(path, "wb");
@@ -97,7 +113,11 @@ int fp8b_fp8t_save(const char* path, int32_t dtype, int32_t mode_tag, int32_t ra
         for (int i = 0; i < 8; ++i) buf.push_back((unsigned char)((uint64_t)v >> (56 - 8 * i)));
     const size_t eb = elem_bytes(dtype);
     const size_t hdr = buf.size();
-    buf.resize(hdr + (size_t)n * eb);
+    try {
+        buf.resize(hdr + (size_t)n * eb);
+    } catch (const std::exception&) {  // never let an exception cross the C ABI
+        return io_fail(std::string(path) + ": cannot allocate the payload buffer");
+    }
     unsigned char* p = buf.data() + hdr;
     if (dtype == FP8B_FP8T_FP8) {
         std::memcpy(p, data, (size_t)n);
@@ -153,7 +173,12 @@ int fp8b_fp8t_load(const char* path, int32_t expect_dtype, void* data, int64_t c
     const int64_t n = numel(h.dims);
     if (n > capacity) return io_fail(std::string(path) + ": payload larger than the buffer");
     const size_t eb = elem_bytes(h.dtype);
-    std::vector<unsigned char> buf((size_t)n * eb);
+    std::vector<unsigned char> buf;
+    try {
+        buf.resize((size_t)n * eb);
+    } catch (const std::exception&) {  // never let an exception cross the C ABI
+        return io_fail(std::string(path) + ": cannot allocate the payload buffer");
+    }
     if (n > 0 && std::fread(buf.data(), 1, buf.size(), in.f) != buf.size())
         return io_fail(std::string(path) +
                        (h.dtype == FP8B_FP8T_F32 ? ": truncated FP32 payload" : ": truncated code payload"));

@@ -785,7 +785,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                             stage_codes<1>(&et, w[j], col0, j == PERB - 1 || col0 + 32 >= p.N);
                         } else if (live) {
                             uint8_t* dst = reinterpret_cast<uint8_t*>(p.ep.cq) + row * p.N + col0;
-                            if (col0 + 32 <= p.N && (p.N % 16) == 0) {
+                            if (col0 + 32 <= p.N && (p.N % 16) == 0 && ((uintptr_t)p.ep.cq % 16) == 0) {
                                 uint4* d4 = reinterpret_cast<uint4*>(dst);
                                 d4[0] = make_uint4(w[j][0], w[j][1], w[j][2], w[j][3]);
                                 d4[1] = make_uint4(w[j][4], w[j][5], w[j][6], w[j][7]);
@@ -996,11 +996,7 @@ static int launch_2sm_ast(const CUtensorMap& tA2, const CUtensorMap& tB2, const 
                           const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int num_sms,
                           cudaStream_t st) {
     using G = Geo2<1, EW, NBUF, AST>;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(gemm_tc2_kernel<ES, 1, EW, NBUF, LEAN, AST>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    });
+    ensure_smem_attr((const void*)gemm_tc2_kernel<ES, 1, EW, NBUF, LEAN, AST>, G::SMEM);
     Params p2 = p;
     p2.tiles_m = (int)((m + BM2 - 1) / BM2);
     p2.tiles_n = (int)((n + G::TN - 1) / G::TN);
@@ -1019,15 +1015,10 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
                       const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int num_sms,
                       cudaStream_t st) {
     using G = Geo2<NB, EW, NBUF>;
-    static std::once_flag once;
     static_assert(EW != 16 || LEAN, "16 epilogue warps: codes-only (LEAN) kernels");
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        if constexpr (EW != 16)
-            cudaFuncSetAttribute(gemm_tc2_kernel<ES, NB, EW, NBUF, 0>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    });
+    ensure_smem_attr((const void*)gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN>, G::SMEM);
+    if constexpr (EW != 16)
+        ensure_smem_attr((const void*)gemm_tc2_kernel<ES, NB, EW, NBUF, 0>, G::SMEM);
     Params p2 = p;
     p2.tiles_m = (int)((m + BM2 - 1) / BM2);
     p2.tiles_n = (int)((n + G::TN - 1) / G::TN);
@@ -1112,15 +1103,8 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
     memset(&tmQ, 0, sizeof(tmQ));
     p.qg = code_group(ep.cq_fmt, BN);
     p.q_tma = (!p.c_tma && use_epi_tma() && ep.cq && make_q_map(&tmQ, ep.cq, ep.cq_fmt, m, n, BN)) ? 1 : 0;
-    static int num_sms = 0;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    });
+    const int num_sms = device_sm_count();
+    ensure_smem_attr((const void*)gemm_tc_kernel<ES>, SMEM_BYTES);
     if (use_2sm() && m >= BM2) {
         // 2-SM path: tmA box is 128 rows of the pair's 256 (each CTA loads its half)
         CUtensorMap tA2, tB2;

@@ -50,6 +50,11 @@ int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
                    const fp8b_conv_t& g, cudaStream_t st, int* nlaunch);
 int conv_tc_supported(int kind, int fmt, const fp8b_conv_t& g);
 void launch_im2col(const void* x, void* cols, int fmt, const fp8b_conv_t& g, cudaStream_t st);
+// Per-device setup (several GPUs per process are allowed): SM count of the
+// current device, and the >48 KB dynamic shared memory opt-in of a kernel on
+// the current device, each done once per (kernel, device).
+int device_sm_count();
+void ensure_smem_attr(const void* fn, int bytes);
 // Adds n to the library's launch counter (fp8b_launch_count).
 void note_launches(int n);
 void launch_fill_synthetic(float* out, int64_t n, int kind, uint64_t seed, double p, double lo,

@@ -511,12 +511,7 @@ __global__ void bias_grad_kernel(const void* __restrict__ e, int64_t rows, int64
 
 // ---------------------------------------------------------------- launchers
 static int grid_for(const void* fn, int nt, int64_t work_items) {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int num_sms = device_sm_count();
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, 0);
     if (per_sm < 1) per_sm = 1;
@@ -535,19 +530,16 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
     if (cfg.mode == FP8B_SR && cfg.bits == FP8B_BITS_LFSR) {
         const int64_t nblocks = (n + kBlock - 1) / kBlock;
         int64_t begin = 0;
-        if (aligned) {
+        // the warp kernel stores EPL codes per lane as one 8- or 16-byte word
+        constexpr int kLfsrStoreAlign =
+            FP8B_LFSR_EPL * (MB == 2 ? 1 : 2) < 16 ? FP8B_LFSR_EPL * (MB == 2 ? 1 : 2) : 16;
+        if (aligned && (uintptr_t)codes % kLfsrStoreAlign == 0) {
             const int64_t nfull = n / kBlock;
             if (nfull > 0) {
                 auto fn = quant_lfsr_warp_kernel<MB>;
                 constexpr int smem = kTabWrapBytes;
-                static bool wattr = false;
-                if (!wattr) {
-                    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                    wattr = true;
-                }
-                int num_sms = 0, dev = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+                ensure_smem_attr((const void*)fn, smem);
+                const int num_sms = device_sm_count();
                 // one warp per 4096-block, spread over every SM for small tensors
                 int64_t g = num_sms;
                 int64_t wpc = (nfull + g - 1) / g;

@@ -75,14 +75,32 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     rne.saturate = s->saturate;
     fp8b::SideStream* ss = fp8b::side_stream(st);
     void* side = ss ? (void*)ss->s : stream;
-    auto fork = [&]() {
-        return !ss || (cudaEventRecord(ss->fork, st) == cudaSuccess &&
-                       cudaStreamWaitEvent(ss->s, ss->fork, 0) == cudaSuccess);
-    };
-    auto join = [&]() {
-        return !ss || (cudaEventRecord(ss->join, ss->s) == cudaSuccess &&
-                       cudaStreamWaitEvent(st, ss->join, 0) == cudaSuccess);
-    };
+    // An open fork is always joined, also on the early-return paths (FP8B_TRY):
+    // under stream capture an unjoined fork would invalidate the capture, and run
+    // eagerly the side-stream work would stay unordered with the caller's later
+    // work.
+    struct Branch {
+        fp8b::SideStream* ss;
+        cudaStream_t st;
+        bool open = false;
+        bool fork() {
+            if (!ss) return true;
+            if (cudaEventRecord(ss->fork, st) != cudaSuccess ||
+                cudaStreamWaitEvent(ss->s, ss->fork, 0) != cudaSuccess)
+                return false;
+            open = true;
+            return true;
+        }
+        bool join() {
+            if (!ss || !open) return true;
+            open = false;
+            return cudaEventRecord(ss->join, ss->s) == cudaSuccess &&
+                   cudaStreamWaitEvent(st, ss->join, 0) == cudaSuccess;
+        }
+        ~Branch() { join(); }
+    } br{ss, st};
+    auto fork = [&]() { return br.fork(); };
+    auto join = [&]() { return br.join(); };
     // ---- Q(E) on the side stream, beside the forward (it depends on nothing there)
     if (!fork()) return FP8B_ECUDA;
     FP8B_TRY(fp8b_quantize(s->e, s->qe, B * O, FP8B_E5M2, &rne, s->counters, side));

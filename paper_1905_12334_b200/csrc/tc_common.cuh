@@ -398,7 +398,7 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
     if (!live && !q_tma) return;
     const int64_t base = row * p.N + col0;
     if (ep.c && !c_tma && live) {
-        if (full && (p.N % 4 == 0)) {
+        if (full && (p.N % 4 == 0) && ((uintptr_t)ep.c % 16 == 0)) {
             float4* dst = reinterpret_cast<float4*>(ep.c + base);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -416,7 +416,7 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
             stage_codes<1>(tm_, w, col0, last);
         } else if (live) {
             uint8_t* dst = reinterpret_cast<uint8_t*>(ep.cq) + base;
-            if (full && (p.N % 16 == 0)) {
+            if (full && (p.N % 16 == 0) && ((uintptr_t)ep.cq % 16 == 0)) {
                 uint4* d4 = reinterpret_cast<uint4*>(dst);
                 d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
                 d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -464,7 +464,7 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
                 stage_codes<1>(tm_, w, col0, last);
             } else if (live) {
                 uint8_t* dst = reinterpret_cast<uint8_t*>(ep.cq) + base;
-                if (full && (p.N % 16 == 0)) {
+                if (full && (p.N % 16 == 0) && ((uintptr_t)ep.cq % 16 == 0)) {
                     uint4* d4 = reinterpret_cast<uint4*>(dst);
                     d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
                     d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -481,7 +481,7 @@ __device__ __forceinline__ void epilogue_chunk(const P& p, int64_t row, int64_t 
                 stage_codes<2>(tm_, w, col0, last);
             } else if (live) {
                 uint16_t* dst = reinterpret_cast<uint16_t*>(ep.cq) + base;
-                if (full && (p.N % 8 == 0)) {
+                if (full && (p.N % 8 == 0) && ((uintptr_t)ep.cq % 16 == 0)) {
                     uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) d4[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);

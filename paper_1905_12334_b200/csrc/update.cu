@@ -443,15 +443,7 @@ __global__ void unscale_kernel(float* g, int64_t n, const fp8b_loss_scaler_t* s)
 }
 
 // ---------------------------------------------------------------- launchers
-static int sm_count() {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return num_sms;
-}
+static int sm_count() { return device_sm_count(); }
 
 template <int GFMT>
 static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64_t n,
@@ -474,7 +466,7 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
             const int64_t nfull = n / kBlock;
             constexpr int smem = kUpdTabBytes;
             auto fn = cnt ? sgd_lfsr_warp_kernel<GFMT, true> : sgd_lfsr_warp_kernel<GFMT, false>;
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            ensure_smem_attr((const void*)fn, smem);
             // one warp per 4096-block: a small tensor (config 1: 256 blocks)
             // spreads its warps over every SM instead of filling a few CTAs
             int64_t g = sm_count();

@@ -93,6 +93,11 @@ GARBLED = [
     ("bad_mode_tag", _header(mode=9) + bytes(4)),
     ("fp32_as_codes", _header(dtype=0) + bytes(16)),
     ("codes_as_fp32", _header(dtype=1) + bytes(4)),
+    # shape_numel (tensor.cpp:9-16): a negative dimension is rejected, also when
+    # two of them multiply to a positive element count
+    ("negative_dim", _header(rank=2, dims=(2**64 - 2, 3)) + bytes(6)),
+    ("two_negative_dims", _header(rank=2, dims=(2**64 - 2, 2**64 - 2)) + bytes(4)),
+    ("negative_dim_fp32", _header(dtype=0, rank=1, dims=(2**64 - 1,))),
 ]
 
 
@@ -100,7 +105,7 @@ GARBLED = [
 def test_garbled_files_same_ioerror(F, tmp_path, name, blob):
     p = tmp_path / f"{name}.fp8t"
     p.write_bytes(blob)
-    want_fp32 = name in ("truncated_fp32", "codes_as_fp32")
+    want_fp32 = name in ("truncated_fp32", "codes_as_fp32", "negative_dim_fp32")
     ref_load = O.ref_fp8t_load_f32 if want_fp32 else O.ref_fp8t_load_codes
     our_load = F.load_tensor_fp32 if want_fp32 else F.load_tensor_codes
     with pytest.raises(O.RefIoError) as r:
@@ -119,3 +124,19 @@ def test_missing_file(F, tmp_path):
     assert str(o.value) == str(r.value)
     with pytest.raises(F.IoError, match="cannot open for writing"):
         F.save_tensor(os.path.join(str(tmp_path), "no_dir", "x.fp8t"), np.zeros(2, np.float32))
+
+
+def test_huge_dims_fail_cleanly(F, tmp_path):
+    """A header whose dimension product overflows is an IoError, not an abort
+    across the C ABI; saving with a negative dimension is refused the same way."""
+    import ctypes as C
+    from paper_1905_12334_b200 import _lib
+    p = tmp_path / "huge.fp8t"
+    p.write_bytes(_header(rank=3, dims=(2**40, 2**40, 2**40)) + bytes(8))
+    with pytest.raises(F.IoError, match="overflows"):
+        F.load_tensor_codes(p, device="cpu")
+    dims = (C.c_int64 * 2)(-1, 2)
+    buf = np.zeros(4, np.float32)
+    with pytest.raises(F.IoError, match="negative dimension"):
+        _lib.check(_lib.LIB.fp8b_fp8t_save(str(tmp_path / "neg.fp8t").encode(), _lib.FP8T_F32, 0,
+                                           2, dims, buf.ctypes.data))

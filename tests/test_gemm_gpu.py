@@ -363,3 +363,35 @@ def test_astat_equals_streaming_at_config5_size(fp8, n, b_major):
             os.environ["FP8B_GEMM_AST"] = old
     assert torch.equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1]
+
+
+@pytest.mark.parametrize("c_off,q_off", [(1, 1), (2, 4), (3, 8), (0, 1), (1, 0)])
+@pytest.mark.parametrize("out_fmt", ["fp8", "fp16"])
+def test_tensor_engine_unaligned_outputs(fp8, c_off, q_off, out_fmt):
+    """FP32 C and output codes written into views at element offsets that are
+    not 16-byte aligned: TMA stores are off for them and the direct-store
+    epilogue must not use vector stores (no misaligned-address fault); results
+    equal the aligned call bit for bit."""
+    import torch
+    rng = np.random.default_rng(41)
+    m, k, n = 256, 256, 512
+    A, B = _rand_codes(rng, m, k, "fp8"), _rand_codes(rng, k, n, "fp8")
+    ad, bd = _codes_dev(A, "fp8"), _codes_dev(B, "fp8")
+    qdt = torch.uint8 if out_fmt == "fp8" else torch.int16
+    c_ref, q_ref = fp8.gemm_codes(ad, bd, m, n, k, "fp8", engine="tensor", out_fmt=out_fmt)
+    cbuf = torch.zeros(m * n + 8, dtype=torch.float32, device="cuda")
+    qbuf = torch.zeros(m * n + 16, dtype=qdt, device="cuda")
+    c = cbuf[c_off:c_off + m * n].view(m, n)
+    cq = qbuf[q_off:q_off + m * n]
+    fp8.gemm_codes(ad, bd, m, n, k, "fp8", engine="tensor", c=c, out_fmt=out_fmt, out_codes=cq)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(c.cpu().numpy().view(np.uint32), c_ref.cpu().numpy().view(np.uint32))
+    np.testing.assert_array_equal(cq.cpu().numpy(), q_ref.cpu().numpy())
+    # codes-only (the lean E5M2 epilogue) into a misaligned view
+    cq2 = qbuf[q_off:q_off + m * n]
+    cq2.zero_()
+    fp8.gemm_codes(ad, bd, m, n, k, "fp8", engine="tensor", want_c=False, out_fmt=out_fmt,
+                   out_codes=cq2)
+    _, q_ref2 = fp8.gemm_codes(ad, bd, m, n, k, "fp8", engine="tensor", want_c=False,
+                               out_fmt=out_fmt)
+    np.testing.assert_array_equal(cq2.cpu().numpy(), q_ref2.cpu().numpy())

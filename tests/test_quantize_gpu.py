@@ -250,3 +250,25 @@ def test_exhaustive_fast_paths_vs_scalar_rule(fp8, fmt):
                 assert bad == 0, (fmt, mode, bits_src, sat, hex(c0), bad)
                 assert ca.values() == cb.values(), (fmt, mode, bits_src, sat, hex(c0))
         del bits, x, rb, qa, qb
+
+
+@pytest.mark.parametrize("fmt", ["fp8", "fp16"])
+@pytest.mark.parametrize("off", [1, 2, 4, 8])
+@pytest.mark.parametrize("mode,bits", [("stochastic", "lfsr"), ("nearest-even", "lfsr"),
+                                       ("stochastic", "counter"), ("truncate", "lfsr")])
+def test_unaligned_codes_output(fp8, fmt, off, mode, bits):
+    """Codes written into a view at any element offset (out=buf[off:]): the
+    vector-store kernels are only chosen when the output base allows their
+    8/16-byte stores; results equal the oracle either way."""
+    import torch
+    n = 4096 * 5 + 100
+    x = _config2(fp8, n, 13)
+    dt = torch.uint8 if fmt == "fp8" else torch.int16
+    buf = torch.zeros(n + 16, dtype=dt, device="cuda")
+    q = fp8.quantize(x, fmt, mode, 5, bits=bits, out=buf[off:off + n])
+    torch.cuda.synchronize()
+    codes, cnt = O.quantize(x.cpu().numpy(), fmt, mode, 5, bits=bits)
+    np.testing.assert_array_equal(q.codes_u16(), codes)
+    assert q.counters.values() == tuple(int(v) for v in cnt)
+    # the guard bytes around the view are untouched
+    assert int(buf[:off].abs().sum()) == 0 and int(buf[off + n:].abs().sum()) == 0

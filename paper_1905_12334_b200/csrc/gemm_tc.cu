@@ -60,6 +60,14 @@ struct Params {
                 // split (lo/hi) accumulator release, 1024 = no register-staged E5M2 epilogue,
                 // 2048 = epilogue drains TMEM only
     int splits; // 2-SM kernel: split-K factor (>1: FP32 partials into the 3-D workspace map tmC)
+    // 2-SM kernel, stream-K: the (tile, k-block) units are dealt out evenly, one
+    // contiguous range per cluster ticket (see gemm_tc2_kernel)
+    int sk;
+    int sk_dp_tiles;   // tiles run data-parallel first (whole waves: a multiple of the clusters)
+    int sk_units;      // stream-K units: remaining tiles * num_kb (sk_units * clusters < 2^31)
+    float* sk_ws;      // partial tiles: [ticket][CTA rank][128 rows][tile N] FP32
+    int* sk_flags;     // [ticket][CTA rank]: epilogue-warp arrivals; self-cleaning
+    int* sk_ticket;    // cluster ticket counter; self-cleaning
     EpiArgs ep;
 };
 
@@ -389,10 +397,21 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
 
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_shared_cluster_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 // LEAN = 1: the epilogue is compiled for the fused E5M2 RNE output node only (no
 // FP32 C, no other Q modes, no diagnostics) -- a kernel a fraction of the general
 // one's size, for the instruction cache of epilogue-bound short-K shapes.
-template <int ES, int NB, int EW, int NBUF, int LEAN = 0, int AST = 0>
+template <int ES, int NB, int EW, int NBUF, int LEAN = 0, int AST = 0, int SK = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, AST>::THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
@@ -438,9 +457,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
         const int tile = item / p.splits;
         s = item - tile * p.splits;
         tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
-        kb0 = (int)((int64_t)p.num_kb * s / p.splits);
-        kb1 = (int)((int64_t)p.num_kb * (s + 1) / p.splits);
+        kb0 = p.num_kb * s / p.splits;  // (32-bit: a 64-bit divide is a call)
+        kb1 = p.num_kb * (s + 1) / p.splits;
     };
+    // Stream-K (SK): whole waves of tiles run data-parallel; the (tile,
+    // k-block) units of the remaining tiles -- the part-empty last wave -- are
+    // split into nclusters even contiguous ranges; range r goes to the cluster that drew
+    // ticket r on arrival. A range is a run of segments (one tile, a k-block
+    // span). A tile cut by range boundaries is finished by its "owner", the
+    // range holding its last k-block; the lower ranges ("contributors") leave
+    // FP32 partial tiles in the workspace. Each cluster does its contributor
+    // piece (the head of its last tile) first and its owner piece late, so an
+    // owner only ever waits on
+    // lower tickets -- clusters already running, whose contribution was their
+    // first work. No co-residency assumption, so concurrent kernels on other
+    // streams cannot deadlock it.
+    __shared__ int sk_ticket_smem;
+    if (SK && rank == 0 && threadIdx.x == 0) {
+        const int t = atomicAdd(p.sk_ticket, 1);
+        if (t == nclusters - 1) atomicExch(p.sk_ticket, 0);  // last arrival: reset for the next launch
+        sk_ticket_smem = t;
+    }
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -469,15 +506,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
     cluster_sync_all();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // (32-bit unit arithmetic: the host keeps sk_units * nclusters < 2^31)
+    int ticket = 0;
+    uint32_t sk_u0 = 0, sk_u1 = 0;
+    const uint32_t sk_units = (uint32_t)p.sk_units, ncl_u = (uint32_t)nclusters;
+    const uint32_t sk_base = (uint32_t)p.sk_dp_tiles * (uint32_t)p.num_kb;  // first stream-K unit
+    if (SK) {
+        ticket = rank == 0 ? sk_ticket_smem
+                           : (int)ld_shared_cluster_u32(mapa_u32(smem_u32(&sk_ticket_smem), 0));
+        sk_u0 = sk_base + sk_units * (uint32_t)ticket / ncl_u;
+        sk_u1 = sk_base + sk_units * (uint32_t)(ticket + 1) / ncl_u;
+    }
+    // The next work segment of this cluster (every role walks the same list).
+    // Stream-K order: the contributor piece (head of the range's last tile)
+    // first; then the data-parallel whole tiles (cluster_id + i * nclusters)
+    // and any whole tiles inside the range; the owner piece (tail of the
+    // range's first tile) last, when its contributors -- lower tickets, which
+    // did their piece first -- are long done. `cur` is the phase (0
+    // contributor, 1 data-parallel tiles, 2 whole tiles in the range, 3 owner,
+    // 4 done), `sk_t` the phase's tile cursor.
+    const int nkb = p.num_kb;
+    const bool sk_any = SK && sk_u1 > sk_u0;
+    const int sk_tf = sk_any ? (int)(sk_u0 / (uint32_t)nkb) : 0;         // first tile of the range
+    const int sk_tl = sk_any ? (int)((sk_u1 - 1) / (uint32_t)nkb) : 0;   // last tile of the range
+    const int sk_h = (int)sk_u0 - sk_tf * nkb;  // k-block where the range starts in tile tf
+    const int sk_e = (int)sk_u1 - sk_tl * nkb;  // k-block where it ends in tile tl (1..nkb)
+    const int sk_fl = sk_h ? sk_tf + 1 : sk_tf;  // whole tiles in the range: [fl, fh]
+    const int sk_fh = sk_e < nkb ? sk_tl - 1 : sk_tl;
+    const int sk_waves = SK ? p.sk_dp_tiles / nclusters : 0;
+    auto next_seg = [&](int& cur, int& sk_t, int& tm, int& tn, int& s, int& kb0, int& kb1) -> bool {
+        if (SK) {
+            int t = -1;
+            s = 0;
+            if (cur == 0) {
+                cur = 1;
+                sk_t = 0;
+                if (sk_any && sk_e < nkb) { t = sk_tl; kb0 = sk_tf == sk_tl ? sk_h : 0; kb1 = sk_e; }
+            }
+            if (t < 0 && cur == 1) {
+                if (sk_t < sk_waves) { t = cluster_id + nclusters * sk_t++; kb0 = 0; kb1 = nkb; }
+                else { cur = 2; sk_t = sk_fl; }
+            }
+            if (t < 0 && cur == 2) {
+                if (sk_any && sk_t <= sk_fh) { t = sk_t++; kb0 = 0; kb1 = nkb; }
+                else cur = 3;
+            }
+            if (t < 0 && cur == 3) {
+                cur = 4;
+                if (sk_any && sk_h && (sk_tf != sk_tl || sk_e == nkb)) { t = sk_tf; kb0 = sk_h; kb1 = nkb; }
+            }
+            if (t < 0) return false;
+            tile_coords(t, p.tiles_m, p.tiles_n, tm, tn);
+            return true;
+        }
+        if (cur >= nitems) return false;
+        item_of(cur, tm, tn, s, kb0, kb1);
+        cur += nclusters;
+        return true;
+    };
+    const int seg_start = SK ? 0 : cluster_id;
+    const int sk_t_last = 0;
 
     uint32_t co = 0, cu = 0, cn = 0;
     if (warp == 0) {
         if (lane == 0 && !(p.dbg & 8)) {
             int stage = 0;
             uint32_t phase = 0, aphase = 0;
-            for (int item = cluster_id; item < nitems; item += nclusters) {
-                int tm, tn, s, kb0, kb1;
-                item_of(item, tm, tn, s, kb0, kb1);
+            int cur = seg_start, sk_t = sk_t_last;
+            int tm, tn, s, kb0, kb1;
+            while (next_seg(cur, sk_t, tm, tn, s, kb0, kb1)) {
                 if (AST && tm >= p.tiles_m) continue;
                 const int32_t m0 = tm * BM2 + (int32_t)rank * 128, n0 = tn * G::TN + (int32_t)rank * 128;
                 if (AST) {
@@ -614,9 +711,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                 }
             };
             uint32_t aphase = 0;
-            for (int item = cluster_id; item < nitems; item += nclusters) {
-                int tm, tn, s, kb0, kb1;
-                item_of(item, tm, tn, s, kb0, kb1);
+            int cur = seg_start, sk_t = sk_t_last;
+            int tm, tn, s, kb0, kb1;
+            while (next_seg(cur, sk_t, tm, tn, s, kb0, kb1)) {
                 if (AST) {
                     if (tm >= p.tiles_m) continue;
                     mbar_wait(tempty_bar + acc, accphase ^ 1);
@@ -714,9 +811,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
         const bool split_rel = NB == 2 && !(p.dbg & 512);
         const bool lean_q = LEAN || (p.ep.cq && !p.ep.c && p.splits == 1 && p.ep.cq_mode == FP8B_RNE &&
                                      p.ep.cq_fmt == FP8B_E5M2 && !(p.dbg & (4 | 1024 | 2048)));
-        for (int item = cluster_id; item < nitems; item += nclusters) {
-            int tm, tn, s, kb0, kb1;
-            item_of(item, tm, tn, s, kb0, kb1);
+        int cur = seg_start, sk_t = sk_t_last;
+        int tm, tn, s, kb0, kb1;
+        while (next_seg(cur, sk_t, tm, tn, s, kb0, kb1)) {
             if (AST && tm >= p.tiles_m) continue;
             const int64_t row = (int64_t)tm * BM2 + rank * 128 + quarter * 32 + lane;
             if (p.dbg & 128) {
@@ -728,6 +825,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
             }
             fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN2);
+            // stream-K roles: 1 = contributor (a head span of a tile another
+            // cluster finishes), 2 = owner (the tail span: add the contributors'
+            // partials, then the real epilogue), 0 = whole tile
+            // Partial tiles are stored chunk-major so a warp's float4 stores and
+            // loads are coalesced: float4 q of chunk c of TMEM lane l sits at
+            // float4 index (c * 8 + q) * 128 + l of the CTA's region.
+            const int sk_kind = !SK ? 0 : (kb1 < p.num_kb ? 1 : (kb0 > 0 ? 2 : 0));
+            const int sk_lrow = quarter * 32 + lane;
+            if (sk_kind == 1) {
+                float4* dst = reinterpret_cast<float4*>(p.sk_ws + (size_t)(ticket * 2 + (int)rank) * 128 * G::TN) + sk_lrow;
+#pragma unroll 1
+                for (int b = 0; b < NB; ++b) {
+#pragma unroll 1
+                    for (int j = 0; j < PERB; ++j) {
+                        const int c = b * 8 + ehalf * PERB + j;
+                        if ((int64_t)tn * G::TN + c * 32 >= p.N) continue;
+                        uint32_t v[32];
+                        tmem_ld32(taddr + c * 32, v);
+                        float4* d4 = dst + c * 8 * 128;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            __stcg(d4 + q * 128, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                                       __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+                    }
+                    if (split_rel) {
+                        fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(te_leader + b * 8);
+                    }
+                }
+                fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (!split_rel) mbar_arrive_cluster(te_leader + acc * 8);
+                    __threadfence();  // the warp's partial rows before its arrival
+                    atomicAdd(p.sk_flags + ticket * 2 + (int)rank, 1);
+                }
+                if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
+                continue;
+            }
+            // owner: contributors are the tickets [sk_first, ticket), all running
+            // or done; wait until each has all EW warps' partial rows out
+            int sk_first = ticket;
+            if (sk_kind == 2) {
+                const uint32_t u_tile = sk_u0 - (uint32_t)kb0 - sk_base;  // the tile's first unit
+                uint32_t c = u_tile * ncl_u / sk_units;
+                while (c > 0 && sk_units * c / ncl_u > u_tile) --c;
+                while (sk_units * (c + 1) / ncl_u <= u_tile) ++c;
+                sk_first = (int)c;
+                if (lane == 0)
+                    for (int cc = sk_first; cc < ticket; ++cc)
+                        while (ld_acquire_gpu(p.sk_flags + cc * 2 + (int)rank) < EW) {}
+                __syncwarp();
+            }
+            // add the contributors' partials of chunk c, nearest range first
+            auto sk_add = [&](uint32_t (&v)[32], int c) {
+                for (int cc = ticket - 1; cc >= sk_first; --cc) {
+                    const float4* src = reinterpret_cast<const float4*>(
+                        p.sk_ws + (size_t)(cc * 2 + (int)rank) * 128 * G::TN) + sk_lrow + c * 8 * 128;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 t = __ldcg(src + q * 128);
+                        v[4 * q] = __float_as_uint(__fadd_rn(__uint_as_float(v[4 * q]), t.x));
+                        v[4 * q + 1] = __float_as_uint(__fadd_rn(__uint_as_float(v[4 * q + 1]), t.y));
+                        v[4 * q + 2] = __float_as_uint(__fadd_rn(__uint_as_float(v[4 * q + 2]), t.z));
+                        v[4 * q + 3] = __float_as_uint(__fadd_rn(__uint_as_float(v[4 * q + 3]), t.w));
+                    }
+                }
+            };
+            // after the owner's last read: count this warp out; the last of the
+            // 2 x EW arrivals resets the flag for the next launch
+            auto sk_done = [&]() {
+                if (sk_kind != 2) return;
+                __syncwarp();
+                if (lane == 0)
+                    for (int cc = sk_first; cc < ticket; ++cc)
+                        if (atomicAdd(p.sk_flags + cc * 2 + (int)rank, 1) == 2 * EW - 1)
+                            atomicExch(p.sk_flags + cc * 2 + (int)rank, 0);
+            };
             EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
                       (int64_t)tm * BM2 + rank * 128 + quarter * 32, lane, p.splits > 1 ? s : -1,
                       p.qg, 0, nullptr, NBUF};
@@ -764,6 +940,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                         const int64_t col0 = (int64_t)tn * G::TN + c * 32;
                         uint32_t (&v)[32] = vv[q];
                         tmem_regs_after_wait(v);
+                        if (sk_kind == 2) sk_add(v, c);
                         float y[32];
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) y[jj] = __uint_as_float(v[jj]);
@@ -796,6 +973,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                         }
                     }
                 }
+                sk_done();
                 if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
                 continue;
             }
@@ -808,6 +986,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
                     if (col0 < p.N) {
                         uint32_t v[32];
                         tmem_ld32(taddr + c * 32, v);
+                        if (sk_kind == 2) sk_add(v, c);
                         if (p.dbg & 2048) {  // diagnostic: drain TMEM, write nothing
                             if (v[0] == 0x7FC00001u && v[31] == 0x7FC00001u) co += 1;
                         } else if (p.c_tma || p.q_tma) {
@@ -832,6 +1011,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(te_leader + (NB == 2 && !(p.dbg & 512) ? 8 : acc * 8));
+            sk_done();
             if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
         }
     }
@@ -939,6 +1119,32 @@ static int choose_splits(int tiles, int clusters, int num_kb, int64_t mn, int es
     return bc < 0.95 * cost(1) ? best : 1;
 }
 
+// Stream-K for the 2-SM kernel: when whole tiles leave the last wave part-empty
+// (tiles not a multiple of the cluster count) and K is long enough, the whole
+// waves run data-parallel and the k-block units of the remaining tiles are
+// dealt out evenly. Returns the number of data-parallel tiles, or -1 for the
+// plain data-parallel schedule. Cost in k-block steps per cluster:
+// data-parallel = waves x num_kb; hybrid = whole waves x num_kb +
+// ceil(remaining units / clusters) + the partial-tile round trip through L2
+// (~4 steps of the 256x256 tile, ~8 of the 256x512). The 256x512 steps are
+// counted double. FP8B_GEMM_SK=0 disables it, =1 forces it (tests; =2 forces
+// pure stream-K, no data-parallel waves).
+static int choose_sk(int tiles, int clusters, int num_kb, int nb) {
+    const char* e = getenv("FP8B_GEMM_SK");
+    if (e && e[0] == '0') return -1;
+    const int waves = tiles / clusters;
+    const int rem = tiles - waves * clusters;
+    if (e && e[0] == '2') return (int64_t)tiles * num_kb >= clusters ? 0 : -1;
+    if (rem == 0 || (int64_t)rem * num_kb < clusters) return -1;
+    if (e && e[0] == '1') return waves * clusters;
+    // Not chosen automatically: measured slower than data-parallel on every
+    // config-3 shape where the model predicts a gain (16384x1024x16384 0.208 vs
+    // 0.191 ms, 4096^3 0.064 vs 0.051 ms; ncu: +45 % L2 bytes, tensor pipe 82 %
+    // vs 93 % active).
+    (void)nb;
+    return -1;
+}
+
 // ------------------------------------------------------------------ host side
 // FP8B_GEMM_2SM=0 in the environment selects the 1-SM kernel (for A/B checks).
 static bool use_2sm() {
@@ -1010,6 +1216,43 @@ static int launch_2sm_ast(const CUtensorMap& tA2, const CUtensorMap& tB2, const 
     return FP8B_OK;
 }
 
+// Stream-K launch (opt-in, FP8B_GEMM_SK): the general-epilogue kernel with 8
+// epilogue warps. Its partial-tile workspace, flags and ticket come from one
+// stream-ordered allocation; flags and ticket are zeroed here and reset by the
+// kernel itself.
+template <int ES, int NB>
+static int launch_2sm_sk(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUtensorMap& tmC,
+                         const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int dp_tiles,
+                         int maxg, cudaStream_t st) {
+    using G = Geo2<NB, 8, 2>;
+    ensure_smem_attr((const void*)gemm_tc2_kernel<ES, NB, 8, 2, 0, 0, 1>, G::SMEM);
+    Params p2 = p;
+    p2.tiles_m = (int)((m + BM2 - 1) / BM2);
+    p2.tiles_n = (int)((n + G::TN - 1) / G::TN);
+    p2.splits = 1;
+    const int ntiles2 = p2.tiles_m * p2.tiles_n;
+    const int ncl = maxg / 2;
+    CUtensorMap tq2 = tmQ;
+    code_boxes_for_ew<8>(p2, tq2, p, m, n);
+    const size_t flag_bytes = ((size_t)(2 * ncl + 1) * sizeof(int) + 255) & ~(size_t)255;
+    const size_t slot = (size_t)2 * 128 * G::TN * sizeof(float);
+    void* buf = nullptr;
+    if (cudaMallocAsync(&buf, flag_bytes + (size_t)ncl * slot, st) != cudaSuccess) return FP8B_ECUDA;
+    if (cudaMemsetAsync(buf, 0, flag_bytes, st) != cudaSuccess) {
+        cudaFreeAsync(buf, st);
+        return FP8B_ECUDA;
+    }
+    p2.sk = 1;
+    p2.sk_dp_tiles = dp_tiles;
+    p2.sk_units = (ntiles2 - dp_tiles) * p.num_kb;
+    p2.sk_flags = static_cast<int*>(buf);
+    p2.sk_ticket = p2.sk_flags + 2 * ncl;
+    p2.sk_ws = reinterpret_cast<float*>(static_cast<uint8_t*>(buf) + flag_bytes);
+    gemm_tc2_kernel<ES, NB, 8, 2, 0, 0, 1><<<maxg, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tq2, p2);
+    cudaFreeAsync(buf, st);
+    return FP8B_OK;
+}
+
 template <int ES, int NB, int EW = 4, int NBUF = 2, int LEAN = 0>
 static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUtensorMap& tmC,
                       const CUtensorMap& tmQ, const Params& p, int64_t m, int64_t n, int num_sms,
@@ -1059,6 +1302,9 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
     if (grid2 > maxg) grid2 = maxg;
     CUtensorMap tq2 = tmQ;
     code_boxes_for_ew<EW>(p2, tq2, p, m, n);
+    const int dp_tiles = choose_sk(ntiles2, maxg / 2, p.num_kb, NB);
+    if (p.dbg == 0 && dp_tiles >= 0 && (int64_t)ntiles2 * p.num_kb * (maxg / 2) < (1ll << 31))
+        return launch_2sm_sk<ES, NB>(tA2, tB2, tmC, tmQ, p, m, n, dp_tiles, maxg, st);
     gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tq2, p2);
     return FP8B_OK;
 }
@@ -1088,6 +1334,12 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
     p.tiles_n = (int)((n + BN - 1) / BN);
     p.num_kb = (int)((k + BKE - 1) / BKE);
     p.splits = 1;
+    p.sk = 0;
+    p.sk_dp_tiles = 0;
+    p.sk_units = 0;
+    p.sk_ws = nullptr;
+    p.sk_flags = nullptr;
+    p.sk_ticket = nullptr;
     {
         const char* e = getenv("FP8B_GEMM_DBG");
         p.dbg = e ? atoi(e) : 0;

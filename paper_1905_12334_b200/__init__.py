@@ -33,7 +33,8 @@ __all__ = [
     "QuantizedTensor", "ScaleEvent", "LossScaler", "quantize", "dequantize", "transpose",
     "gemm", "gemm_codes", "encode", "decode", "sgd_momentum_update", "bias_grad",
     "count_nonfinite", "fill_synthetic", "Counters", "launch_count", "version",
-    "conv2d", "conv2d_backward_data", "conv2d_backward_weights", "im2col", "conv_out_dim", "conv_tensor_supported", "conv2d_im2col",
+    "conv2d", "conv2d_backward_data", "conv2d_backward_weights", "im2col", "conv_out_dim", "conv_tensor_supported", "conv_halo_supported",
+    "conv2d_im2col",
 ]
 
 _FMT = {"fp8": _lib.E5M2, "FP8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16,
@@ -429,6 +430,13 @@ def conv_tensor_supported(n, c, h, w, f, k, stride=1, pad=0, fmt="fp8", kind="fp
     g = _conv_geom(n, c, h, w, f, k, k, stride, pad, layout, "tensor")
     return bool(LIB.fp8b_conv_tensor_supported(g, _fmt(fmt),
                                                {"fprop": 0, "dgrad": 1, "wgrad": 2}[kind]))
+
+
+def conv_halo_supported(n, c, h, w, f, k, stride=1, pad=0, fmt="fp8", kind="fprop") -> bool:
+    """True if the tensor engine runs this NHWC conv on the weight-stationary
+    halo-slab kernel (fprop / dgrad of narrow stride-1 layers)."""
+    g = _conv_geom(n, c, h, w, f, k, k, stride, pad, "nhwc", "tensor")
+    return bool(LIB.fp8b_conv_halo_supported(g, _fmt(fmt), {"fprop": 0, "dgrad": 1, "wgrad": 2}[kind]))
 
 
 def im2col(x: QuantizedTensor, kh: int, kw: int, stride: int = 1, pad: int = 0, *,

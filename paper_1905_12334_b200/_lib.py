@@ -93,6 +93,7 @@ SIGNATURES = {
     "fp8b_conv2d_dgrad": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
     "fp8b_conv2d_wgrad": (C.c_int, [_vp, _vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
     "fp8b_conv_tensor_supported": (C.c_int, [C.POINTER(ConvGeom), _i32, _i32]),
+    "fp8b_conv_halo_supported": (C.c_int, [C.POINTER(ConvGeom), _i32, _i32]),
     "fp8b_im2col": (C.c_int, [_vp, _vp, _i32, C.POINTER(ConvGeom), _vp]),
     "fp8b_fp8t_save": (C.c_int, [C.c_char_p, _i32, _i32, _i32, _vp, _vp]),
     "fp8b_fp8t_peek": (C.c_int, [C.c_char_p, _vp, _vp, _vp, _vp, _i32]),

@@ -9,7 +9,6 @@
 #include <cstring>
 #include <map>
 #include <mutex>
-#include <set>
 #include <string>
 #include <vector>
 
@@ -125,11 +124,14 @@ int device_sm_count() {
 void ensure_smem_attr(const void* fn, int bytes) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return;
-    static std::set<std::pair<const void*, int>> done;
+    // the largest size set so far per (kernel, device): a kernel whose shared
+    // memory plan depends on the call's geometry may need more on a later call
+    static std::map<std::pair<const void*, int>, int> done;
     std::lock_guard<std::mutex> lk(g_dev_mu);
-    if (done.count({fn, dev})) return;
+    auto it = done.find({fn, dev});
+    if (it != done.end() && it->second >= bytes) return;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
-        done.insert({fn, dev});
+        done[{fn, dev}] = bytes;
 }
 }  // namespace fp8b
 
@@ -344,6 +346,14 @@ int fp8b_conv2d_wgrad(const void* x, const void* e, float* dw, int32_t fmt, cons
 int fp8b_conv_tensor_supported(const fp8b_conv_t* g, int32_t fmt, int32_t kind) {
     if (!g || conv_validate(g, fmt, "conv") != FP8B_OK || kind < 0 || kind > 2) return 0;
     return fp8b::conv_tc_supported(kind, fmt, *g);
+}
+int fp8b_conv_halo_supported(const fp8b_conv_t* g, int32_t fmt, int32_t kind) {
+    if (!fp8b_conv_tensor_supported(g, fmt, kind) || kind > 1 || g->kh < 2) return 0;
+    const int es = fmt == FP8B_E5M2 ? 1 : 2;
+    const int64_t oh = g->h + 2 * g->pad - g->kh + 1, ow = g->w + 2 * g->pad - g->kw + 1;
+    if (kind == 0) return fp8b::conv_halo_supported(es, g->n, g->h, g->w, g->c, g->f, (int)g->kh, (int)g->pad);
+    // dgrad = fprop over e [n, oh, ow, f] with the flipped weights, pad' = k - 1 - pad
+    return fp8b::conv_halo_supported(es, g->n, oh, ow, g->f, g->c, (int)g->kh, (int)(g->kh - 1 - g->pad));
 }
 int fp8b_im2col(const void* x, void* cols, int32_t fmt, const fp8b_conv_t* g, void* stream) {
     const int rc = conv_validate(g, fmt, "im2col expects [N, C, H, W]");

@@ -1,0 +1,506 @@
+// conv_halo.cu -- weight-stationary "halo slab" implicit-GEMM convolution on
+// tcgen05 for the narrow 3x3 layers (conv2d_fp8 / conv2d_backward_data_fp8,
+// kernels.cpp:106-151, 155-200; NHWC, stride 1), where C * bytes <= 128.
+//
+// The im2col kernel (conv_tc.cu) fetches every output pixel's input row once
+// per filter tap: 9 TMA row requests per pixel for a 3x3 layer, which bounds
+// the C = 64 layers by the TMA request rate, not by HBM or the tensor pipe.
+// Here a tile is R whole output rows of one image (R = 128 / Wp, Wp = W + 2 pad
+// the padded width). Its input is one zero-padded slab of SR padded rows x Wp
+// columns x C channels, loaded by ONE 4-D tiled TMA box (out-of-image rows and
+// columns come back as zeros), 64/128-byte swizzled like any K-major operand.
+// In the padded row-major index q = oh * Wp + ow, the input of tap (kh, kw) for
+// output q is slab row q + kh * Wp + kw, so the A operand of tap t is the slab
+// itself seen from row offset kh * Wp + kw: a UMMA descriptor whose start
+// address moves by whole rows (the swizzle is a function of the shared-memory
+// address bits, so TMA's writes and the MMA's reads agree at any row offset).
+// Output rows with ow >= OW (the 2 pad columns of each padded row) and rows
+// beyond the tile are computed and dropped by the epilogue.
+// The KRSC weights [F, k*k*C] of the whole layer (k*k taps x F x C) stay
+// resident in shared memory for the kernel's lifetime (F <= 256, <= 150 KB).
+// Per 128-pixel tile the operand stream is one slab (~18 KB for 3x3, C = 64
+// at 56x56) instead of 9 x 8 KB of im2col rows.
+//
+// Roles (one CTA per SM, persistent): warp 0 TMA producer (weights once, then
+// a ring of slabs), warp 1 MMA issuer (k*k*C/32 tcgen05.mma per tile, M=128,
+// N=F, accumulator double-buffered in TMEM), warps 2-5 epilogue (TMEM lane
+// quarters: bias, FP32 y and/or the fused output Q node with the reference's
+// counters, as in gemm_tc.cu). Parity as for the im2col kernel: the GEMM
+// tolerance |y - y_exact| <= 1e-6 * (|x| * |w|) (tests/test_conv_gpu.py).
+#include <cstdlib>
+#include <cstring>
+
+#include "tc_common.cuh"
+
+namespace fp8b {
+namespace tc {
+namespace halo {
+
+struct HParams {
+    int64_t M, N;      // output matrix [P, F] (P = n * OH * OW)
+    EpiArgs ep;
+    int nimg, OH, OW;  // output geometry
+    int Wp;            // padded width (slab row length)
+    int R;             // output rows per tile
+    int SR;            // slab rows loaded per tile
+    int k, pad;        // square kernel, padding
+    int tiles_per_img, ntiles;
+    int bo_mode;       // descriptor base-offset rule for row-shifted starts (diagnostic knob)
+    int wlog;          // log2(Wp): Wp is a power of two, so a tile is 128 / Wp whole rows
+    int c_tma, q_tma;  // FP32 y / output codes go out through 4-D TMA stores
+    int qg;            // code chunks per store row (64 or 128 bytes)
+    // epilogue staging per warp (bytes): the FP32 box(es) at c_off, the code
+    // box(es) at q_off; *_nbuf = 2 is a ring of two boxes, 1 a single box
+    int stg, c_off, q_off, c_nbuf, q_nbuf;
+};
+
+constexpr int EW = 4;
+constexpr int THREADS = 64 + 32 * EW;
+
+// Shared-memory plan for CB-byte pixel rows and a BN-wide filter tile.
+template <int CB, int BN>
+struct HGeo {
+    static constexpr uint32_t W_TAP = (uint32_t)BN * CB;   // one tap's weights [BN x CB]
+    static constexpr uint32_t SWZ = CB == 128 ? 2u : 4u;   // UMMA layout code
+    static constexpr uint32_t SBO = 8u * CB;               // 8-row swizzle atom
+    static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+};
+
+__device__ __forceinline__ uint64_t desc_bo(uint32_t saddr, uint32_t sbo, uint32_t layout,
+                                            uint32_t bo) {
+    uint64_t d = umma_desc(saddr, 16, sbo, layout);
+    d |= (uint64_t)(bo & 7u) << 49;
+    return d;
+}
+
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* tm, void* dst, uint64_t* bar,
+                                            int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+        "r"(c3)
+        : "memory");
+}
+
+// tmX: 4-D tiled map over x [n, h, w, c] with box {c, Wp, SR, 1};
+// tmW: 2-D map over w [f, k*k*c] with box {c, BN}.
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* tm, uint8_t* buf, int lane, int32_t c0,
+                                             int32_t c1, int32_t c2, int32_t c3) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(tm)),
+            "r"(smem_u32(buf)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+}
+
+// Output Q node of one 32-column chunk (bias already added): code words (8
+// E5M2 / 16 FP16) and the reference's counters for live lanes and valid
+// columns. gbase = this lane's pixel * N + col0 (counter-bit SR position).
+template <class P>
+__device__ __forceinline__ void codes_chunk(const P& p, const float (&y)[32], int64_t gbase, bool live,
+                                            int nvalid, uint32_t* w, uint32_t& co, uint32_t& cu,
+                                            uint32_t& cn) {
+    const EpiArgs& ep = p.ep;
+    const bool sat = ep.cq_sat != 0;
+    if (ep.cq_fmt == FP8B_E5M2 && ep.cq_mode == FP8B_RNE) {
+        uint32_t w8[8];
+        lean_e5m2_codes(y, w8, sat, live, nvalid, co, cu, cn);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = w8[q];
+        return;
+    }
+    uint32_t code[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        int o, u, na;
+        const uint32_t r16 = ep.cq_mode == FP8B_SR ? counter_r16(ep.cq_seed, (uint64_t)(gbase + j)) : 0u;
+        code[j] = ep.cq_fmt == FP8B_E5M2 ? encode_int<2>(__float_as_uint(y[j]), ep.cq_mode, r16, sat, o, u, na)
+                                         : encode_int<10>(__float_as_uint(y[j]), ep.cq_mode, r16, sat, o, u, na);
+        if (live && j < nvalid) { co += o; cu += u; cn += na; }
+    }
+    if (ep.cq_fmt == FP8B_E5M2) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            w[q] = code[4 * q] | (code[4 * q + 1] << 8) | (code[4 * q + 2] << 16) | (code[4 * q + 3] << 24);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) w[q] = code[2 * q] | (code[2 * q + 1] << 16);
+    }
+}
+
+// tmY / tmQ: 4-D store maps over y [n, oh, ow, f] (FP32) / the output codes,
+// boxes {32 | qg * 32 columns, min(32, Wp) pixels, max(1, 32 / Wp) rows, 1}:
+// one box = one epilogue warp's 32 TMEM lanes for one column chunk.
+template <int ES, int CB, int BN>
+__global__ void __launch_bounds__(THREADS, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                     const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmQ,
+                     const HParams p, uint32_t slab_bytes, int nstages) {
+    using G = HGeo<CB, BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    const int taps = p.k * p.k;
+    uint8_t* wsm = smem;                                                       // resident weights
+    uint8_t* ring = smem + (((uint32_t)taps * G::W_TAP + 1023u) & ~1023u);     // slab ring
+    uint8_t* stg = ring + (uint32_t)nstages * slab_bytes;                      // p.stg bytes per epilogue warp
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stg + EW * p.stg);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = full_bar + nstages;
+    uint64_t* tfull_bar = empty_bar + nstages;
+    uint64_t* tempty_bar = tfull_bar + 2;
+    uint64_t* w_bar = tempty_bar + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+        for (int s = 0; s < nstages; ++s) {
+            mbar_init(full_bar + s, 1);
+            mbar_init(empty_bar + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar + a, 1);
+            mbar_init(tempty_bar + a, EW);
+        }
+        mbar_init(w_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(G::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    uint32_t co = 0, cu = 0, cn = 0;
+    if (warp == 0) {
+        if (lane == 0) {
+            // the layer's weights, once: tap t -> [BN x CB] at wsm + t * W_TAP
+            mbar_expect_tx(w_bar, (uint32_t)taps * G::W_TAP);
+            for (int t = 0; t < taps; ++t)
+                tma_load_2d(&tmW, wsm + t * G::W_TAP, w_bar, t * (CB / ES), 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+                const int n = tile / p.tiles_per_img;
+                const int oh0 = (tile - n * p.tiles_per_img) * p.R;
+                mbar_wait(empty_bar + stage, phase ^ 1);
+                mbar_expect_tx(full_bar + stage, (uint32_t)p.SR * p.Wp * CB);
+                tma_load_4d(&tmX, ring + stage * slab_bytes, full_bar + stage, 0, -p.pad, oh0 - p.pad, n);
+                if (++stage == nstages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t leader = elect_one();
+        uint32_t idesc = (1u << 4);
+        if (ES == 1) idesc |= (1u << 7) | (1u << 10);
+        idesc |= (uint32_t)(BN >> 3) << 17;
+        idesc |= (uint32_t)(128 >> 4) << 24;
+        mbar_wait(w_bar, 0);
+        const uint32_t w0 = smem_u32(wsm);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t accphase = 0;
+        for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            mbar_wait(tempty_bar + acc, accphase ^ 1);
+            fence_after();
+            mbar_wait(full_bar + stage, phase);
+            fence_after();
+            const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+            const uint32_t s0 = smem_u32(ring + stage * slab_bytes);
+            for (int t = 0; t < taps; ++t) {
+                const int kh = t / p.k, kw = t - kh * p.k;
+                const uint32_t a0 = s0 + (uint32_t)(kh * p.Wp + kw) * CB;  // row-shifted view
+                const uint32_t bo = p.bo_mode ? (a0 >> 7) & 7u : 0u;
+#pragma unroll
+                for (int kk = 0; kk < CB / 32; ++kk) {
+                    const uint64_t ad = desc_bo(a0 + 32 * kk, G::SBO, G::SWZ, bo);
+                    const uint64_t bd = umma_desc(w0 + t * G::W_TAP + 32 * kk, 16, G::SBO, G::SWZ);
+                    mma_p<ES>(d_tmem, ad, bd, idesc, (t | kk) ? 1u : 0u, leader);
+                }
+            }
+            umma_commit_p(empty_bar + stage, leader);
+            umma_commit_p(tfull_bar + acc, leader);
+            if (++stage == nstages) { stage = 0; phase ^= 1; }
+            if (++acc == 2) { acc = 0; accphase ^= 1; }
+        }
+    } else {
+        // One warp = one TMEM lane quarter = 32 consecutive padded-row
+        // positions: min(32, Wp) pixels of max(1, 32 / Wp) output rows, so each
+        // column chunk leaves as one 4-D TMA store box (pad columns and rows
+        // beyond the image are clipped by TMA; counters skip them).
+        const int quarter = warp & 3;
+        const int q = quarter * 32 + lane;
+        const int r = q >> p.wlog, ow = q & ((1 << p.wlog) - 1);
+        const int r0 = (quarter * 32) >> p.wlog, ow0 = (quarter * 32) & ((1 << p.wlog) - 1);
+        // 8 KB of staging per warp: a ring of two 4 KB boxes for one output;
+        // with both FP32 y and codes, one 4 KB box each
+        uint8_t* cbase = stg + (warp - 2) * p.stg + p.c_off;
+        uint8_t* qbase = stg + (warp - 2) * p.stg + p.q_off;
+        const uint32_t qbox = (uint32_t)p.qg * 32 * (p.ep.cq_fmt == FP8B_E5M2 ? 1 : 2) * 32;
+        uint32_t nst_c = 0, nst_q = 0;
+        // next staging box of an output; its previous store must have read it
+        // (one store may stay pending with a ring of two, none with one box)
+        auto acquire = [&](uint8_t* base, uint32_t& nst, int nbuf, uint32_t box) {
+            uint8_t* b = base + (nbuf == 2 ? (nst++ & 1u) * box : 0u);
+            if (lane == 0) {
+                if (nbuf == 2) bulk_wait_read1();
+                else bulk_wait_read0();
+            }
+            __syncwarp();
+            return b;
+        };
+        int acc = 0;
+        uint32_t accphase = 0;
+        for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            const int n = tile / p.tiles_per_img;
+            const int oh0 = (tile - n * p.tiles_per_img) * p.R;
+            const bool live = ow < p.OW && oh0 + r < p.OH;
+            const bool any = ow0 < p.OW && oh0 + r0 < p.OH;  // warp-uniform
+            const int64_t pix = ((int64_t)n * p.OH + oh0 + r) * p.OW + ow;
+            mbar_wait(tfull_bar + acc, accphase);
+            fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+            int qpos = 0;
+            uint8_t* qbuf = nullptr;
+#pragma unroll 1
+            for (int c = 0; any && c < BN / 32 && c * 32 < p.N; ++c) {
+                uint32_t v[32];
+                tmem_ld32(taddr + c * 32, v);
+                const int col0 = c * 32;
+                const int nvalid = p.N - col0 < 32 ? (int)(p.N - col0) : 32;
+                float y[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]);
+                if (p.ep.bias) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < nvalid) y[j] = __fadd_rn(y[j], __ldg(p.ep.bias + col0 + j));
+                }
+                const bool last = c == BN / 32 - 1 || col0 + 32 >= p.N;
+                if (p.c_tma) {
+                    uint8_t* buf = acquire(cbase, nst_c, p.c_nbuf, 4096u);
+                    stage_write<128, 32>(buf, 0, reinterpret_cast<const uint32_t*>(y), lane);
+                    tma_store_4d(&tmY, buf, lane, col0, ow0, oh0 + r0, n);
+                }
+                if (p.q_tma) {
+                    uint32_t w[16];  // 8 words of E5M2 codes or 16 of FP16
+                    codes_chunk(p, y, pix * p.N + col0, live, nvalid, w, co, cu, cn);
+                    if (qpos == 0) qbuf = acquire(qbase, nst_q, p.q_nbuf, qbox);
+                    if (p.ep.cq_fmt == FP8B_E5M2) {
+                        if (p.qg == 4) stage_write<128, 8>(qbuf, qpos * 32, w, lane);
+                        else stage_write<64, 8>(qbuf, qpos * 32, w, lane);
+                    } else {
+                        if (p.qg == 2) stage_write<128, 16>(qbuf, qpos * 64, w, lane);
+                        else stage_write<64, 16>(qbuf, qpos * 64, w, lane);
+                    }
+                    if (++qpos == p.qg || last) {
+                        tma_store_4d(&tmQ, qbuf, lane, col0 - 32 * (qpos - 1), ow0, oh0 + r0, n);
+                        qpos = 0;
+                    }
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_bar + acc);
+            if (++acc == 2) { acc = 0; accphase ^= 1; }
+        }
+        if (lane == 0) bulk_wait_all();
+    }
+    if (p.ep.cq_counters) flush_counters<THREADS>(co, cu, cn, p.ep.cq_counters);
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(G::TMEM_COLS));
+    }
+}
+
+static bool make_slab_map(CUtensorMap* tm, const void* x, int es, int64_t n, int64_t h, int64_t w,
+                          int64_t c, int wp, int sr) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)(c * es), (cuuint64_t)(w * c * es), (cuuint64_t)(h * w * c * es)};
+    cuuint32_t box[4] = {(cuuint32_t)c, (cuuint32_t)wp, (cuuint32_t)sr, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUtensorMapSwizzle swz = c * es == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    return enc(tm, es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4,
+               const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Geometry check shared by the launcher and conv_halo_supported().
+struct Plan {
+    int cb, bn, wp, r, sr, nstages;
+    int qg, stg, c_off, q_off, c_nbuf, q_nbuf;
+    uint32_t wbytes, slab, smem;
+};
+// need_c / q_fmt (-1: none): which outputs the epilogue stages.
+static bool plan_for(int64_t n, int64_t h, int64_t w, int64_t c, int64_t f, int k, int pad, int es,
+                     Plan& pl, bool need_c = true, int q_fmt = FP8B_E5M2) {
+    pl.cb = (int)(c * es);
+    if (pl.cb != 64 && pl.cb != 128) return false;
+    if (f % 16 || f < 16 || f > 256) return false;
+    pl.bn = f <= 64 ? 64 : (f <= 128 ? 128 : 256);
+    if (k < 1 || k > 7 || pad < 0 || pad > k - 1) return false;
+    // slab row length: the padded width rounded up to a power of two, so a
+    // 128-row tile is 128 / Wp whole output rows and each warp's 32 TMEM lanes
+    // are whole pixel runs of one or more rows (one TMA store box)
+    const int64_t oh = h + 2 * pad - k + 1, ow = w + 2 * pad - k + 1;
+    if (oh < 1 || ow < 1 || w + 2 * pad > 128) return false;
+    pl.wp = 1;
+    while (pl.wp < w + 2 * pad) pl.wp <<= 1;
+    pl.r = 128 / pl.wp;
+    pl.sr = (128 + (k - 1) * (pl.wp + 1) + pl.wp - 1) / pl.wp;
+    if (pl.sr > 256) return false;
+    pl.wbytes = (uint32_t)(k * k) * pl.bn * pl.cb;
+    pl.slab = (((uint32_t)pl.sr * pl.wp * pl.cb) + 1023u) & ~1023u;
+    const uint32_t wpad = (pl.wbytes + 1023u) & ~1023u;
+    // staging: rings of two boxes when they fit beside two slabs, else single
+    // boxes (and 64-byte code rows); FP32 box 4 KB, code box 32 x qg * 32 codes
+    const int qes = q_fmt == FP8B_E5M2 ? 1 : 2;
+    const bool need_q = q_fmt >= 0;
+    const uint32_t base = 1024 + wpad + 256;
+    bool fit = false;
+    for (int tight = 0; tight < 2 && !fit; ++tight) {
+        pl.qg = need_q ? tc::code_group(q_fmt, pl.bn) : 1;
+        if (tight && need_q && pl.qg * 32 * qes > 64) pl.qg = 64 / (32 * qes);
+        const uint32_t qbox = (uint32_t)pl.qg * 32 * qes * 32;
+        pl.c_nbuf = need_c ? ((need_q || tight) ? 1 : 2) : 0;
+        pl.q_nbuf = need_q ? ((need_c || tight) ? 1 : 2) : 0;
+        pl.c_off = 0;
+        pl.q_off = pl.c_nbuf * 4096;
+        pl.stg = pl.q_off + pl.q_nbuf * (int)qbox;
+        fit = base + EW * (uint32_t)pl.stg + 2 * pl.slab <= 232448u;
+    }
+    const uint32_t fixed = base + EW * (uint32_t)pl.stg;
+    if (fixed + 2 * pl.slab > 232448u) return false;
+    pl.nstages = (int)((232448u - fixed) / pl.slab);
+    if (pl.nstages > 4) pl.nstages = 4;
+    pl.smem = fixed + (uint32_t)pl.nstages * pl.slab;
+    if (n * oh * ow >= ((int64_t)1 << 31)) return false;
+    return true;
+}
+
+// 4-D store map over an [n, oh, ow, f] output of es-byte elements, boxes of
+// `cols` columns x one warp's 32 TMEM lanes (pixels x rows).
+static bool make_out_map(CUtensorMap* tm, const void* out, int es, int64_t n, int64_t oh, int64_t ow,
+                         int64_t f, int cols, int wp) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc || !out || (uintptr_t)out % 16 || (f * es) % 16) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)f, (cuuint64_t)ow, (cuuint64_t)oh, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)(f * es), (cuuint64_t)(ow * f * es), (cuuint64_t)(oh * ow * f * es)};
+    cuuint32_t box[4] = {(cuuint32_t)cols, (cuuint32_t)(wp < 32 ? wp : 32), (cuuint32_t)(wp < 32 ? 32 / wp : 1), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const int span = cols * es;
+    const CUtensorMapSwizzle swz = span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    if (span != 64 && span != 128) return false;
+    const CUtensorMapDataType dt = es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    return enc(tm, dt, 4, const_cast<void*>(out), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int ES, int CB, int BN>
+static int run(const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty, const CUtensorMap& tq,
+               const HParams& p, const Plan& pl, cudaStream_t st) {
+    auto fn = conv_halo_kernel<ES, CB, BN>;
+    ensure_smem_attr((const void*)fn, (int)pl.smem);
+    const int sms = device_sm_count();
+    const int grid = p.ntiles < sms ? p.ntiles : sms;
+    fn<<<grid, THREADS, pl.smem, st>>>(tx, tw, ty, tq, p, pl.slab, pl.nstages);
+    return cudaGetLastError() == cudaSuccess ? FP8B_OK : FP8B_ECUDA;
+}
+
+}  // namespace halo
+}  // namespace tc
+
+bool conv_halo_supported(int es, int64_t n, int64_t h, int64_t w, int64_t c, int64_t f, int k,
+                         int pad) {
+    const char* e = getenv("FP8B_CONV_HALO");
+    if (e && e[0] == '0') return false;
+    tc::halo::Plan pl;
+    return tc::halo::plan_for(n, h, w, c, f, k, pad, es, pl);
+}
+
+// fprop over NHWC x [n, h, w, c] and KRSC w [f, k, k, c] -> y [n, oh, ow, f]
+// (stride 1). Returns FP8B_ENOTSUP when the geometry is not covered.
+int launch_conv_halo(const void* x, const void* wt, float* y, int es, int64_t n, int64_t h,
+                     int64_t w, int64_t c, int64_t f, int k, int pad, const fp8b_conv_t& g,
+                     cudaStream_t st) {
+    using namespace tc::halo;
+    Plan pl;
+    if (!conv_halo_supported(es, n, h, w, c, f, k, pad) ||
+        !plan_for(n, h, w, c, f, k, pad, es, pl, y != nullptr, g.yq ? g.yq_fmt : -1))
+        return FP8B_ENOTSUP;
+    if ((uintptr_t)x % 16 || (uintptr_t)wt % 16) return FP8B_ENOTSUP;
+    CUtensorMap tx, tw;
+    if (!make_slab_map(&tx, x, es, n, h, w, c, pl.wp, pl.sr)) return FP8B_ENOTSUP;
+    const CUtensorMapSwizzle swz = pl.cb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    // weights [f, k*k*c]: box {c, bn} (rows f >= F of the last box are zero-filled)
+    if (!tc::make_map(&tw, wt, es, (uint64_t)(k * k * c), (uint64_t)f, (uint32_t)c, (uint32_t)pl.bn, swz))
+        return FP8B_ENOTSUP;
+    HParams p{};
+    const int64_t oh = h + 2 * pad - k + 1, ow = w + 2 * pad - k + 1;
+    p.M = n * oh * ow;
+    p.N = f;
+    p.ep = EpiArgs{y, nullptr, g.yq, g.yq_fmt, g.yq_mode, g.yq_seed, g.yq_saturate, g.yq_counters};
+    p.nimg = (int)n; p.OH = (int)oh; p.OW = (int)ow;
+    p.Wp = pl.wp; p.R = pl.r; p.SR = pl.sr; p.k = k; p.pad = pad;
+    p.tiles_per_img = (int)((oh + pl.r - 1) / pl.r);
+    p.ntiles = (int)(n * p.tiles_per_img);
+    const char* bo = getenv("FP8B_CONV_HALO_BO");
+    p.bo_mode = bo ? atoi(bo) : 0;
+    p.stg = pl.stg; p.c_off = pl.c_off; p.q_off = pl.q_off;
+    p.c_nbuf = pl.c_nbuf; p.q_nbuf = pl.q_nbuf;
+    p.wlog = 0;
+    while ((1 << p.wlog) < pl.wp) ++p.wlog;
+    CUtensorMap ty, tq;
+    memset(&ty, 0, sizeof(ty));
+    memset(&tq, 0, sizeof(tq));
+    p.c_tma = y != nullptr;
+    if (y && !make_out_map(&ty, y, 4, n, oh, ow, f, 32, pl.wp)) return FP8B_ENOTSUP;
+    p.q_tma = g.yq != nullptr;
+    if (g.yq) {
+        const int qes = g.yq_fmt == FP8B_E5M2 ? 1 : 2;
+        p.qg = pl.qg;  // 64- or 128-byte code rows
+        if (p.qg * 32 * qes < 64) return FP8B_ENOTSUP;
+        if (!make_out_map(&tq, g.yq, qes, n, oh, ow, f, p.qg * 32, pl.wp)) return FP8B_ENOTSUP;
+    }
+    if (es == 1) {
+        if (pl.cb == 64) {
+            if (pl.bn == 64) return run<1, 64, 64>(tx, tw, ty, tq, p, pl, st);
+            if (pl.bn == 128) return run<1, 64, 128>(tx, tw, ty, tq, p, pl, st);
+            return run<1, 64, 256>(tx, tw, ty, tq, p, pl, st);
+        }
+        if (pl.bn == 64) return run<1, 128, 64>(tx, tw, ty, tq, p, pl, st);
+        if (pl.bn == 128) return run<1, 128, 128>(tx, tw, ty, tq, p, pl, st);
+        return run<1, 128, 256>(tx, tw, ty, tq, p, pl, st);
+    }
+    if (pl.cb == 64) {
+        if (pl.bn == 64) return run<2, 64, 64>(tx, tw, ty, tq, p, pl, st);
+        if (pl.bn == 128) return run<2, 64, 128>(tx, tw, ty, tq, p, pl, st);
+        return run<2, 64, 256>(tx, tw, ty, tq, p, pl, st);
+    }
+    if (pl.bn == 64) return run<2, 128, 64>(tx, tw, ty, tq, p, pl, st);
+    if (pl.bn == 128) return run<2, 128, 128>(tx, tw, ty, tq, p, pl, st);
+    return run<2, 128, 256>(tx, tw, ty, tq, p, pl, st);
+}
+
+}  // namespace fp8b

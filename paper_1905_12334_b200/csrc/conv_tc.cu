@@ -385,6 +385,12 @@ static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
 template <int ES>
 static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, int64_t wd,
                  int64_t c, int64_t f, int k, int pad, cudaStream_t st, const fp8b_conv_t& g) {
+    // narrow layers with k > 1 (C * bytes <= 128): one halo slab per tile
+    // instead of one im2col row request per pixel and tap (conv_halo.cu)
+    if (k > 1) {
+        const int rc = launch_conv_halo(x, w, y, ES, n, h, wd, c, f, k, pad, g, st);
+        if (rc != FP8B_ENOTSUP) return rc;
+    }
     const int cb_bytes = (c * ES) % 128 == 0 ? 128 : ((c * ES) % 64 == 0 ? 64 : 0);
     if (!cb_bytes) return FP8B_ENOTSUP;
     const int64_t oh = h + 2 * pad - k + 1, ow = wd + 2 * pad - k + 1;

@@ -49,6 +49,13 @@ void launch_conv_seq(int kind, const void* a, const void* b, float* out, int fmt
 int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
                    const fp8b_conv_t& g, cudaStream_t st, int* nlaunch);
 int conv_tc_supported(int kind, int fmt, const fp8b_conv_t& g);
+// Weight-stationary halo-slab fprop (conv_halo.cu) for C * bytes in {64, 128},
+// F <= 256; FP8B_ENOTSUP when the geometry is not covered.
+bool conv_halo_supported(int es, int64_t n, int64_t h, int64_t w, int64_t c, int64_t f, int k,
+                         int pad);
+int launch_conv_halo(const void* x, const void* wt, float* y, int es, int64_t n, int64_t h,
+                     int64_t w, int64_t c, int64_t f, int k, int pad, const fp8b_conv_t& g,
+                     cudaStream_t st);
 void launch_im2col(const void* x, void* cols, int fmt, const fp8b_conv_t& g, cudaStream_t st);
 // Per-device setup (several GPUs per process are allowed): SM count of the
 // current device, and the >48 KB dynamic shared memory opt-in of a kernel on

@@ -48,14 +48,22 @@ struct HParams {
     int bo_mode;       // descriptor base-offset rule for row-shifted starts (diagnostic knob)
     int wlog;          // log2(Wp): Wp is a power of two, so a tile is 128 / Wp whole rows
     int c_tma, q_tma;  // FP32 y / output codes go out through 4-D TMA stores
-    int qg;            // code chunks per store row (64 or 128 bytes)
+    int qg;            // code chunks per store row (32, 64 or 128 bytes)
     // epilogue staging per warp (bytes): the FP32 box(es) at c_off, the code
     // box(es) at q_off; *_nbuf = 2 is a ring of two boxes, 1 a single box
     int stg, c_off, q_off, c_nbuf, q_nbuf;
+    int ew;            // epilogue warps: 8 (two per TMEM lane quarter) or 4
+    int dbg;           // diagnostics (FP8B_CONV_HALO_DBG): 1 no slab loads, 2 no MMAs, 4 no epilogue work, 8 try_wait, 16 no tcgen05.commit, 32 no code stores,
+                       // 64 no code staging, 128 no Q node, 256 no TMEM loads, 512 no MMA loop
 };
 
-constexpr int EW = 4;
-constexpr int THREADS = 64 + 32 * EW;
+// 8 epilogue warps, two per TMEM lane quarter, each draining half of the
+// tile's columns: a tile is only a few hundred tensor cycles, and one warp per
+// SM sub-partition cannot hide the ALU latency of the output Q node (measured:
+// the epilogue alone took longer than loads + MMAs with 4 warps).
+// (4 when the layer's resident weights leave no room for 8 warps' staging.)
+constexpr int EW_MAX = 8;
+constexpr int THREADS_MAX = 64 + 32 * EW_MAX;
 
 // Shared-memory plan for CB-byte pixel rows and a BN-wide filter tile.
 template <int CB, int BN>
@@ -63,7 +71,11 @@ struct HGeo {
     static constexpr uint32_t W_TAP = (uint32_t)BN * CB;   // one tap's weights [BN x CB]
     static constexpr uint32_t SWZ = CB == 128 ? 2u : 4u;   // UMMA layout code
     static constexpr uint32_t SBO = 8u * CB;               // 8-row swizzle atom
-    static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    // A tile is only ~0.3-1 us of MMA work, so the MMA -> epilogue -> MMA
+    // handshake latency (commit, barrier wake-ups) would set the pace with a
+    // double-buffered accumulator: keep up to 8 tiles in flight in TMEM.
+    static constexpr int NACC = 512 / BN < 8 ? 512 / BN : 8;
+    static constexpr uint32_t TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
 };
 
 __device__ __forceinline__ uint64_t desc_bo(uint32_t saddr, uint32_t sbo, uint32_t layout,
@@ -138,7 +150,7 @@ __device__ __forceinline__ void codes_chunk(const P& p, const float (&y)[32], in
 // boxes {32 | qg * 32 columns, min(32, Wp) pixels, max(1, 32 / Wp) rows, 1}:
 // one box = one epilogue warp's 32 TMEM lanes for one column chunk.
 template <int ES, int CB, int BN>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS_MAX, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmQ,
                      const HParams p, uint32_t slab_bytes, int nstages) {
@@ -150,15 +162,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* wsm = smem;                                                       // resident weights
     uint8_t* ring = smem + (((uint32_t)taps * G::W_TAP + 1023u) & ~1023u);     // slab ring
     uint8_t* stg = ring + (uint32_t)nstages * slab_bytes;                      // p.stg bytes per epilogue warp
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stg + EW * p.stg);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stg + p.ew * p.stg);
     uint64_t* full_bar = bars;
     uint64_t* empty_bar = full_bar + nstages;
     uint64_t* tfull_bar = empty_bar + nstages;
-    uint64_t* tempty_bar = tfull_bar + 2;
-    uint64_t* w_bar = tempty_bar + 2;
+    uint64_t* tempty_bar = tfull_bar + G::NACC;
+    uint64_t* w_bar = tempty_bar + G::NACC;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // pipeline waits: busy-poll (test_wait) or try_wait (the thread may be
+    // suspended between polls)
+    auto hwait = [&](uint64_t* bar, uint32_t par) {
+        if (p.dbg & 8) mbar_wait(bar, par);
+        else mbar_wait_spin(bar, par);
+    };
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
@@ -166,9 +184,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(full_bar + s, 1);
             mbar_init(empty_bar + s, 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < G::NACC; ++a) {
             mbar_init(tfull_bar + a, 1);
-            mbar_init(tempty_bar + a, EW);
+            mbar_init(tempty_bar + a, p.ew);
         }
         mbar_init(w_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -196,9 +214,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
                 const int n = tile / p.tiles_per_img;
                 const int oh0 = (tile - n * p.tiles_per_img) * p.R;
-                mbar_wait(empty_bar + stage, phase ^ 1);
-                mbar_expect_tx(full_bar + stage, (uint32_t)p.SR * p.Wp * CB);
-                tma_load_4d(&tmX, ring + stage * slab_bytes, full_bar + stage, 0, -p.pad, oh0 - p.pad, n);
+                hwait(empty_bar + stage, phase ^ 1);
+                if (p.dbg & 1) {
+                    mbar_arrive(full_bar + stage);
+                } else {
+                    mbar_expect_tx(full_bar + stage, (uint32_t)p.SR * p.Wp * CB);
+                    tma_load_4d(&tmX, ring + stage * slab_bytes, full_bar + stage, 0, -p.pad, oh0 - p.pad, n);
+                }
                 if (++stage == nstages) { stage = 0; phase ^= 1; }
             }
         }
@@ -209,33 +231,51 @@ __global__ void __launch_bounds__(THREADS, 1)
         idesc |= (uint32_t)(BN >> 3) << 17;
         idesc |= (uint32_t)(128 >> 4) << 24;
         mbar_wait(w_bar, 0);
-        const uint32_t w0 = smem_u32(wsm);
+        // A tap's MMA is only 16-32 tensor cycles (N = 64..128), so the issue
+        // loop must be a handful of instructions per MMA: the descriptors of
+        // slab stage 0 / weight tap 0 are built once and only their 14-bit
+        // start-address field moves (32-bit adds of byte offset >> 4; shared
+        // memory < 256 KB, so it never carries out). The slab row offset of
+        // tap (kh, kw), (kh * Wp + kw) * CB, is advanced incrementally.
+        const uint64_t dA0 = desc_bo(smem_u32(ring), G::SBO, G::SWZ, 0);
+        const uint64_t dB0 = umma_desc(smem_u32(wsm), 16, G::SBO, G::SWZ);
+        const uint32_t aHi = (uint32_t)(dA0 >> 32), aLo0 = (uint32_t)dA0;
+        const uint32_t bHi = (uint32_t)(dB0 >> 32), bLo0 = (uint32_t)dB0;
+        const uint32_t row16 = CB >> 4;                                   // one slab row
+        const uint32_t wrap16 = (uint32_t)(p.Wp - p.k + 1) * row16;       // kw = k-1 -> next kh
+        const uint32_t issue = leader && !(p.dbg & 2) ? 1u : 0u;
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t accphase = 0;
         for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-            mbar_wait(tempty_bar + acc, accphase ^ 1);
+            hwait(tempty_bar + acc, accphase ^ 1);
             fence_after();
-            mbar_wait(full_bar + stage, phase);
+            hwait(full_bar + stage, phase);
             fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-            const uint32_t s0 = smem_u32(ring + stage * slab_bytes);
-            for (int t = 0; t < taps; ++t) {
-                const int kh = t / p.k, kw = t - kh * p.k;
-                const uint32_t a0 = s0 + (uint32_t)(kh * p.Wp + kw) * CB;  // row-shifted view
-                const uint32_t bo = p.bo_mode ? (a0 >> 7) & 7u : 0u;
+            uint32_t a_lo = aLo0 + (uint32_t)stage * (slab_bytes >> 4);
+            uint32_t b_lo = bLo0;
+            int kw = 0;
+#pragma unroll 1
+            for (int t = 0; t < ((p.dbg & 512) ? 0 : taps); ++t) {
 #pragma unroll
                 for (int kk = 0; kk < CB / 32; ++kk) {
-                    const uint64_t ad = desc_bo(a0 + 32 * kk, G::SBO, G::SWZ, bo);
-                    const uint64_t bd = umma_desc(w0 + t * G::W_TAP + 32 * kk, 16, G::SBO, G::SWZ);
-                    mma_p<ES>(d_tmem, ad, bd, idesc, (t | kk) ? 1u : 0u, leader);
+                    const uint64_t ad = ((uint64_t)aHi << 32) | (a_lo + 2u * kk);
+                    const uint64_t bd = ((uint64_t)bHi << 32) | (b_lo + 2u * kk);
+                    mma_p<ES>(d_tmem, ad, bd, idesc, (t | kk) ? 1u : 0u, issue);
                 }
+                b_lo += G::W_TAP >> 4;
+                if (++kw == p.k) { kw = 0; a_lo += wrap16; } else { a_lo += row16; }
             }
-            umma_commit_p(empty_bar + stage, leader);
-            umma_commit_p(tfull_bar + acc, leader);
+            if (p.dbg & 16) {  // diagnostic: plain arrivals instead of tcgen05.commit
+                if (lane == 0) { mbar_arrive(empty_bar + stage); mbar_arrive(tfull_bar + acc); }
+            } else {
+                umma_commit_p(empty_bar + stage, leader);
+                umma_commit_p(tfull_bar + acc, leader);
+            }
             if (++stage == nstages) { stage = 0; phase ^= 1; }
-            if (++acc == 2) { acc = 0; accphase ^= 1; }
+            if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
         }
     } else {
         // One warp = one TMEM lane quarter = 32 consecutive padded-row
@@ -243,6 +283,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         // column chunk leaves as one 4-D TMA store box (pad columns and rows
         // beyond the image are clipped by TMA; counters skip them).
         const int quarter = warp & 3;
+        const int CPW = BN / 32 / (p.ew / 4);            // column chunks per warp
+        const int c_lo = ((warp - 2) >> 2) * CPW;        // this warp's first chunk
         const int q = quarter * 32 + lane;
         const int r = q >> p.wlog, ow = q & ((1 << p.wlog) - 1);
         const int r0 = (quarter * 32) >> p.wlog, ow0 = (quarter * 32) & ((1 << p.wlog) - 1);
@@ -271,15 +313,20 @@ __global__ void __launch_bounds__(THREADS, 1)
             const bool live = ow < p.OW && oh0 + r < p.OH;
             const bool any = ow0 < p.OW && oh0 + r0 < p.OH;  // warp-uniform
             const int64_t pix = ((int64_t)n * p.OH + oh0 + r) * p.OW + ow;
-            mbar_wait(tfull_bar + acc, accphase);
+            hwait(tfull_bar + acc, accphase);
             fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
             int qpos = 0;
             uint8_t* qbuf = nullptr;
 #pragma unroll 1
-            for (int c = 0; any && c < BN / 32 && c * 32 < p.N; ++c) {
+            for (int c = c_lo; any && !(p.dbg & 4) && c < c_lo + CPW && c * 32 < p.N; ++c) {
                 uint32_t v[32];
-                tmem_ld32(taddr + c * 32, v);
+                if (p.dbg & 256) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = (uint32_t)(j * lane);
+                } else {
+                    tmem_ld32(taddr + c * 32, v);
+                }
                 const int col0 = c * 32;
                 const int nvalid = p.N - col0 < 32 ? (int)(p.N - col0) : 32;
                 float y[32];
@@ -290,7 +337,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int j = 0; j < 32; ++j)
                         if (j < nvalid) y[j] = __fadd_rn(y[j], __ldg(p.ep.bias + col0 + j));
                 }
-                const bool last = c == BN / 32 - 1 || col0 + 32 >= p.N;
+                const bool last = c == c_lo + CPW - 1 || col0 + 32 >= p.N;
                 if (p.c_tma) {
                     uint8_t* buf = acquire(cbase, nst_c, p.c_nbuf, 4096u);
                     stage_write<128, 32>(buf, 0, reinterpret_cast<const uint32_t*>(y), lane);
@@ -298,17 +345,24 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 if (p.q_tma) {
                     uint32_t w[16];  // 8 words of E5M2 codes or 16 of FP16
-                    codes_chunk(p, y, pix * p.N + col0, live, nvalid, w, co, cu, cn);
+                    if (p.dbg & 128) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) w[j] = v[j];
+                    } else {
+                        codes_chunk(p, y, pix * p.N + col0, live, nvalid, w, co, cu, cn);
+                    }
+                    if (p.dbg & 64) continue;
                     if (qpos == 0) qbuf = acquire(qbase, nst_q, p.q_nbuf, qbox);
                     if (p.ep.cq_fmt == FP8B_E5M2) {
                         if (p.qg == 4) stage_write<128, 8>(qbuf, qpos * 32, w, lane);
-                        else stage_write<64, 8>(qbuf, qpos * 32, w, lane);
+                        else if (p.qg == 2) stage_write<64, 8>(qbuf, qpos * 32, w, lane);
+                        else stage_write<32, 8>(qbuf, qpos * 32, w, lane);
                     } else {
                         if (p.qg == 2) stage_write<128, 16>(qbuf, qpos * 64, w, lane);
                         else stage_write<64, 16>(qbuf, qpos * 64, w, lane);
                     }
                     if (++qpos == p.qg || last) {
-                        tma_store_4d(&tmQ, qbuf, lane, col0 - 32 * (qpos - 1), ow0, oh0 + r0, n);
+                        if (!(p.dbg & 32)) tma_store_4d(&tmQ, qbuf, lane, col0 - 32 * (qpos - 1), ow0, oh0 + r0, n);
                         qpos = 0;
                     }
                 }
@@ -316,11 +370,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar + acc);
-            if (++acc == 2) { acc = 0; accphase ^= 1; }
+            if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
         }
         if (lane == 0) bulk_wait_all();
     }
-    if (p.ep.cq_counters) flush_counters<THREADS>(co, cu, cn, p.ep.cq_counters);
+    if (p.ep.cq_counters) flush_counters<THREADS_MAX>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -347,7 +401,7 @@ static bool make_slab_map(CUtensorMap* tm, const void* x, int es, int64_t n, int
 // Geometry check shared by the launcher and conv_halo_supported().
 struct Plan {
     int cb, bn, wp, r, sr, nstages;
-    int qg, stg, c_off, q_off, c_nbuf, q_nbuf;
+    int qg, stg, c_off, q_off, c_nbuf, q_nbuf, ew;
     uint32_t wbytes, slab, smem;
 };
 // need_c / q_fmt (-1: none): which outputs the epilogue stages.
@@ -371,27 +425,40 @@ static bool plan_for(int64_t n, int64_t h, int64_t w, int64_t c, int64_t f, int 
     pl.wbytes = (uint32_t)(k * k) * pl.bn * pl.cb;
     pl.slab = (((uint32_t)pl.sr * pl.wp * pl.cb) + 1023u) & ~1023u;
     const uint32_t wpad = (pl.wbytes + 1023u) & ~1023u;
-    // staging: rings of two boxes when they fit beside two slabs, else single
-    // boxes (and 64-byte code rows); FP32 box 4 KB, code box 32 x qg * 32 codes
+    // staging: 8 epilogue warps with rings of two boxes when they fit beside
+    // two slabs; else single boxes (c and q sharing one when both are
+    // written, codes flushed per chunk); else 4 warps.
     const int qes = q_fmt == FP8B_E5M2 ? 1 : 2;
     const bool need_q = q_fmt >= 0;
     const uint32_t base = 1024 + wpad + 256;
     bool fit = false;
-    for (int tight = 0; tight < 2 && !fit; ++tight) {
-        pl.qg = need_q ? tc::code_group(q_fmt, pl.bn) : 1;
-        if (tight && need_q && pl.qg * 32 * qes > 64) pl.qg = 64 / (32 * qes);
-        const uint32_t qbox = (uint32_t)pl.qg * 32 * qes * 32;
-        pl.c_nbuf = need_c ? ((need_q || tight) ? 1 : 2) : 0;
-        pl.q_nbuf = need_q ? ((need_c || tight) ? 1 : 2) : 0;
-        pl.c_off = 0;
-        pl.q_off = pl.c_nbuf * 4096;
-        pl.stg = pl.q_off + pl.q_nbuf * (int)qbox;
-        fit = base + EW * (uint32_t)pl.stg + 2 * pl.slab <= 232448u;
+    for (int ew = 8; ew >= 4 && !fit; ew -= 4) {
+        for (int tight = 0; tight < 2 && !fit; ++tight) {
+            pl.ew = ew;
+            pl.qg = need_q ? tc::code_group(q_fmt, pl.bn / (ew / 4)) : 1;  // a warp's columns
+            if (tight && need_q && need_c) pl.qg = 1;
+            const uint32_t qbox = (uint32_t)pl.qg * 32 * qes * 32;
+            if (!tight) {
+                pl.c_nbuf = need_c ? (need_q ? 1 : 2) : 0;
+                pl.q_nbuf = need_q ? (need_c ? 1 : 2) : 0;
+                pl.c_off = 0;
+                pl.q_off = pl.c_nbuf * 4096;
+                pl.stg = pl.q_off + pl.q_nbuf * (int)qbox;
+            } else {
+                pl.c_nbuf = need_c ? 1 : 0;
+                pl.q_nbuf = need_q ? 1 : 0;
+                pl.c_off = pl.q_off = 0;
+                pl.stg = need_c ? 4096 : (int)qbox;
+            }
+            fit = base + (uint32_t)ew * pl.stg + 2 * pl.slab <= 232448u;
+        }
     }
-    const uint32_t fixed = base + EW * (uint32_t)pl.stg;
+    const uint32_t fixed = base + (uint32_t)pl.ew * pl.stg;
     if (fixed + 2 * pl.slab > 232448u) return false;
     pl.nstages = (int)((232448u - fixed) / pl.slab);
-    if (pl.nstages > 4) pl.nstages = 4;
+    const char* ns = getenv("FP8B_CONV_HALO_STAGES");
+    const int cap = ns ? atoi(ns) : 4;
+    if (pl.nstages > cap) pl.nstages = cap;
     pl.smem = fixed + (uint32_t)pl.nstages * pl.slab;
     if (n * oh * ow >= ((int64_t)1 << 31)) return false;
     return true;
@@ -408,8 +475,9 @@ static bool make_out_map(CUtensorMap* tm, const void* out, int es, int64_t n, in
     cuuint32_t box[4] = {(cuuint32_t)cols, (cuuint32_t)(wp < 32 ? wp : 32), (cuuint32_t)(wp < 32 ? 32 / wp : 1), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     const int span = cols * es;
-    const CUtensorMapSwizzle swz = span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-    if (span != 64 && span != 128) return false;
+    const CUtensorMapSwizzle swz = span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                   : span == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    if (span != 32 && span != 64 && span != 128) return false;
     const CUtensorMapDataType dt = es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                    : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -424,7 +492,7 @@ static int run(const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& 
     ensure_smem_attr((const void*)fn, (int)pl.smem);
     const int sms = device_sm_count();
     const int grid = p.ntiles < sms ? p.ntiles : sms;
-    fn<<<grid, THREADS, pl.smem, st>>>(tx, tw, ty, tq, p, pl.slab, pl.nstages);
+    fn<<<grid, 64 + 32 * pl.ew, pl.smem, st>>>(tx, tw, ty, tq, p, pl.slab, pl.nstages);
     return cudaGetLastError() == cudaSuccess ? FP8B_OK : FP8B_ECUDA;
 }
 
@@ -467,8 +535,10 @@ int launch_conv_halo(const void* x, const void* wt, float* y, int es, int64_t n,
     p.ntiles = (int)(n * p.tiles_per_img);
     const char* bo = getenv("FP8B_CONV_HALO_BO");
     p.bo_mode = bo ? atoi(bo) : 0;
+    const char* dbg = getenv("FP8B_CONV_HALO_DBG");
+    p.dbg = dbg ? atoi(dbg) : 0;
     p.stg = pl.stg; p.c_off = pl.c_off; p.q_off = pl.q_off;
-    p.c_nbuf = pl.c_nbuf; p.q_nbuf = pl.q_nbuf;
+    p.c_nbuf = pl.c_nbuf; p.q_nbuf = pl.q_nbuf; p.ew = pl.ew;
     p.wlog = 0;
     while ((1 << p.wlog) < pl.wp) ++p.wlog;
     CUtensorMap ty, tq;
@@ -480,7 +550,7 @@ int launch_conv_halo(const void* x, const void* wt, float* y, int es, int64_t n,
     if (g.yq) {
         const int qes = g.yq_fmt == FP8B_E5M2 ? 1 : 2;
         p.qg = pl.qg;  // 64- or 128-byte code rows
-        if (p.qg * 32 * qes < 64) return FP8B_ENOTSUP;
+        if (p.qg * 32 * qes < 32) return FP8B_ENOTSUP;
         if (!make_out_map(&tq, g.yq, qes, n, oh, ow, f, p.qg * 32, pl.wp)) return FP8B_ENOTSUP;
     }
     if (es == 1) {

@@ -532,6 +532,20 @@ int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
     if (((uintptr_t)a % 16) || ((uintptr_t)b % 16)) return FP8B_ENOTSUP;
     const int k = (int)g.kh, pad = (int)g.pad;
     int rc;
+    // A 1x1 stride-1 unpadded NHWC conv is a plain GEMM on the tensors as they
+    // lie: e [P, F] (P = n*h*w pixels) and w [F, C]. Its dgrad runs on the
+    // pair-tile GEMM engine (dx [P, C] = e . w, B = w N-major: no weight flip
+    // pass), measured 1.3-1.5x faster than the im2col kernel at 14x14 / 7x7
+    // and on par at 56x56 / 28x28. fprop measured on par, wgrad (long K,
+    // M = F) far slower through the GEMM's split-K: both stay here.
+    // FP8B_CONV_1X1_GEMM=0 keeps dgrad here too.
+    const char* e1 = getenv("FP8B_CONV_1X1_GEMM");
+    if (kind == 1 && k == 1 && pad == 0 && g.stride == 1 && !(e1 && e1[0] == '0')) {
+        const EpiArgs ep{out, nullptr, g.yq, g.yq_fmt, g.yq_mode, g.yq_seed, g.yq_saturate, g.yq_counters};
+        rc = launch_gemm_tc(a, b, g.n * g.h * g.w, g.c, g.f, fmt, 0, 1, ep, st, nlaunch);
+        if (rc != FP8B_ENOTSUP) return rc;
+        *nlaunch = 0;
+    }
     if (kind == 0) {
         rc = fmt == FP8B_E5M2 ? tc::cv::fprop<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, g)
                               : tc::cv::fprop<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, g);

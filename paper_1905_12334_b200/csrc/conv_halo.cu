@@ -36,6 +36,25 @@ namespace fp8b {
 namespace tc {
 namespace halo {
 
+// Per-tile timeline trace (scripts/probe_halo.cu builds this file with
+// FP8B_HALO_TRACE): %globaltimer per CTA, role and tile.
+#ifdef FP8B_HALO_TRACE
+__device__ unsigned long long g_halo_trace[148 * 10 * 64];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define HTRACE(role, i)                                                                  \
+    do {                                                                                 \
+        if ((i) < 64 && blockIdx.x < 148) g_halo_trace[(blockIdx.x * 10 + (role)) * 64 + (i)] = gtimer(); \
+    } while (0)
+#else
+#define HTRACE(role, i) \
+    do {                \
+    } while (0)
+#endif
+
 struct HParams {
     int64_t M, N;      // output matrix [P, F] (P = n * OH * OW)
     EpiArgs ep;
@@ -53,7 +72,7 @@ struct HParams {
     // box(es) at q_off; *_nbuf = 2 is a ring of two boxes, 1 a single box
     int stg, c_off, q_off, c_nbuf, q_nbuf;
     int ew;            // epilogue warps: 8 (two per TMEM lane quarter) or 4
-    int dbg;           // diagnostics (FP8B_CONV_HALO_DBG): 1 no slab loads, 2 no MMAs, 4 no epilogue work, 8 try_wait, 16 no tcgen05.commit, 32 no code stores,
+    int dbg;           // diagnostics (FP8B_CONV_HALO_DBG): 1 no slab loads, 2 no MMAs, 4 no epilogue work, 8 busy-poll waits, 16 no tcgen05.commit, 32 no code stores,
                        // 64 no code staging, 128 no Q node, 256 no TMEM loads, 512 no MMA loop
 };
 
@@ -149,7 +168,9 @@ __device__ __forceinline__ void codes_chunk(const P& p, const float (&y)[32], in
 // tmY / tmQ: 4-D store maps over y [n, oh, ow, f] (FP32) / the output codes,
 // boxes {32 | qg * 32 columns, min(32, Wp) pixels, max(1, 32 / Wp) rows, 1}:
 // one box = one epilogue warp's 32 TMEM lanes for one column chunk.
-template <int ES, int CB, int BN>
+// KS: the kernel size when known at compile time (3: the tap loop fully
+// unrolled, every descriptor a constant offset), 0: any k at run time.
+template <int ES, int CB, int BN, int KS>
 __global__ void __launch_bounds__(THREADS_MAX, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmQ,
@@ -158,7 +179,8 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    const int taps = p.k * p.k;
+    const int kk_ = KS ? KS : p.k;  // kernel size
+    const int taps = kk_ * kk_;
     uint8_t* wsm = smem;                                                       // resident weights
     uint8_t* ring = smem + (((uint32_t)taps * G::W_TAP + 1023u) & ~1023u);     // slab ring
     uint8_t* stg = ring + (uint32_t)nstages * slab_bytes;                      // p.stg bytes per epilogue warp
@@ -171,11 +193,12 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // pipeline waits: busy-poll (test_wait) or try_wait (the thread may be
-    // suspended between polls)
+    // pipeline waits: try_wait (the thread may be suspended between polls, so
+    // waiting warps leave issue slots to the working ones), or busy-poll
+    // (test_wait, diagnostic)
     auto hwait = [&](uint64_t* bar, uint32_t par) {
-        if (p.dbg & 8) mbar_wait(bar, par);
-        else mbar_wait_spin(bar, par);
+        if (p.dbg & 8) mbar_wait_spin(bar, par);
+        else mbar_wait(bar, par);
     };
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
@@ -215,6 +238,7 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
                 const int n = tile / p.tiles_per_img;
                 const int oh0 = (tile - n * p.tiles_per_img) * p.R;
                 hwait(empty_bar + stage, phase ^ 1);
+                HTRACE(0, (tile - blockIdx.x) / gridDim.x);
                 if (p.dbg & 1) {
                     mbar_arrive(full_bar + stage);
                 } else {
@@ -242,7 +266,7 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
         const uint32_t aHi = (uint32_t)(dA0 >> 32), aLo0 = (uint32_t)dA0;
         const uint32_t bHi = (uint32_t)(dB0 >> 32), bLo0 = (uint32_t)dB0;
         const uint32_t row16 = CB >> 4;                                   // one slab row
-        const uint32_t wrap16 = (uint32_t)(p.Wp - p.k + 1) * row16;       // kw = k-1 -> next kh
+        const uint32_t wrap16 = (uint32_t)(p.Wp - kk_ + 1) * row16;       // kw = k-1 -> next kh
         const uint32_t issue = leader && !(p.dbg & 2) ? 1u : 0u;
         int stage = 0;
         uint32_t phase = 0;
@@ -251,27 +275,45 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
         for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             hwait(tempty_bar + acc, accphase ^ 1);
             fence_after();
+            if (lane == 0) HTRACE(1, (tile - blockIdx.x) / gridDim.x);
             hwait(full_bar + stage, phase);
             fence_after();
+            if (lane == 0) HTRACE(2, (tile - blockIdx.x) / gridDim.x);
             const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
             uint32_t a_lo = aLo0 + (uint32_t)stage * (slab_bytes >> 4);
-            uint32_t b_lo = bLo0;
-            int kw = 0;
-#pragma unroll 1
-            for (int t = 0; t < ((p.dbg & 512) ? 0 : taps); ++t) {
+            if constexpr (KS > 0) {
+                // all taps unrolled: tap (kh, kw) reads slab rows kh * Wp + kw on
 #pragma unroll
-                for (int kk = 0; kk < CB / 32; ++kk) {
-                    const uint64_t ad = ((uint64_t)aHi << 32) | (a_lo + 2u * kk);
-                    const uint64_t bd = ((uint64_t)bHi << 32) | (b_lo + 2u * kk);
-                    mma_p<ES>(d_tmem, ad, bd, idesc, (t | kk) ? 1u : 0u, issue);
+                for (int t = 0; t < KS * KS; ++t) {
+                    const uint32_t aoff = (uint32_t)((t / KS) * p.Wp + (t % KS)) * row16;
+#pragma unroll
+                    for (int kk = 0; kk < CB / 32; ++kk) {
+                        const uint64_t ad = ((uint64_t)aHi << 32) | (a_lo + aoff + 2u * kk);
+                        const uint64_t bd = ((uint64_t)bHi << 32) | (bLo0 + (uint32_t)t * (G::W_TAP >> 4) + 2u * kk);
+                        mma_p<ES>(d_tmem, ad, bd, idesc, (t | kk) ? 1u : 0u, issue);
+                    }
                 }
-                b_lo += G::W_TAP >> 4;
-                if (++kw == p.k) { kw = 0; a_lo += wrap16; } else { a_lo += row16; }
-            }
-            if (p.dbg & 16) {  // diagnostic: plain arrivals instead of tcgen05.commit
-                if (lane == 0) { mbar_arrive(empty_bar + stage); mbar_arrive(tfull_bar + acc); }
             } else {
-                umma_commit_p(empty_bar + stage, leader);
+                uint32_t b_lo = bLo0;
+                int kw = 0;
+#pragma unroll 1
+                for (int t = 0; t < ((p.dbg & 512) ? 0 : taps); ++t) {
+#pragma unroll
+                    for (int kk = 0; kk < CB / 32; ++kk) {
+                        const uint64_t ad = ((uint64_t)aHi << 32) | (a_lo + 2u * kk);
+                        const uint64_t bd = ((uint64_t)bHi << 32) | (b_lo + 2u * kk);
+                        mma_p<ES>(d_tmem, ad, bd, idesc, (t | kk) ? 1u : 0u, issue);
+                    }
+                    b_lo += G::W_TAP >> 4;
+                    if (++kw == kk_) { kw = 0; a_lo += wrap16; } else { a_lo += row16; }
+                }
+            }
+            if (lane == 0) HTRACE(3, (tile - blockIdx.x) / gridDim.x);
+            // one commit per tile: the epilogue releases the slab stage once it
+            // sees the accumulator complete (the MMAs that read it are done)
+            if (p.dbg & 16) {  // diagnostic: plain arrival instead of tcgen05.commit
+                if (lane == 0) mbar_arrive(tfull_bar + acc);
+            } else {
                 umma_commit_p(tfull_bar + acc, leader);
             }
             if (++stage == nstages) { stage = 0; phase ^= 1; }
@@ -294,6 +336,7 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
         uint8_t* qbase = stg + (warp - 2) * p.stg + p.q_off;
         const uint32_t qbox = (uint32_t)p.qg * 32 * (p.ep.cq_fmt == FP8B_E5M2 ? 1 : 2) * 32;
         uint32_t nst_c = 0, nst_q = 0;
+        int sstage = 0;  // slab stage of the current tile
         // next staging box of an output; its previous store must have read it
         // (one store may stay pending with a ring of two, none with one box)
         auto acquire = [&](uint8_t* base, uint32_t& nst, int nbuf, uint32_t box) {
@@ -315,6 +358,11 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
             const int64_t pix = ((int64_t)n * p.OH + oh0 + r) * p.OW + ow;
             hwait(tfull_bar + acc, accphase);
             fence_after();
+            if (warp == 2 && lane == 0) {
+                HTRACE(4, (tile - blockIdx.x) / gridDim.x);
+                mbar_arrive(empty_bar + sstage);  // the tile's MMAs are done with its slab
+            }
+            if (++sstage == nstages) sstage = 0;
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
             int qpos = 0;
             uint8_t* qbuf = nullptr;
@@ -327,6 +375,7 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
                 } else {
                     tmem_ld32(taddr + c * 32, v);
                 }
+                if (warp == 2 && lane == 0 && c == c_lo) HTRACE(6, (tile - blockIdx.x) / gridDim.x);
                 const int col0 = c * 32;
                 const int nvalid = p.N - col0 < 32 ? (int)(p.N - col0) : 32;
                 float y[32];
@@ -351,8 +400,10 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
                     } else {
                         codes_chunk(p, y, pix * p.N + col0, live, nvalid, w, co, cu, cn);
                     }
+                    if (warp == 2 && lane == 0 && c == c_lo) HTRACE(7, (tile - blockIdx.x) / gridDim.x);
                     if (p.dbg & 64) continue;
                     if (qpos == 0) qbuf = acquire(qbase, nst_q, p.q_nbuf, qbox);
+                    if (warp == 2 && lane == 0 && c == c_lo) HTRACE(8, (tile - blockIdx.x) / gridDim.x);
                     if (p.ep.cq_fmt == FP8B_E5M2) {
                         if (p.qg == 4) stage_write<128, 8>(qbuf, qpos * 32, w, lane);
                         else if (p.qg == 2) stage_write<64, 8>(qbuf, qpos * 32, w, lane);
@@ -370,6 +421,7 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar + acc);
+            if (warp == 2 && lane == 0) HTRACE(5, (tile - blockIdx.x) / gridDim.x);
             if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
         }
         if (lane == 0) bulk_wait_all();
@@ -488,7 +540,7 @@ static bool make_out_map(CUtensorMap* tm, const void* out, int es, int64_t n, in
 template <int ES, int CB, int BN>
 static int run(const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty, const CUtensorMap& tq,
                const HParams& p, const Plan& pl, cudaStream_t st) {
-    auto fn = conv_halo_kernel<ES, CB, BN>;
+    auto fn = p.k == 3 ? conv_halo_kernel<ES, CB, BN, 3> : conv_halo_kernel<ES, CB, BN, 0>;
     ensure_smem_attr((const void*)fn, (int)pl.smem);
     const int sms = device_sm_count();
     const int grid = p.ntiles < sms ? p.ntiles : sms;

@@ -10,8 +10,8 @@ P = nb * hw * hw
 xs = torch.empty(P * c, device="cuda"); F.fill_synthetic(xs, "halfnormal", 11, 1.0)
 ws = torch.empty(f * k * k * c, device="cuda"); F.fill_synthetic(ws, "normal", 12, (2.0 / (k * k * c)) ** 0.5)
 X = F.quantize(xs).reshaped([nb, hw, hw, c]); W = F.quantize(ws).reshaped([f, k, k, c])
-for q in (True,):
-    for dbg in ("519", "535", "519s8", "535s8", "4", "4s8", "0s8", "0"):
+for q in (False, True):
+    for dbg in ("0", "4", "7"):
         os.environ["FP8B_CONV_HALO_DBG"] = dbg.split("s")[0]
         os.environ["FP8B_CONV_HALO_STAGES"] = dbg.split("s")[1] if "s" in dbg else "4"
         kw = dict(layout="nhwc", engine="tensor")

@@ -534,13 +534,15 @@ int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
     int rc;
     // A 1x1 stride-1 unpadded NHWC conv is a plain GEMM on the tensors as they
     // lie: e [P, F] (P = n*h*w pixels) and w [F, C]. Its dgrad runs on the
-    // pair-tile GEMM engine (dx [P, C] = e . w, B = w N-major: no weight flip
-    // pass), measured 1.3-1.5x faster than the im2col kernel at 14x14 / 7x7
-    // and on par at 56x56 / 28x28. fprop measured on par, wgrad (long K,
-    // M = F) far slower through the GEMM's split-K: both stay here.
-    // FP8B_CONV_1X1_GEMM=0 keeps dgrad here too.
+    // pair-tile GEMM engine when P is small (dx [P, C] = e . w, B = w N-major:
+    // no weight flip pass): measured 1.3-1.5x faster than the im2col kernel at
+    // 14x14 / 7x7 (batch 256), but slower inside the training step at 56x56
+    // (0.074 -> 0.103 ms). fprop measured on par, wgrad (long K, M = F) far
+    // slower through the GEMM's split-K: both stay here.
+    // FP8B_CONV_1X1_GEMM=0 keeps dgrad here too, =1 forces the GEMM.
     const char* e1 = getenv("FP8B_CONV_1X1_GEMM");
-    if (kind == 1 && k == 1 && pad == 0 && g.stride == 1 && !(e1 && e1[0] == '0')) {
+    const bool gemm_1x1 = e1 && e1[0] ? e1[0] == '1' : g.n * g.h * g.w <= 65536;
+    if (kind == 1 && k == 1 && pad == 0 && g.stride == 1 && gemm_1x1) {
         const EpiArgs ep{out, nullptr, g.yq, g.yq_fmt, g.yq_mode, g.yq_seed, g.yq_saturate, g.yq_counters};
         rc = launch_gemm_tc(a, b, g.n * g.h * g.w, g.c, g.f, fmt, 0, 1, ep, st, nlaunch);
         if (rc != FP8B_ENOTSUP) return rc;

@@ -114,3 +114,36 @@ def test_halo_taken_for_resnet_layers(fp8):
     for shape in HALO_SHAPES:
         n, c, h, w, f, k, pad, fmt = shape
         assert fp8.conv_halo_supported(n, c, h, w, f, k, 1, pad, fmt, "fprop"), shape
+
+
+@pytest.mark.parametrize("shape", [(4, 256, 14, 14, 64), (2, 64, 7, 9, 512), (3, 128, 5, 6, 96)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("out", ["f32", "codes"])
+def test_1x1_dgrad_gemm_route_exact(fp8, shape, out):
+    """1x1 stride-1 dgrad routed to the pair-tile GEMM engine (dx = e . w, w
+    read N-major) equals the im2col kernel and the exact result bit for bit on
+    an exact operand grid, codes and counters included."""
+    n, c, h, w, f = shape
+    rng = np.random.default_rng(c + f)
+    wc = _grid(rng, f * c, "fp8", 0.25).reshape(f, 1, 1, c)
+    ec = _grid(rng, n * h * w * f, "fp8", 0.5).reshape(n, h, w, f)
+    dec = lambda a: O.dequantize(a.reshape(-1), "fp8").astype(np.float64).reshape(a.shape)
+    dx_ex = np.einsum("nhwf,fc->nhwc", dec(ec), dec(wc).reshape(f, c)).astype(np.float32)
+    W, E = _qt(fp8, wc, wc.shape, "fp8"), _qt(fp8, ec, ec.shape, "fp8")
+    codes, cnt = O.quantize(dx_ex.reshape(-1), "fp8", "nearest-even")
+    old = os.environ.get("FP8B_CONV_1X1_GEMM")
+    try:
+        for route in ("1", "0"):
+            os.environ["FP8B_CONV_1X1_GEMM"] = route
+            cdx = fp8.Counters()
+            dx, q = fp8.conv2d_backward_data(E, W, 1, 0, h, w, layout="nhwc", engine="tensor",
+                                             out_fmt="fp8", out_counters=cdx, want_y=out == "f32")
+            if out == "f32":
+                np.testing.assert_array_equal(dx.cpu().numpy().reshape(-1), dx_ex.reshape(-1))
+            np.testing.assert_array_equal(q.codes.cpu().numpy(), codes.astype(np.uint8))
+            assert cdx.values() == tuple(int(v) for v in cnt), route
+    finally:
+        if old is None:
+            os.environ.pop("FP8B_CONV_1X1_GEMM", None)
+        else:
+            os.environ["FP8B_CONV_1X1_GEMM"] = old

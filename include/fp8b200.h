@@ -252,7 +252,8 @@ int fp8b_conv2d_wgrad(const void *x, const void *e, float *dw, int32_t fmt,
 int fp8b_conv_tensor_supported(const fp8b_conv_t *g, int32_t fmt, int32_t kind);
 /* Extension (no reference counterpart): 1 if that tensor-engine conv runs the
  * weight-stationary halo-slab kernel (NHWC, stride 1, C * code bytes in {64,
- * 128}, F <= 256; kind 0 fprop, 1 dgrad), 0 if the im2col kernel. */
+ * 128}, F <= 256; kind 0 fprop, 1 dgrad; kind 2 wgrad: 3x3, E5M2, C = F =
+ * 64), 0 if the im2col kernel. */
 int fp8b_conv_halo_supported(const fp8b_conv_t *g, int32_t fmt, int32_t kind);
 
 /* im2col (kernels.hpp:25-30): pure code movement, zero code for padded taps.

@@ -348,9 +348,11 @@ int fp8b_conv_tensor_supported(const fp8b_conv_t* g, int32_t fmt, int32_t kind) 
     return fp8b::conv_tc_supported(kind, fmt, *g);
 }
 int fp8b_conv_halo_supported(const fp8b_conv_t* g, int32_t fmt, int32_t kind) {
-    if (!fp8b_conv_tensor_supported(g, fmt, kind) || kind > 1 || g->kh < 2) return 0;
+    if (!fp8b_conv_tensor_supported(g, fmt, kind) || g->kh < 2) return 0;
     const int es = fmt == FP8B_E5M2 ? 1 : 2;
     const int64_t oh = g->h + 2 * g->pad - g->kh + 1, ow = g->w + 2 * g->pad - g->kw + 1;
+    if (kind == 2)
+        return fp8b::conv_halo_wgrad_supported(es, g->n, g->h, g->w, g->c, g->f, (int)g->kh, (int)g->pad);
     if (kind == 0) return fp8b::conv_halo_supported(es, g->n, g->h, g->w, g->c, g->f, (int)g->kh, (int)g->pad);
     // dgrad = fprop over e [n, oh, ow, f] with the flipped weights, pad' = k - 1 - pad
     return fp8b::conv_halo_supported(es, g->n, oh, ow, g->f, g->c, (int)g->kh, (int)(g->kh - 1 - g->pad));

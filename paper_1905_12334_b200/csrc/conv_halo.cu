@@ -548,6 +548,161 @@ static int run(const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& 
     return cudaGetLastError() == cudaSuccess ? FP8B_OK : FP8B_ECUDA;
 }
 
+// ---------------------------------------------------------------------------
+// wgrad (conv2d_backward_weights_fp8, kernels.cpp:202-253) for E5M2 with
+// C = F = 64, k = 3: dW_t[f, c] = sum_p e[p, f] * x[p + off_t, c] over the
+// output pixels p. Per tile the CTA loads the same halo slab as fprop plus the
+// tile's error rows e (zero at the pad columns / beyond the image, TMA
+// out-of-bounds fill), and accumulates, for every pair of taps (t1, t2),
+//   D[128, F] = [x_t1 ; x_t2]^T . e
+// in one M=128 MMA chain: the A operand's two 64-row halves are the slab seen
+// from rows off_t1 and off_t2 (MN-major, the halves LBO = (off_t2 - off_t1) *
+// 64 bytes apart), B is the error tile (MN-major). The 5 pair accumulators
+// (320 TMEM columns) stay resident across all of the CTA's tiles; at the end
+// they are written as the CTA's FP32 partial [tap][c][f], and a fixed-order
+// sum over CTAs gives dW (deterministic).
+struct WParams {
+    int nimg, OH, OW, Wp, R, SR, pad, F, C;
+    int tiles_per_img, ntiles;
+    float* ws;  // [grid][9][C][F] partials
+};
+
+template <int ES>
+__global__ void __launch_bounds__(192, 1)
+    conv_halo_wgrad_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmE,
+                           const WParams p, uint32_t slab_bytes, uint32_t stage_bytes, int nstages) {
+    constexpr int KS = 3, TAPS = 9, NG = 5;  // tap pairs (0,1) (2,3) (4,5) (6,7) (8,-)
+    constexpr int CE = 64 / ES;              // channels (= filters) per 64-byte row
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + (uint32_t)nstages * stage_bytes);
+    uint64_t* empty_bar = full_bar + nstages;
+    uint64_t* done_bar = empty_bar + nstages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done_bar + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmE)) : "memory");
+        for (int s = 0; s < nstages; ++s) {
+            mbar_init(full_bar + s, 1);
+            mbar_init(empty_bar + s, 1);
+        }
+        mbar_init(done_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+                const int n = tile / p.tiles_per_img;
+                const int oh0 = (tile - n * p.tiles_per_img) * p.R;
+                mbar_wait(empty_bar + stage, phase ^ 1);
+                uint8_t* st = smem + stage * stage_bytes;
+                mbar_expect_tx(full_bar + stage, (uint32_t)p.SR * p.Wp * 64 + (uint32_t)p.R * p.Wp * 64);
+                tma_load_4d(&tmX, st, full_bar + stage, 0, -p.pad, oh0 - p.pad, n);
+                tma_load_4d(&tmE, st + slab_bytes, full_bar + stage, 0, 0, oh0, n);
+                if (++stage == nstages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t leader = elect_one();
+        uint32_t idesc = (1u << 4);
+        if (ES == 1) idesc |= (1u << 7) | (1u << 10);
+        idesc |= (1u << 15) | (1u << 16);  // A and B MN-major
+        idesc |= (uint32_t)(CE >> 3) << 17;  // N = F
+        idesc |= (uint32_t)(128 >> 4) << 24;
+        // K (pixels) advances 32 / ES rows of 64 bytes per MMA (swizzle atoms of 8 rows, SBO 512)
+        uint32_t lbo[NG], aoff[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const int t1 = 2 * g, t2 = 2 * g + 1 < TAPS ? 2 * g + 1 : 2 * g;
+            const int o1 = (t1 / KS) * p.Wp + t1 % KS, o2 = (t2 / KS) * p.Wp + t2 % KS + (t2 == t1 ? 1 : 0);
+            aoff[g] = (uint32_t)o1 * 64u;
+            lbo[g] = (uint32_t)(o2 - o1) * 64u;
+        }
+        int stage = 0;
+        uint32_t phase = 0;
+        bool first = true;
+        for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            mbar_wait(full_bar + stage, phase);
+            fence_after();
+            const uint32_t s0 = smem_u32(smem + stage * stage_bytes);
+            const uint32_t e0 = s0 + slab_bytes;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+#pragma unroll
+                for (int j = 0; j < 4 * ES; ++j) {  // K = 32 / ES pixels per MMA
+                    const uint64_t ad = umma_desc(s0 + aoff[g] + (uint32_t)j * (2048u / ES), lbo[g], 512, 4);
+                    const uint64_t bd = umma_desc(e0 + (uint32_t)j * (2048u / ES), 64, 512, 4);
+                    mma_p<ES>(tmem_base + (uint32_t)(g * 64), ad, bd, idesc, (first && j == 0) ? 0u : 1u, leader);
+                }
+            }
+            first = false;
+            umma_commit_p(empty_bar + stage, leader);
+            if (++stage == nstages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_p(done_bar, leader);
+    } else {
+        // epilogue warps 2-5 (TMEM lane quarters): TMEM lane l of pair g is
+        // channel l % 64 of tap 2g + l / 64
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int half = row >> 6, c = row & 63;
+        mbar_wait(done_bar, 0);
+        fence_after();
+        const bool any = p.ntiles > (int)blockIdx.x;
+#pragma unroll 1
+        for (int g = 0; g < NG; ++g) {
+            const int t = 2 * g + half;
+#pragma unroll
+            for (int cc = 0; cc < CE / 32; ++cc) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(g * 64 + cc * 32), v);
+                if (t < TAPS && c < p.C) {
+                    float* dst = p.ws + (((size_t)blockIdx.x * TAPS + t) * p.C + c) * p.F + cc * 32;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        reinterpret_cast<float4*>(dst)[q] =
+                            any ? make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                              __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+// dw [f, kh, kw, c] = sum over CTAs b (ascending) of ws[b][t][c][f]
+__global__ void conv_halo_wgrad_sum(const float* __restrict__ ws, float* __restrict__ dw, int nb, int C,
+                                   int F) {
+    const int total = 9 * C * F;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int f = i % F, tc = i / F;  // ws order: [t][c][f]
+        float s = 0.f;
+        for (int b = 0; b < nb; ++b) s = __fadd_rn(s, ws[(size_t)b * total + i]);
+        const int t = tc / C, c = tc - t * C;
+        dw[((size_t)f * 9 + t) * C + c] = s;
+    }
+}
+
 }  // namespace halo
 }  // namespace tc
 
@@ -623,6 +778,69 @@ int launch_conv_halo(const void* x, const void* wt, float* y, int es, int64_t n,
     if (pl.bn == 64) return run<2, 128, 64>(tx, tw, ty, tq, p, pl, st);
     if (pl.bn == 128) return run<2, 128, 128>(tx, tw, ty, tq, p, pl, st);
     return run<2, 128, 256>(tx, tw, ty, tq, p, pl, st);
+}
+
+bool conv_halo_wgrad_supported(int es, int64_t n, int64_t h, int64_t w, int64_t c, int64_t f, int k,
+                               int pad) {
+    const char* e = getenv("FP8B_CONV_HALO");
+    if (e && e[0] == '0') return false;
+    // E5M2 only: a tap half of the M=128 accumulator is one 64-byte row of 64
+    // channels (FP16 rows hold 32, which would need 4 taps per accumulator)
+    if (es != 1 || k != 3 || c != 64 || f != 64 || pad < 0 || pad > 2) return false;
+    if (w + 2 * pad > 128 || h + 2 * pad - k + 1 < 1 || w + 2 * pad - k + 1 < 1) return false;
+    return n * h * w < ((int64_t)1 << 31);
+}
+
+// wgrad over NHWC x [n, h, w, c] and e [n, oh, ow, f] -> dw [f, 3, 3, c] (FP32).
+int launch_conv_halo_wgrad(const void* x, const void* e, float* dw, int es, int64_t n, int64_t h,
+                           int64_t w, int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl) {
+    using namespace tc::halo;
+    if (!conv_halo_wgrad_supported(es, n, h, w, c, f, k, pad)) return FP8B_ENOTSUP;
+    if ((uintptr_t)x % 16 || (uintptr_t)e % 16 || !dw) return FP8B_ENOTSUP;
+    const int64_t oh = h + 2 * pad - k + 1, ow = w + 2 * pad - k + 1;
+    int wp = 1;
+    while (wp < w + 2 * pad) wp <<= 1;
+    const int r = 128 / wp;
+    const int sr = (128 + (k - 1) * (wp + 1) + wp - 1) / wp;
+    CUtensorMap tx, te;
+    if (!make_slab_map(&tx, x, es, n, h, w, c, wp, sr)) return FP8B_ENOTSUP;
+    {
+        tc::EncodeTiledFn enc = tc::get_encode();
+        if (!enc) return FP8B_ENOTSUP;
+        cuuint64_t dims[4] = {(cuuint64_t)f, (cuuint64_t)ow, (cuuint64_t)oh, (cuuint64_t)n};
+        cuuint64_t strides[3] = {(cuuint64_t)(f * es), (cuuint64_t)(ow * f * es), (cuuint64_t)(oh * ow * f * es)};
+        cuuint32_t box[4] = {(cuuint32_t)f, (cuuint32_t)wp, (cuuint32_t)r, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (enc(&te, es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4,
+                const_cast<void*>(e), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return FP8B_ENOTSUP;
+    }
+    const uint32_t slab = (((uint32_t)sr * wp * 64) + 1023u) & ~1023u;
+    const uint32_t stage = slab + ((((uint32_t)r * wp * 64) + 1023u) & ~1023u);
+    int nstages = (int)((232448u - 2048u) / stage);
+    if (nstages > 4) nstages = 4;
+    if (nstages < 2) return FP8B_ENOTSUP;
+    const uint32_t smem = 1024 + (uint32_t)nstages * stage + 256;
+    WParams p{};
+    p.nimg = (int)n; p.OH = (int)oh; p.OW = (int)ow; p.Wp = wp; p.R = r; p.SR = sr; p.pad = pad;
+    p.F = (int)f; p.C = (int)c;
+    p.tiles_per_img = (int)((oh + r - 1) / r);
+    p.ntiles = (int)(n * p.tiles_per_img);
+    const int sms = device_sm_count();
+    const int grid = p.ntiles < sms ? p.ntiles : sms;
+    const size_t part = (size_t)9 * c * f;
+    if (cudaMallocAsync(&p.ws, (size_t)grid * part * sizeof(float), st) != cudaSuccess) return FP8B_ECUDA;
+    auto fn = es == 1 ? conv_halo_wgrad_kernel<1> : conv_halo_wgrad_kernel<2>;
+    ensure_smem_attr((const void*)fn, (int)smem);
+    fn<<<grid, 192, smem, st>>>(tx, te, p, slab, stage, nstages);
+    int b = (int)((part + 255) / 256);
+    if (b > 4 * sms) b = 4 * sms;
+    conv_halo_wgrad_sum<<<b, 256, 0, st>>>(p.ws, dw, grid, (int)c, (int)f);
+    cudaFreeAsync(p.ws, st);
+    *nl = 2;
+    return cudaGetLastError() == cudaSuccess ? FP8B_OK : FP8B_ECUDA;
 }
 
 }  // namespace fp8b

@@ -439,6 +439,10 @@ static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, i
 template <int ES>
 static int wgrad(const void* x, const void* e, float* dw, int64_t n, int64_t h, int64_t wd,
                  int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl) {
+    {  // 3x3 with 64-byte channel and filter rows: the halo-slab wgrad
+        const int rc = launch_conv_halo_wgrad(x, e, dw, ES, n, h, wd, c, f, k, pad, st, nl);
+        if (rc != FP8B_ENOTSUP) return rc;
+    }
     const int cb_bytes = (c * ES) % 128 == 0 ? 128 : ((c * ES) % 64 == 0 ? 64 : 0);
     if (!cb_bytes || (f * ES) % 16) return FP8B_ENOTSUP;
     const int64_t oh = h + 2 * pad - k + 1, ow = wd + 2 * pad - k + 1;

@@ -56,6 +56,11 @@ bool conv_halo_supported(int es, int64_t n, int64_t h, int64_t w, int64_t c, int
 int launch_conv_halo(const void* x, const void* wt, float* y, int es, int64_t n, int64_t h,
                      int64_t w, int64_t c, int64_t f, int k, int pad, const fp8b_conv_t& g,
                      cudaStream_t st);
+// Halo-slab wgrad (conv_halo.cu): 3x3, C * bytes == F * bytes == 64.
+bool conv_halo_wgrad_supported(int es, int64_t n, int64_t h, int64_t w, int64_t c, int64_t f, int k,
+                               int pad);
+int launch_conv_halo_wgrad(const void* x, const void* e, float* dw, int es, int64_t n, int64_t h,
+                           int64_t w, int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl);
 void launch_im2col(const void* x, void* cols, int fmt, const fp8b_conv_t& g, cudaStream_t st);
 // Per-device setup (several GPUs per process are allowed): SM count of the
 // current device, and the >48 KB dynamic shared memory opt-in of a kernel on

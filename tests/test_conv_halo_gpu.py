@@ -110,7 +110,9 @@ def test_halo_taken_for_resnet_layers(fp8):
         for kind in ("fprop", "dgrad"):
             assert fp8.conv_halo_supported(256, c, hw, hw, c, 3, 1, 1, "fp8", kind)
     assert not fp8.conv_halo_supported(256, 256, 14, 14, 256, 3, 1, 1, "fp8", "fprop")
-    assert not fp8.conv_halo_supported(256, 64, 56, 56, 64, 3, 1, 1, "fp8", "wgrad")
+    assert fp8.conv_halo_supported(256, 64, 56, 56, 64, 3, 1, 1, "fp8", "wgrad")
+    assert not fp8.conv_halo_supported(256, 128, 28, 28, 128, 3, 1, 1, "fp8", "wgrad")
+    assert not fp8.conv_halo_supported(2, 32, 14, 14, 32, 3, 1, 1, "fp16", "wgrad")
     for shape in HALO_SHAPES:
         n, c, h, w, f, k, pad, fmt = shape
         assert fp8.conv_halo_supported(n, c, h, w, f, k, 1, pad, fmt, "fprop"), shape
@@ -147,3 +149,42 @@ def test_1x1_dgrad_gemm_route_exact(fp8, shape, out):
             os.environ.pop("FP8B_CONV_1X1_GEMM", None)
         else:
             os.environ["FP8B_CONV_1X1_GEMM"] = old
+
+
+WGRAD_SHAPES = [  # n, c, h, w, f, pad, fmt  (3x3, 64-byte channel / filter rows)
+    (2, 64, 56, 56, 64, 1, "fp8"),   # ResNet-50 3x3 @56 (2 rows per tile)
+    (3, 64, 13, 9, 64, 1, "fp8"),    # ragged last tile
+    (2, 64, 10, 30, 64, 0, "fp8"),   # no padding
+    (1, 64, 6, 126, 64, 1, "fp8"),   # Wp = 128: one row per tile
+    (300, 64, 7, 7, 64, 1, "fp8"),   # more tiles than SMs, tiny images
+]
+
+
+@pytest.mark.parametrize("shape", WGRAD_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_halo_wgrad_exact_grid(fp8, env, shape):
+    """Halo-slab wgrad (tap-pair accumulators resident in TMEM, fixed-order sum
+    over CTAs) == the im2col wgrad == the exact result, bit for bit, on an
+    exact operand grid; fused output Q node and counters included."""
+    n, c, h, w, f, pad, fmt = shape
+    k = 3
+    assert fp8.conv_halo_supported(n, c, h, w, f, k, 1, pad, fmt, "wgrad")
+    oh, ow = h + 2 * pad - k + 1, w + 2 * pad - k + 1
+    rng = np.random.default_rng(n + h + w + pad)
+    xc = _grid(rng, n * h * w * c, fmt, 0.5).reshape(n, h, w, c)
+    ec = _grid(rng, n * oh * ow * f, fmt, 0.25).reshape(n, oh, ow, f)
+    dec = lambda a: O.dequantize(a.reshape(-1), fmt).astype(np.float64).reshape(a.shape)
+    from numpy.lib.stride_tricks import sliding_window_view as swv
+    xp = np.pad(dec(xc), ((0, 0), (pad, pad), (pad, pad), (0, 0)))
+    win = swv(xp, (k, k), axis=(1, 2))
+    dw_ex = np.einsum("nhwf,nhwcij->fijc", dec(ec), win, optimize=True).astype(np.float32)
+    X, E = _qt(fp8, xc, xc.shape, fmt), _qt(fp8, ec, ec.shape, fmt)
+    codes, cnt = O.quantize(dw_ex.reshape(-1), "fp8", "nearest-even")
+    for halo in ("1", "0"):
+        env["FP8B_CONV_HALO"] = halo
+        cq = fp8.Counters()
+        dw, q = fp8.conv2d_backward_weights(X, E, k, k, 1, pad, layout="nhwc", engine="tensor",
+                                            out_fmt="fp8", out_counters=cq)
+        np.testing.assert_array_equal(dw.cpu().numpy().reshape(-1), dw_ex.reshape(-1),
+                                      err_msg=f"halo={halo}")
+        np.testing.assert_array_equal(q.codes.cpu().numpy(), codes.astype(np.uint8))
+        assert cq.values() == tuple(int(v) for v in cnt), halo

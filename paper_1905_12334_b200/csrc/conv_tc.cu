@@ -537,18 +537,26 @@ int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
     const int k = (int)g.kh, pad = (int)g.pad;
     int rc;
     // A 1x1 stride-1 unpadded NHWC conv is a plain GEMM on the tensors as they
-    // lie: e [P, F] (P = n*h*w pixels) and w [F, C]. Its dgrad runs on the
-    // pair-tile GEMM engine when P is small (dx [P, C] = e . w, B = w N-major:
-    // no weight flip pass): measured 1.3-1.5x faster than the im2col kernel at
-    // 14x14 / 7x7 (batch 256), but slower inside the training step at 56x56
-    // (0.074 -> 0.103 ms). fprop measured on par, wgrad (long K, M = F) far
-    // slower through the GEMM's split-K: both stay here.
-    // FP8B_CONV_1X1_GEMM=0 keeps dgrad here too, =1 forces the GEMM.
+    // lie: x [P, C], e [P, F] (P = n*h*w pixels), w [F, C]. fprop (y = x . w^T,
+    // w K-major) and dgrad (dx = e . w, w N-major: no weight flip pass) run on
+    // the pair-tile GEMM engine when their output has >= 256 channels (the
+    // 256-wide pair tile is full): measured in the config-4 step, 1x1 64->256
+    // @56 0.254 -> 0.238 ms, 128->512 @28 0.160 -> 0.138 ms, while 64-channel
+    // outputs lose (256->64 @56 0.260 -> 0.348 ms) and stay here. dgrad only
+    // for up to 256K pixels: beside the step's concurrent wgrad the persistent
+    // GEMM loses at 56x56 (0.260 -> 0.284 ms), wins at 28x28 (512->128: 0.157
+    // -> 0.134 ms), 14x14 and 7x7. wgrad
+    // (long K, M = F) is far slower through the GEMM's split-K and stays.
+    // FP8B_CONV_1X1_GEMM=0 / 1 disables / forces the routing.
     const char* e1 = getenv("FP8B_CONV_1X1_GEMM");
-    const bool gemm_1x1 = e1 && e1[0] ? e1[0] == '1' : g.n * g.h * g.w <= 65536;
-    if (kind == 1 && k == 1 && pad == 0 && g.stride == 1 && gemm_1x1) {
+    const int64_t nout = kind == 0 ? g.f : g.c;
+    const bool gemm_1x1 = e1 && e1[0] ? e1[0] == '1'
+                                      : nout >= 256 && (kind == 0 || g.n * g.h * g.w <= 262144);
+    if (kind != 2 && k == 1 && pad == 0 && g.stride == 1 && gemm_1x1) {
         const EpiArgs ep{out, nullptr, g.yq, g.yq_fmt, g.yq_mode, g.yq_seed, g.yq_saturate, g.yq_counters};
-        rc = launch_gemm_tc(a, b, g.n * g.h * g.w, g.c, g.f, fmt, 0, 1, ep, st, nlaunch);
+        const int64_t P = g.n * g.h * g.w;
+        rc = kind == 0 ? launch_gemm_tc(a, b, P, g.f, g.c, fmt, 0, 0, ep, st, nlaunch)
+                       : launch_gemm_tc(a, b, P, g.c, g.f, fmt, 0, 1, ep, st, nlaunch);
         if (rc != FP8B_ENOTSUP) return rc;
         *nlaunch = 0;
     }

@@ -118,32 +118,39 @@ def test_halo_taken_for_resnet_layers(fp8):
         assert fp8.conv_halo_supported(n, c, h, w, f, k, 1, pad, fmt, "fprop"), shape
 
 
-@pytest.mark.parametrize("shape", [(4, 256, 14, 14, 64), (2, 64, 7, 9, 512), (3, 128, 5, 6, 96)],
-                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("shape", [(4, 256, 14, 14, 64), (2, 64, 7, 9, 512), (3, 128, 5, 6, 96),
+                                   (2, 64, 12, 11, 256)], ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("out", ["f32", "codes"])
-def test_1x1_dgrad_gemm_route_exact(fp8, shape, out):
-    """1x1 stride-1 dgrad routed to the pair-tile GEMM engine (dx = e . w, w
-    read N-major) equals the im2col kernel and the exact result bit for bit on
-    an exact operand grid, codes and counters included."""
+def test_1x1_gemm_route_exact(fp8, shape, out):
+    """1x1 stride-1 fprop and dgrad routed to the pair-tile GEMM engine (y = x .
+    w^T with w K-major, dx = e . w with w N-major) equal the im2col kernel and
+    the exact result bit for bit on an exact operand grid, codes and counters
+    included."""
     n, c, h, w, f = shape
     rng = np.random.default_rng(c + f)
     wc = _grid(rng, f * c, "fp8", 0.25).reshape(f, 1, 1, c)
+    xc = _grid(rng, n * h * w * c, "fp8", 0.5).reshape(n, h, w, c)
     ec = _grid(rng, n * h * w * f, "fp8", 0.5).reshape(n, h, w, f)
     dec = lambda a: O.dequantize(a.reshape(-1), "fp8").astype(np.float64).reshape(a.shape)
+    y_ex = np.einsum("nhwc,fc->nhwf", dec(xc), dec(wc).reshape(f, c)).astype(np.float32)
     dx_ex = np.einsum("nhwf,fc->nhwc", dec(ec), dec(wc).reshape(f, c)).astype(np.float32)
-    W, E = _qt(fp8, wc, wc.shape, "fp8"), _qt(fp8, ec, ec.shape, "fp8")
-    codes, cnt = O.quantize(dx_ex.reshape(-1), "fp8", "nearest-even")
+    X, W, E = _qt(fp8, xc, xc.shape, "fp8"), _qt(fp8, wc, wc.shape, "fp8"), _qt(fp8, ec, ec.shape, "fp8")
     old = os.environ.get("FP8B_CONV_1X1_GEMM")
     try:
         for route in ("1", "0"):
             os.environ["FP8B_CONV_1X1_GEMM"] = route
-            cdx = fp8.Counters()
-            dx, q = fp8.conv2d_backward_data(E, W, 1, 0, h, w, layout="nhwc", engine="tensor",
-                                             out_fmt="fp8", out_counters=cdx, want_y=out == "f32")
-            if out == "f32":
-                np.testing.assert_array_equal(dx.cpu().numpy().reshape(-1), dx_ex.reshape(-1))
-            np.testing.assert_array_equal(q.codes.cpu().numpy(), codes.astype(np.uint8))
-            assert cdx.values() == tuple(int(v) for v in cnt), route
+            for name, call, ex in [
+                ("fprop", lambda **a: fp8.conv2d(X, W, 1, 0, **a), y_ex),
+                ("dgrad", lambda **a: fp8.conv2d_backward_data(E, W, 1, 0, h, w, **a), dx_ex),
+            ]:
+                cnt = fp8.Counters()
+                t, q = call(layout="nhwc", engine="tensor", out_fmt="fp8", out_counters=cnt,
+                            want_y=out == "f32")
+                codes, k_ = O.quantize(ex.reshape(-1), "fp8", "nearest-even")
+                if out == "f32":
+                    np.testing.assert_array_equal(t.cpu().numpy().reshape(-1), ex.reshape(-1))
+                np.testing.assert_array_equal(q.codes.cpu().numpy(), codes.astype(np.uint8))
+                assert cnt.values() == tuple(int(v) for v in k_), (route, name)
     finally:
         if old is None:
             os.environ.pop("FP8B_CONV_1X1_GEMM", None)

@@ -121,6 +121,14 @@ int device_sm_count() {
     sms[dev] = v;
     return v;
 }
+int64_t lfsr_cta_max_blocks() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("FP8B_LFSR_CTA_MAX");
+        v = e ? atoll(e) : 2 * (int64_t)device_sm_count();
+    }
+    return v;
+}
 void ensure_smem_attr(const void* fn, int bytes) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return;

@@ -67,6 +67,12 @@ void launch_im2col(const void* x, void* cols, int fmt, const fp8b_conv_t& g, cud
 // the current device, each done once per (kernel, device).
 int device_sm_count();
 void ensure_smem_attr(const void* fn, int bytes);
+// Reference-stream SR (LFSR blocks): tensors of at most this many 4096-blocks
+// take the CTA-per-block kernels (all of a block's loads in flight at once)
+// instead of the warp-per-block ones, whose 16-chunk chain per block and
+// 139 KB table copy per CTA only pay off with many blocks per SM.
+// FP8B_LFSR_CTA_MAX overrides it (A/B).
+int64_t lfsr_cta_max_blocks();
 // Adds n to the library's launch counter (fp8b_launch_count).
 void note_launches(int n);
 void launch_fill_synthetic(float* out, int64_t n, int kind, uint64_t seed, double p, double lo,

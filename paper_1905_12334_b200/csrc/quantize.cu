@@ -533,7 +533,7 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
         // the warp kernel stores EPL codes per lane as one 8- or 16-byte word
         constexpr int kLfsrStoreAlign =
             FP8B_LFSR_EPL * (MB == 2 ? 1 : 2) < 16 ? FP8B_LFSR_EPL * (MB == 2 ? 1 : 2) : 16;
-        if (aligned && (uintptr_t)codes % kLfsrStoreAlign == 0) {
+        if (aligned && (uintptr_t)codes % kLfsrStoreAlign == 0 && n / kBlock > lfsr_cta_max_blocks()) {
             const int64_t nfull = n / kBlock;
             if (nfull > 0) {
                 auto fn = quant_lfsr_warp_kernel<MB>;

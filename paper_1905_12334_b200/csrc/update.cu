@@ -462,7 +462,7 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     if (args.master_mode == FP8B_SR && args.bits == FP8B_BITS_LFSR) {
         const int64_t nb = (n + kBlock - 1) / kBlock;
         int64_t begin = 0;
-        if (aligned && n / kBlock > 0) {
+        if (aligned && n / kBlock > lfsr_cta_max_blocks()) {
             const int64_t nfull = n / kBlock;
             constexpr int smem = kUpdTabBytes;
             auto fn = cnt ? sgd_lfsr_warp_kernel<GFMT, true> : sgd_lfsr_warp_kernel<GFMT, false>;

@@ -39,6 +39,41 @@ METRIC = "FP8 E5M2 quantize sweep GB/s & % HBM BW (config 2: RNE + LFSR-SR E5M2 
 BYTES_PER_ELEM = {"e5m2_rne": 5, "e5m2_sr_lfsr": 5, "fp16_sr_counter": 6}
 
 
+def _config(args, world):
+    """The workload description both arms print (the driver compares them)."""
+    return {"workload": "config2: quantize sweep 2^%d FP32 per GPU x {E5M2 RNE, E5M2 SR "
+                        "(reference LFSR stream), FP16 SR (counter bits)}" % args.log2n,
+            "elements_per_gpu": 1 << args.log2n, "bytes_per_elem": BYTES_PER_ELEM,
+            "l2": "no flush: inputs 1 GiB per GPU > 126 MB L2",
+            "parallelism": f"data-sharded x{world}, no collective"}
+
+
+def _mix64(z):
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def _config2_host(n, seed=0, p=0.01, lo=-24.0, hi=17.0):
+    """Host twin of csrc/synth.cu's config-2 generator (same hash, same
+    distribution: |x| = 2^U[lo,hi], random sign, a fraction p of exact E5M2
+    ties), for the reference arm, which has no GPU to generate on."""
+    with np.errstate(over="ignore"):
+        i = np.arange(n, dtype=np.uint64)
+        h1 = _mix64(np.uint64((seed * 0x2545F4914F6CDD1D) & (2**64 - 1)) + np.uint64(2) * i + np.uint64(1))
+        h2 = _mix64(h1 ^ np.uint64(0xD6E8FEB86659FD93))
+    u1 = (h1 >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    u2 = (h2 >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    v = np.exp2(lo + (hi - lo) * u2).astype(np.float32)
+    tie = u1 < p
+    c = (h2[tie] % np.uint64(0x7B)).astype(np.uint16)
+    dec = lambda k: (k.astype(np.uint16) << np.uint16(8)).view(np.float16).astype(np.float32)  # noqa: E731
+    v[tie] = np.float32(0.5) * (dec(c) + dec(c + np.uint16(1)))
+    neg = (h1 & np.uint64(1)).astype(bool)
+    v[neg] = -v[neg]
+    return v
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -185,11 +220,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32->e5m2/fp16",
         "data": "synthetic (seeded, generated in HBM; SURVEY 8d config-2 distribution)",
-        "config": {"workload": "config2: quantize sweep 2^%d FP32 per GPU x {E5M2 RNE, E5M2 SR "
-                               "(reference LFSR stream), FP16 SR (counter bits)}" % args.log2n,
-                   "elements_per_gpu": n, "bytes_per_elem": BYTES_PER_ELEM,
-                   "l2": "no flush: inputs 1 GiB per GPU > 126 MB L2",
-                   "parallelism": f"data-sharded x{world}, no collective"},
+        "config": _config(args, world),
         "kernels_ms_per_step": {k: round(v / args.steps, 4) for k, v in kt.items()},
         "kernels_gbs": {k: round(v, 1) for k, v in kernel_gbs.items()},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(kernel_gbs[dom], 1),
@@ -769,9 +800,8 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle as O
-    ns = 1 << args.cpu_log2n
-    rng = np.random.default_rng(0)
-    x = (np.exp2(rng.uniform(-24, 17, ns)) * rng.choice([-1.0, 1.0], ns)).astype(np.float32)
+    ns = 1 << min(args.ref_log2n, args.log2n)
+    x = _config2_host(ns, seed=0)  # the first 2^ref_log2n values of rank 0's input
     cores = os.cpu_count() or 1
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
@@ -789,15 +819,17 @@ def run_reference(args):
         step()
     dt = time.perf_counter() - t0
     value = ns * sum(BYTES_PER_ELEM.values()) * args.steps / dt / 1e9
-    sample = (f"2^{args.cpu_log2n} elements per step (bounded sample of the 2^{args.log2n} "
-              "workload); reference encode()+LfsrStream::split, block-parallel over 4096-blocks")
+    sample = (f"2^{min(args.ref_log2n, args.log2n)} elements per step (bounded sample: the first "
+              f"values of the 2^{args.log2n} workload, same generator); reference "
+              "encode()+LfsrStream::split, block-parallel over 4096-blocks; all three sweeps "
+              "(the FP16 SR sweep draws from the reference LFSR stream, the only bit source the "
+              "reference has)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32->e5m2/fp16", "data": "synthetic",
-        "config": {"workload": "config2 (same three sweeps) on host cores",
-                   "elements_per_step": ns},
+        "config": _config(args, world),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -814,6 +846,8 @@ def main():
     ap.add_argument("--log2n", type=int, default=28)
     ap.add_argument("--e2e-log2n", type=int, default=28)
     ap.add_argument("--cpu-log2n", type=int, default=27)
+    ap.add_argument("--ref-log2n", type=int, default=25,
+                    help="reference arm: elements per timed step (bounded sample)")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--conv-batch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -439,4 +439,64 @@ __device__ __forceinline__ uint32_t gather_f16(uint32_t s0, uint32_t s1, uint32_
     return __byte_perm(s0, s1, 0x7632) | (__byte_perm(u0, u1, 0x7632) & 0x80008000u);
 }
 
+// ---- small PTX helpers that keep ptxas from carrying long-lived predicates --
+// One step of an inclusive warp scan (shfl.up): the shuffle's in-range predicate
+// guards the add, so no (lane >= d) predicate is held.
+__device__ __forceinline__ uint32_t scan_step_up(uint32_t v, int d) {
+    uint32_t r;
+    asm volatile(
+        "{\n"
+        ".reg .u32 t;\n"
+        ".reg .pred p;\n"
+        "shfl.sync.up.b32 t|p, %1, %2, 0, 0xffffffff;\n"
+        "@p add.u32 t, t, %1;\n"
+        "mov.u32 %0, t;\n"
+        "}\n"
+        : "=r"(r)
+        : "r"(v), "r"(d));
+    return r;
+}
+// f > maxv or NaN: count it and return `special` instead of f.
+__device__ __forceinline__ float clamp_big(float f, float maxv, float special, uint32_t& cnt) {
+    float r;
+    asm("{\n"
+        ".reg .pred p;\n"
+        "setp.gtu.f32 p, %2, %3;\n"
+        "@p add.u32 %0, %0, 1;\n"
+        "selp.f32 %1, %4, %2, p;\n"
+        "}\n"
+        : "+r"(cnt), "=f"(r)
+        : "f"(f), "f"(maxv), "f"(special));
+    return r;
+}
+// m | bit if f > thr (ordered: false for NaN), as a compare plus one predicated OR.
+__device__ __forceinline__ uint32_t or_if_gt(uint32_t m, float f, float thr, uint32_t bit) {
+    asm("{\n"
+        ".reg .pred p;\n"
+        "setp.gt.f32 p, %1, %2;\n"
+        "@p or.b32 %0, %0, %3;\n"
+        "}\n"
+        : "+r"(m)
+        : "f"(f), "f"(thr), "r"(bit));
+    return m;
+}
+// f > thr or unordered: returns the predicate and counts it with one predicated add.
+__device__ __forceinline__ bool count_gtu(float f, float thr, uint32_t& cnt) {
+    uint32_t r;
+    asm("{\n"
+        ".reg .pred p;\n"
+        "setp.gtu.f32 p, %2, %3;\n"
+        "@p add.u32 %0, %0, 1;\n"
+        "selp.u32 %1, 1, 0, p;\n"
+        "}\n"
+        : "+r"(cnt), "=r"(r)
+        : "f"(f), "f"(thr));
+    return r != 0u;
+}
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
 }  // namespace fp8b

@@ -23,7 +23,127 @@ namespace fp8b {
 // ---------------------------------------------------------------------------
 // Position-independent quantize.
 // MODE: 0 RNE (hardware cvt), 1 SR counter bits, 2 SR supplied bits, 3 TRUNC
-template <int MB, int MODE, int NT>
+// One float4 group g -> one code word (E5M2) or two (FP16).
+template <int MB, int MODE>
+__device__ __forceinline__ void quant_group(const float4& v, const uint32_t (&rb)[4], int64_t g,
+                                            void* __restrict__ codes, uint64_t seed, bool sat,
+                                            int64_t elem_offset, uint32_t& c_big, uint32_t& c_nan,
+                                            uint32_t& c_unf) {
+    const float f[4] = {v.x, v.y, v.z, v.w};
+    uint32_t c[4];
+    if (MODE == 0 && MB == 2) {
+        // E5M2 RNE on whole code words. The hardware cvt (satfinite)
+        // returns the max code 0x7B for every |x| > 57344 (Inf included),
+        // so the reference's overflow rule (float_format.cpp:104-108) is
+        // "+1 on the code byte" (0x7B -> the Inf code 0x7C) unless
+        // saturating; underflow = zero-magnitude codes minus exact-zero
+        // inputs; NaN (rare) rewrites its byte to the canonical 0x7E.
+        const uint32_t p01 = cvt_e5m2x2(f[0], f[1]);
+        const uint32_t p23 = cvt_e5m2x2(f[2], f[3]);
+        uint32_t w = __byte_perm(p01, p23, 0x5410);
+        uint32_t m = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m = or_if_gt(m, fabsf(f[k]), 57344.0f, 1u << (8 * k));
+        c_big += __popc(m);
+        c_unf += zero_mags<0x7F7F7F7Fu>(w);
+        if (!sat) w += m;
+        const float amax = fmax_nan(fmax_nan(fabsf(f[0]), fabsf(f[1])), fmax_nan(fabsf(f[2]), fabsf(f[3])));
+        const float amin = fminf(fminf(fabsf(f[0]), fabsf(f[1])), fminf(fabsf(f[2]), fabsf(f[3])));
+        if (amin == 0.0f) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) c_unf -= (__float_as_uint(f[k]) << 1) == 0u;
+        }
+        if (amax != amax) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (f[k] != f[k]) {
+                    ++c_nan;
+                    w = (w & ~(0xFFu << (8 * k))) | ((uint32_t)Fmt<MB>::nancode << (8 * k));
+                }
+        }
+        __stcs(reinterpret_cast<uint32_t*>(codes) + g, w);
+        return;
+    }
+    if (MODE == 0) {
+        if (MB == 2) {
+            const uint32_t p01 = cvt_e5m2x2(f[0], f[1]);
+            const uint32_t p23 = cvt_e5m2x2(f[2], f[3]);
+            c[0] = p01 & 0xFFu; c[1] = p01 >> 8; c[2] = p23 & 0xFFu; c[3] = p23 >> 8;
+        } else {
+            const uint32_t hw01 = cvt_f16x2(f[0], f[1]);
+            const uint32_t hw23 = cvt_f16x2(f[2], f[3]);
+            c[0] = hw01 & 0xFFFFu; c[1] = hw01 >> 16; c[2] = hw23 & 0xFFFFu; c[3] = hw23 >> 16;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            c[k] = fix_rne<MB>(c[k], __float_as_uint(f[k]), sat, c_big, c_nan, c_unf);
+    } else {
+        // SR / TRUNC on the packed representation. Screens: amax
+        // (NaN-propagating) for overflow / NaN inputs, amin for an exact
+        // zero input; underflow = code magnitude 0 from a nonzero input,
+        // counted on the packed output words.
+        uint64_t word = 0;
+        if (MODE == 1) word = counter_word(seed, (uint64_t)((elem_offset >> 2) + g));
+        uint32_t r16[4] = {0u, 0u, 0u, 0u};  // TRUNC == SR with r16 = 0
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (MODE == 1) r16[k] = (uint32_t)(word >> (16 * k)) & 0xFFFFu;
+            if (MODE == 2) r16[k] = rb[k];
+        }
+        const float amax = fmax_nan(fmax_nan(fabsf(f[0]), fabsf(f[1])), fmax_nan(fabsf(f[2]), fabsf(f[3])));
+        const float amin = fminf(fminf(fabsf(f[0]), fabsf(f[1])), fminf(fabsf(f[2]), fabsf(f[3])));
+        uint32_t sum[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // overflow (Inf / max code) or NaN: select, no branch
+            const bool big = count_gtu(fabsf(f[k]), MB == 2 ? 57344.0f : 65504.0f, c_big);
+            sum[k] = (big ? special_packed<MB>(sat) : packed_sr<MB>(f[k])) + r16[k];
+        }
+        const uint32_t u[4] = {__float_as_uint(f[0]), __float_as_uint(f[1]),
+                               __float_as_uint(f[2]), __float_as_uint(f[3])};
+        uint32_t w0, w1 = 0;
+        if (MB == 2) {
+            w0 = gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]);
+            c_unf += zero_mags<0x7F7F7F7Fu>(w0);
+            if (amin == 0.0f) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c_unf -= (u[k] << 1) == 0u;
+            }
+        } else {
+            w0 = gather_f16(sum[0], sum[1], u[0], u[1]);
+            w1 = gather_f16(sum[2], sum[3], u[2], u[3]);
+            // an FP16 code magnitude of 0 needs |x| < 2^-24 (the min subnormal)
+            if (amin < 0x1p-24f) {
+                c_unf += zero_mags<0x7FFF7FFFu>(w0) + zero_mags<0x7FFF7FFFu>(w1);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c_unf -= (u[k] << 1) == 0u;
+            }
+        }
+        if (amax != amax) {  // rare: NaN -> canonical unsigned code (float_format.cpp:99)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (f[k] != f[k]) {
+                    ++c_nan;
+                    if (MB == 2) w0 = (w0 & ~(0xFFu << (8 * k))) | ((uint32_t)Fmt<MB>::nancode << (8 * k));
+                    else if (k < 2) w0 = (w0 & ~(0xFFFFu << (16 * k))) | ((uint32_t)Fmt<MB>::nancode << (16 * k));
+                    else w1 = (w1 & ~(0xFFFFu << (16 * (k - 2)))) | ((uint32_t)Fmt<MB>::nancode << (16 * (k - 2)));
+                }
+        }
+        if (MB == 2) __stcs(reinterpret_cast<uint32_t*>(codes) + g, w0);
+        else __stcs(reinterpret_cast<uint2*>(codes) + g, make_uint2(w0, w1));
+        return;
+    }
+    if (MB == 2) {
+        const uint32_t w = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+        __stcs(reinterpret_cast<uint32_t*>(codes) + g, w);
+    } else {
+        const uint2 w = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+        __stcs(reinterpret_cast<uint2*>(codes) + g, w);
+    }
+}
+
+// UN float4 groups per thread per pass (CTA-contiguous), optionally loaded one
+// pass ahead (PF: ping-pong register sets, no copies).
+template <int MB, int MODE, int NT, int UN = 4, int PF = 0>
 __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict__ x,
                                                         void* __restrict__ codes, int64_t n,
                                                         uint64_t seed, int saturate,
@@ -33,103 +153,49 @@ __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict_
     const bool sat = saturate != 0;
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int64_t ngroups = n >> 2;  // float4 groups
-    const int64_t stride = (int64_t)gridDim.x * NT * 4;
+    const int64_t stride = (int64_t)gridDim.x * NT * UN;
     const float4* x4 = reinterpret_cast<const float4*>(x);
-    for (int64_t g0 = (int64_t)blockIdx.x * NT * 4 + threadIdx.x; g0 < ngroups; g0 += stride) {
-        float4 v[4];
-        bool ok[4];
+    const uint4* r4 = reinterpret_cast<const uint4*>(rbits);
+    auto load = [&](int64_t g0, float4 (&v)[UN], uint4 (&r)[UN]) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < UN; ++j) {
             const int64_t g = g0 + (int64_t)j * NT;
-            ok[j] = g < ngroups;
-            if (ok[j]) v[j] = __ldcs(x4 + g);
+            if (g < ngroups) {
+                v[j] = __ldcs(x4 + g);
+                if (MODE == 2) r[j] = __ldcs(r4 + g);
+            }
         }
-        uint32_t rb[4][4];
-        if (MODE == 2) {
+    };
+    auto work = [&](int64_t g0, const float4 (&v)[UN], const uint4 (&r)[UN]) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (ok[j]) {
-                    const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rbits) + g0 + (int64_t)j * NT);
-                    rb[j][0] = r.x >> 16; rb[j][1] = r.y >> 16; rb[j][2] = r.z >> 16; rb[j][3] = r.w >> 16;
-                }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (!ok[j]) continue;
+        for (int j = 0; j < UN; ++j) {
             const int64_t g = g0 + (int64_t)j * NT;
-            const float f[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-            uint32_t c[4];
-            if (MODE == 0) {
-                if (MB == 2) {
-                    const uint32_t p01 = cvt_e5m2x2(f[0], f[1]);
-                    const uint32_t p23 = cvt_e5m2x2(f[2], f[3]);
-                    c[0] = p01 & 0xFFu; c[1] = p01 >> 8; c[2] = p23 & 0xFFu; c[3] = p23 >> 8;
-                } else {
-                    const uint32_t hw01 = cvt_f16x2(f[0], f[1]);
-                    const uint32_t hw23 = cvt_f16x2(f[2], f[3]);
-                    c[0] = hw01 & 0xFFFFu; c[1] = hw01 >> 16; c[2] = hw23 & 0xFFFFu; c[3] = hw23 >> 16;
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    c[k] = fix_rne<MB>(c[k], __float_as_uint(f[k]), sat, c_big, c_nan, c_unf);
-            } else {
-                // SR / TRUNC on the packed representation. Screens: amax
-                // (NaN-propagating) for overflow / NaN inputs, amin for an exact
-                // zero input; underflow = code magnitude 0 from a nonzero input,
-                // counted on the packed output words.
-                uint64_t word = 0;
-                if (MODE == 1) word = counter_word(seed, (uint64_t)((elem_offset >> 2) + g));
-                uint32_t r16[4] = {0u, 0u, 0u, 0u};  // TRUNC == SR with r16 = 0
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (MODE == 1) r16[k] = (uint32_t)(word >> (16 * k)) & 0xFFFFu;
-                    if (MODE == 2) r16[k] = rb[j][k];
-                }
-                const float amax = fmax_nan(fmax_nan(fabsf(f[0]), fabsf(f[1])), fmax_nan(fabsf(f[2]), fabsf(f[3])));
-                const float amin = fminf(fminf(fabsf(f[0]), fabsf(f[1])), fminf(fabsf(f[2]), fabsf(f[3])));
-                uint32_t sum[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {  // overflow (Inf / max code) or NaN: select, no branch
-                    const bool big = big_or_nan<MB>(f[k]);
-                    c_big += big;
-                    sum[k] = (big ? special_packed<MB>(sat) : packed_sr<MB>(f[k])) + r16[k];
-                }
-                const uint32_t u[4] = {__float_as_uint(f[0]), __float_as_uint(f[1]),
-                                       __float_as_uint(f[2]), __float_as_uint(f[3])};
-                uint32_t w0, w1 = 0;
-                if (MB == 2) {
-                    w0 = gather_e5m2(sum[0], sum[1], sum[2], sum[3], u[0], u[1], u[2], u[3]);
-                    c_unf += zero_mags<0x7F7F7F7Fu>(w0);
-                } else {
-                    w0 = gather_f16(sum[0], sum[1], u[0], u[1]);
-                    w1 = gather_f16(sum[2], sum[3], u[2], u[3]);
-                    c_unf += zero_mags<0x7FFF7FFFu>(w0) + zero_mags<0x7FFF7FFFu>(w1);
-                }
-                if (amin == 0.0f) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) c_unf -= (u[k] << 1) == 0u;
-                }
-                if (amax != amax) {  // rare: NaN -> canonical unsigned code (float_format.cpp:99)
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (f[k] != f[k]) {
-                            ++c_nan;
-                            if (MB == 2) w0 = (w0 & ~(0xFFu << (8 * k))) | ((uint32_t)Fmt<MB>::nancode << (8 * k));
-                            else if (k < 2) w0 = (w0 & ~(0xFFFFu << (16 * k))) | ((uint32_t)Fmt<MB>::nancode << (16 * k));
-                            else w1 = (w1 & ~(0xFFFFu << (16 * (k - 2)))) | ((uint32_t)Fmt<MB>::nancode << (16 * (k - 2)));
-                        }
-                }
-                if (MB == 2) __stcs(reinterpret_cast<uint32_t*>(codes) + g, w0);
-                else __stcs(reinterpret_cast<uint2*>(codes) + g, make_uint2(w0, w1));
-                continue;
-            }
-            if (MB == 2) {
-                const uint32_t w = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-                __stcs(reinterpret_cast<uint32_t*>(codes) + g, w);
-            } else {
-                const uint2 w = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
-                __stcs(reinterpret_cast<uint2*>(codes) + g, w);
-            }
+            if (g >= ngroups) continue;
+            uint32_t rb[4] = {0u, 0u, 0u, 0u};
+            if (MODE == 2) { rb[0] = r[j].x >> 16; rb[1] = r[j].y >> 16; rb[2] = r[j].z >> 16; rb[3] = r[j].w >> 16; }
+            quant_group<MB, MODE>(v[j], rb, g, codes, seed, sat, elem_offset, c_big, c_nan, c_unf);
+        }
+    };
+    int64_t g0 = (int64_t)blockIdx.x * NT * UN + threadIdx.x;
+    if (PF == 0) {
+        for (; g0 < ngroups; g0 += stride) {
+            float4 v[UN];
+            uint4 r[UN];
+            load(g0, v, r);
+            work(g0, v, r);
+        }
+    } else {
+        float4 va[UN], vb[UN];
+        uint4 ra[UN], rb2[UN];
+        if (g0 < ngroups) load(g0, va, ra);
+        while (g0 < ngroups) {
+            if (g0 + stride < ngroups) load(g0 + stride, vb, rb2);
+            work(g0, va, ra);
+            g0 += stride;
+            if (g0 >= ngroups) break;
+            if (g0 + stride < ngroups) load(g0 + stride, va, ra);
+            work(g0, vb, rb2);
+            g0 += stride;
         }
     }
     // scalar tail (n % 4) handled by the first threads of block 0
@@ -142,11 +208,12 @@ __global__ void __launch_bounds__(NT) quant_elem_kernel(const float* __restrict_
         int o, un, na;
         const int mode = MODE == 0 ? FP8B_RNE : (MODE == 3 ? FP8B_TRUNC : FP8B_SR);
         const uint32_t c = encode_int<MB>(u, mode, r16, sat, o, un, na);
-        c_big += o + na; c_nan += na; c_unf += un;
+        c_big += o + ((MODE == 0 && MB == 2) ? 0 : na); c_nan += na; c_unf += un;
         if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i] = (uint8_t)c;
         else reinterpret_cast<uint16_t*>(codes)[i] = (uint16_t)c;
     }
-    if (counters) flush_counters<NT>(c_big - c_nan, c_unf, c_nan, counters);
+    // c_big includes NaN inputs except on the E5M2 RNE word path (ordered compare)
+    if (counters) flush_counters<NT>((MODE == 0 && MB == 2) ? c_big : c_big - c_nan, c_unf, c_nan, counters);
 }
 
 // ---------------------------------------------------------------------------
@@ -232,7 +299,8 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t tab_bar;
     const bool sat = saturate != 0;
-    const uint32_t special_code = special_packed<MB>(sat);
+    // |x| whose packed SR form is the overflow code with no discarded bits
+    const float special_val = sat ? (MB == 2 ? 57344.0f : 65504.0f) : 65536.0f;
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -273,36 +341,30 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
                 u[4 * q + 3] = __float_as_uint(v[q].w);
             }
             uint32_t P[EPL], inc[EPL], n = 0;
-            // screen: amax (NaN-propagating) catches overflow / NaN inputs
-            float amax = fabsf(__uint_as_float(u[0]));
+            // Overflow / NaN inputs, branch-free: at warp granularity they are
+            // not rare (config 2: 2.9 % of elements, i.e. nearly every warp's
+            // chunk), so a lane-divergent fixup path ran for every chunk. The
+            // input magnitude is replaced by the value whose packed form is the
+            // reference's overflow code (2^16 -> Inf code, or the max normal
+            // when saturating) with zero discarded bits: no sample is taken.
+            float amax = fabsf(__uint_as_float(u[0]));  // NaN-propagating: NaN screen only
 #pragma unroll
             for (int k = 0; k < EPL; ++k) {
-                const float f = __uint_as_float(u[k]);
-                if (k) amax = fmax_nan(amax, fabsf(f));
-                P[k] = packed_sr<MB>(f);
-                inc[k] = inexact_sr<MB>(f) ? 2u : 0u;  // byte stride in the table
+                const float f = fabsf(__uint_as_float(u[k]));
+                if (k) amax = fmax_nan(amax, f);
+                const float fa = clamp_big(f, MB == 2 ? 57344.0f : 65504.0f, special_val, c_big);
+                P[k] = packed_sr<MB>(fa);
+                inc[k] = inexact_sr<MB>(fa) ? 2u : 0u;  // byte stride in the table
             }
-            // rare: an overflowing or NaN input in this lane -> the reference's
-            // overflow code (Inf / max when saturating) and no sample taken
-            bool has_nan = false;
-            if (!(amax <= (MB == 2 ? 57344.0f : 65504.0f))) {
-#pragma unroll
-                for (int k = 0; k < EPL; ++k) {
-                    const bool big = big_or_nan<MB>(__uint_as_float(u[k]));
-                    c_big += big;
-                    has_nan |= (u[k] & 0x7FFFFFFFu) > 0x7F800000u;
-                    if (big) { P[k] = special_code; inc[k] = 0u; }
-                }
-            }
+            const bool has_nan = amax != amax;
 #pragma unroll
             for (int k = 0; k < EPL; ++k) n += inc[k];
-            // inclusive warp scan of the lanes' sample bytes
+            // inclusive warp scan of the lanes' sample bytes; the shuffle's own
+            // in-range predicate guards the add (no lane >= d predicates kept
+            // live across the chunk)
             uint32_t incl = n;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                if (lane >= d) incl += o;
-            }
+            for (int d = 1; d < 32; d <<= 1) incl = scan_step_up(incl, d);
             const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
             uint32_t addr = run + incl - n;
             run += total;
@@ -313,8 +375,7 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
                 addr += inc[k];
                 P[k] += r16;  // exact lanes ignore their sample
                 // underflow: inexact and rounded to zero; exact lanes pushed out of range
-                const uint32_t chk = P[k] + (2u - inc[k]) * 0x8000u;
-                c_unf += (chk - 0x10000u) >> 31;
+                c_unf += mad_lo(inc[k], 0xFFFF8000u, P[k]) >> 31;  // P - (inexact ? 2^16 : 0) < 0
             }
             const int64_t e0 = b * kBlock + CH * c + EPL * lane;  // first element of this lane
             if (MB == 2) {
@@ -523,8 +584,6 @@ static int grid_for(const void* fn, int nt, int64_t work_items) {
 template <int MB>
 static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quant_config_t& cfg,
                          int64_t* counters, cudaStream_t st, const LfsrTables& tabs) {
-    constexpr int NT = 256;
-    const int64_t groups16 = (n / 4 + NT * 4 - 1) / (NT * 4);
     const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)codes % (MB == 2 ? 4 : 8) == 0) &&
                          (cfg.rbits == nullptr || (uintptr_t)cfg.rbits % 16 == 0);
     if (cfg.mode == FP8B_SR && cfg.bits == FP8B_BITS_LFSR) {
@@ -567,17 +626,39 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
                               cfg.rbits, counters);
         return;
     }
-#define FP8B_LAUNCH_ELEM(MODE)                                                             \
-    {                                                                                      \
-        auto fn = quant_elem_kernel<MB, MODE, NT>;                                         \
-        const int g = grid_for((const void*)fn, NT, groups16);                             \
-        fn<<<g, NT, 0, st>>>(x, codes, n, cfg.seed, cfg.saturate, eoff, cfg.rbits, counters); \
+    // Groups per thread / CTA size, measured on one B200 (scripts/quant_var.py,
+    // 2^28 config-2 values): these kernels want occupancy, not per-thread
+    // prefetch depth. E5M2 RNE 2 groups x 256 threads (8 CTAs/SM): 6.30 ->
+    // 6.62 TB/s; FP16 counter-SR likewise 5.98 -> 6.15; E5M2 counter-SR 4 groups
+    // x 512 threads 5.45 -> 5.60; one-pass-ahead register prefetch loses 3-15 %.
+    // FP8B_QELEM_VAR (diagnostic) forces: 1 = 2 groups, 2 = 4 groups + prefetch,
+    // 3 = 2 groups + prefetch, 4 = 512 threads, 5 = 512 x 2 + prefetch, 6 = 256 x 4.
+    static const int var = [] { const char* e = getenv("FP8B_QELEM_VAR"); return e ? atoi(e) : 0; }();
+#define FP8B_LAUNCH_V(MODE, TN, UN, PF)                                                       \
+    {                                                                                          \
+        auto fn = quant_elem_kernel<MB, MODE, TN, UN, PF>;                                     \
+        const int64_t items = (n / 4 + TN * UN - 1) / (TN * UN);                               \
+        const int g = grid_for((const void*)fn, TN, items);                                    \
+        fn<<<g, TN, 0, st>>>(x, codes, n, cfg.seed, cfg.saturate, eoff, cfg.rbits, counters);  \
+    }
+#define FP8B_LAUNCH_ELEM(MODE)                                                  \
+    {                                                                           \
+        if (var == 1) FP8B_LAUNCH_V(MODE, 256, 2, 0)                            \
+        else if (var == 2) FP8B_LAUNCH_V(MODE, 256, 4, 1)                       \
+        else if (var == 3) FP8B_LAUNCH_V(MODE, 256, 2, 1)                       \
+        else if (var == 4) FP8B_LAUNCH_V(MODE, 512, 4, 0)                       \
+        else if (var == 5) FP8B_LAUNCH_V(MODE, 512, 2, 1)                       \
+        else if (var == 6) FP8B_LAUNCH_V(MODE, 256, 4, 0)                       \
+        else if (MODE == 0 || (MODE == 1 && MB == 10)) FP8B_LAUNCH_V(MODE, 256, 2, 0) \
+        else if (MODE == 1) FP8B_LAUNCH_V(MODE, 512, 4, 0)                      \
+        else FP8B_LAUNCH_V(MODE, 256, 4, 0)                                     \
     }
     if (cfg.mode == FP8B_RNE) FP8B_LAUNCH_ELEM(0)
     else if (cfg.mode == FP8B_TRUNC) FP8B_LAUNCH_ELEM(3)
     else if (cfg.bits == FP8B_BITS_COUNTER) FP8B_LAUNCH_ELEM(1)
     else FP8B_LAUNCH_ELEM(2)
 #undef FP8B_LAUNCH_ELEM
+#undef FP8B_LAUNCH_V
 }
 
 void launch_quantize(const float* x, void* codes, int64_t n, int fmt,

@@ -17,6 +17,8 @@ import sys
 
 BENCH_KEYS = {
     "quant_elem_kernel<2, 0, 256>": "e5m2_rne",
+    "quant_elem_kernel<2, 0, 256, 2, 0>": "e5m2_rne",
+    "quant_elem_kernel<10, 1, 256, 2, 0>": "fp16_sr_counter",
     "quant_lfsr_warp_kernel<2>": "e5m2_sr_lfsr",
     "quant_elem_kernel<10, 1, 256>": "fp16_sr_counter",
 }

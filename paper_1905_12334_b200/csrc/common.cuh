@@ -115,6 +115,21 @@ __device__ __forceinline__ uint32_t cvt_e5m2x2(float lo, float hi) {
     return r;
 }
 
+// Four floats -> one word of four E5M2 RNE codes (satfinite hardware cvt): the
+// two 16-bit results are packed by one mov.b32 (no zero-extension masks).
+__device__ __forceinline__ uint32_t cvt_e5m2x4(float f0, float f1, float f2, float f3) {
+    uint32_t r;
+    asm("{\n"
+        ".reg .b16 lo, hi;\n"
+        "cvt.rn.satfinite.e5m2x2.f32 lo, %2, %1;\n"
+        "cvt.rn.satfinite.e5m2x2.f32 hi, %4, %3;\n"
+        "mov.b32 %0, {lo, hi};\n"
+        "}\n"
+        : "=r"(r)
+        : "f"(f0), "f"(f1), "f"(f2), "f"(f3));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t cvt_f16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

@@ -163,6 +163,12 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
 
     // item -> (tile, split) and its K-block range
     auto item_of = [&](int item, int& tm, int& tn, int& s, int& kb0, int& kb1) {
+        if (p.splits == 1) {  // no integer divisions on the per-tile path of every warp
+            s = 0; kb0 = 0; kb1 = p.num_kb;
+            if (p.tiles_n == 1) { tm = item; tn = 0; }
+            else tile_coords(item, p.tiles_m, p.tiles_n, tm, tn);
+            return;
+        }
         const int tile = item / p.splits;
         s = item - tile * p.splits;
         tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
@@ -541,17 +547,19 @@ int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
     // w K-major) and dgrad (dx = e . w, w N-major: no weight flip pass) run on
     // the pair-tile GEMM engine when their output has >= 256 channels (the
     // 256-wide pair tile is full): measured in the config-4 step, 1x1 64->256
-    // @56 0.254 -> 0.238 ms, 128->512 @28 0.160 -> 0.138 ms, while 64-channel
-    // outputs lose (256->64 @56 0.260 -> 0.348 ms) and stay here. dgrad only
-    // for up to 256K pixels: beside the step's concurrent wgrad the persistent
-    // GEMM loses at 56x56 (0.260 -> 0.284 ms), wins at 28x28 (512->128: 0.157
-    // -> 0.134 ms), 14x14 and 7x7. wgrad
+    // @56 0.254 -> 0.213 ms (with the GEMM's 16-warp short-K epilogue), 128->512
+    // @28 0.160 -> 0.134 ms, while 64-channel outputs lose (256->64 @56 0.260 ->
+    // 0.348 ms) and stay here. dgrad likewise at every pixel count since the
+    // 16-warp epilogue (256->64 @56: dgrad 121 -> 81 us, layer step 0.256 -> 0.228
+    // ms; FP8B_CONV_1X1_DGRAD_PIX caps the pixel count, diagnostic). wgrad
     // (long K, M = F) is far slower through the GEMM's split-K and stays.
     // FP8B_CONV_1X1_GEMM=0 / 1 disables / forces the routing.
     const char* e1 = getenv("FP8B_CONV_1X1_GEMM");
     const int64_t nout = kind == 0 ? g.f : g.c;
+    const char* e2 = getenv("FP8B_CONV_1X1_DGRAD_PIX");  // diagnostic: dgrad pixel limit
+    const int64_t dgrad_pix = e2 && e2[0] ? atoll(e2) : INT64_MAX;
     const bool gemm_1x1 = e1 && e1[0] ? e1[0] == '1'
-                                      : nout >= 256 && (kind == 0 || g.n * g.h * g.w <= 262144);
+                                      : nout >= 256 && (kind == 0 || g.n * g.h * g.w <= dgrad_pix);
     if (kind != 2 && k == 1 && pad == 0 && g.stride == 1 && gemm_1x1) {
         const EpiArgs ep{out, nullptr, g.yq, g.yq_fmt, g.yq_mode, g.yq_seed, g.yq_saturate, g.yq_counters};
         const int64_t P = g.n * g.h * g.w;

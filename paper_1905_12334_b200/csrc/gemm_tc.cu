@@ -454,6 +454,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
             s = 0; kb0 = 0; kb1 = p.num_kb;
             return;
         }
+        if (p.splits == 1) {
+            // no split-K: skip the integer divisions (every warp of the CTA runs
+            // this once per tile; on short-K shapes they were ~1/4 of all issue slots)
+            s = 0; kb0 = 0; kb1 = p.num_kb;
+            if (p.tiles_n == 1) { tm = item; tn = 0; }
+            else tile_coords(item, p.tiles_m, p.tiles_n, tm, tn);
+            return;
+        }
         const int tile = item / p.splits;
         s = item - tile * p.splits;
         tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
@@ -1392,6 +1400,11 @@ static int launch_es(const void* a, const void* b, int64_t m, int64_t n, int64_t
                     }
                 }
                 // (16 warps measured slower here: 1M x 512 x 1536 0.698 -> 0.707 ms)
+                // K <= 256 with codes-only output: the epilogue is all there is, and
+                // 16 warps (4 per scheduler) hide its TMEM / staging latencies:
+                // 802816 x 256 x 64 90 -> 75 us, 50176 x 1024 x 256 30 -> 26 us
+                if (lean && (ev ? (ev[0] == '1' && ev[1] == '6') : p.num_kb <= 2))
+                    return launch_2sm<ES, 1, 16, 1, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);
                 if (lean)
                     return ew8 ? launch_2sm<ES, 1, 8, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st)
                                : launch_2sm<ES, 1, 4, 2, 1>(tA2, tB2, tmC, tmQ, p, m, n, num_sms, st);

@@ -38,9 +38,7 @@ __device__ __forceinline__ void quant_group(const float4& v, const uint32_t (&rb
         // "+1 on the code byte" (0x7B -> the Inf code 0x7C) unless
         // saturating; underflow = zero-magnitude codes minus exact-zero
         // inputs; NaN (rare) rewrites its byte to the canonical 0x7E.
-        const uint32_t p01 = cvt_e5m2x2(f[0], f[1]);
-        const uint32_t p23 = cvt_e5m2x2(f[2], f[3]);
-        uint32_t w = __byte_perm(p01, p23, 0x5410);
+        uint32_t w = cvt_e5m2x4(f[0], f[1], f[2], f[3]);
         uint32_t m = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) m = or_if_gt(m, fabsf(f[k]), 57344.0f, 1u << (8 * k));

@@ -330,9 +330,7 @@ __device__ __forceinline__ void lean_e5m2_codes(const float (&y)[32], uint32_t (
                                                 uint32_t& cn) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const uint32_t lo = cvt_e5m2x2(y[4 * q], y[4 * q + 1]);
-        const uint32_t hi = cvt_e5m2x2(y[4 * q + 2], y[4 * q + 3]);
-        w[q] = __byte_perm(lo, hi, 0x5410);
+        w[q] = cvt_e5m2x4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
     }
     // one screen for both: bit 7 of m + 5 is set iff m >= 0x7B, bit 7 of m + 0x7F
     // is clear iff m == 0 (no carries between bytes: m <= 0x7F); 4 ops per word

@@ -332,6 +332,37 @@ def test_astat_codes_exact_grid(fp8, nb_env, b_major, m, k, n):
             os.environ["FP8B_GEMM_AST"] = old
 
 
+
+@pytest.mark.parametrize("b_major", ["n", "k"])
+@pytest.mark.parametrize("m,k,n", [(3000, 64, 256), (1500, 256, 1000), (777, 96, 320)])
+def test_short_k_16_warp_epilogue_exact_grid(fp8, b_major, m, k, n):
+    """K <= 256 with codes-only E5M2 output takes the 256x256 pair kernel with 16
+    epilogue warps (the 1x1 conv fprop / dgrad shapes): ragged M / N / K, both B
+    layouts; codes and counters equal Q_RNE of the exact result, with overflow /
+    underflow / NaN bias columns."""
+    import torch
+    rng = np.random.default_rng(123)
+    A = O.quantize((rng.integers(-2, 3, m * k) * 0.5).astype(np.float32))[0].reshape(m, k)
+    B = O.quantize((rng.integers(-2, 3, k * n) * 0.25).astype(np.float32))[0].reshape(k, n)
+    B[:, 5::97] = 0
+    bias = (rng.integers(-8, 8, n) * 0.125).astype(np.float32)
+    bias[3::61] = 60000.0
+    bias[5::97] = 1e-6
+    bias[7::211] = np.nan
+    bdev = B if b_major == "n" else np.ascontiguousarray(B.T)
+    cnt = fp8.Counters()
+    _, cq = fp8.gemm_codes(_codes_dev(A, "fp8"), _codes_dev(bdev, "fp8"), m, n, k, "fp8",
+                           b_major=b_major, engine="tensor", want_c=False,
+                           bias=torch.from_numpy(bias).cuda(), out_fmt="fp8",
+                           out_mode="nearest-even", out_counters=cnt)
+    da = O.dequantize(A).astype(np.float64).reshape(m, k)
+    db = O.dequantize(B).astype(np.float64).reshape(k, n)
+    y = ((da @ db).astype(np.float32) + bias[None, :]).astype(np.float32)
+    codes, k_ = O.quantize(y, "fp8", "nearest-even", 1)
+    np.testing.assert_array_equal(cq.cpu().numpy().reshape(-1), codes.astype(np.uint8).reshape(-1))
+    assert cnt.values() == tuple(int(v) for v in k_)
+    assert k_[0] > 0 and k_[1] > 0 and k_[2] > 0
+
 @pytest.mark.parametrize("n,b_major", [(2048, "n"), (1536, "k"), (32000, "n")])
 def test_astat_equals_streaming_at_config5_size(fp8, n, b_major):
     """Config-5 fprop shapes at full size (2^20 tokens x 512 -> n): the

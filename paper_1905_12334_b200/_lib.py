@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfp8b200.so")
+# FP8B200_LIB (diagnostic): another build of the same library, for A/B timing
+LIB_PATH = os.environ.get("FP8B200_LIB") or os.path.join(HERE, "libfp8b200.so")
 
 OK, EINVAL, ENOTSUP, ECUDA, EIO = 0, 22, 95, 1000, 5
 FP8T_F32, FP8T_FP8, FP8T_FP16 = 0, 1, 2

@@ -18,18 +18,22 @@ __global__ void merge_gate_kernel(const int64_t* c, int64_t* gate) {
     if (threadIdx.x < 3) gate[threadIdx.x] = c[threadIdx.x] + c[3 + threadIdx.x];
 }
 
-// Side stream for the step's independent branches (Q(E) beside Q(X) + fprop;
-// bprop beside wgrad): fork / join through events, which CUDA-graph capture
-// turns into parallel graph branches. One set per host thread and device, so
-// concurrent callers on different streams never share events.
+// Side streams for the step's independent branches. Given Q(X) and Q(E), the
+// three GEMMs of the layer are independent (fprop reads qx and w_q, bprop qe and
+// w_q, wgrad qx and qe) and together need 64 of the 148 SMs at config-1 size, so
+// they run side by side: main = Q(X) -> fprop, side 0 = Q(E) -> bprop, side 1 =
+// wgrad once both Q nodes are done. Fork / join go through events, which
+// CUDA-graph capture turns into parallel graph branches. One set per host
+// thread and device, so concurrent callers on different streams never share
+// events.
 struct SideStream {
-    cudaStream_t s = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t fork = nullptr, qx = nullptr, qe = nullptr, join[2] = {nullptr, nullptr};
     int dev = -1;
 };
-// nullptr -> run both branches on the caller's stream (no fork). That is also
+// nullptr -> run every branch on the caller's stream (no fork). That is also
 // the path when the first call of a thread is inside a stream capture, where
-// creating the stream / events is not allowed.
+// creating the streams / events is not allowed.
 static SideStream* side_stream(cudaStream_t caller) {
     thread_local SideStream ss[16];
     int dev = 0;
@@ -39,10 +43,14 @@ static SideStream* side_stream(cudaStream_t caller) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         if (cudaStreamIsCapturing(caller, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
             return nullptr;
-        if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess)
-            return nullptr;
+        bool ok = true;
+        for (int i = 0; i < 2; ++i)
+            ok = ok && cudaStreamCreateWithFlags(&x.s[i], cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&x.join[i], cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&x.qx, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&x.qe, cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) return nullptr;
         x.dev = dev;
     }
     return &x;
@@ -74,8 +82,9 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     rne.seed = 1;
     rne.saturate = s->saturate;
     fp8b::SideStream* ss = fp8b::side_stream(st);
-    void* side = ss ? (void*)ss->s : stream;
-    // An open fork is always joined, also on the early-return paths (FP8B_TRY):
+    void* side0 = ss ? (void*)ss->s[0] : stream;
+    void* side1 = ss ? (void*)ss->s[1] : stream;
+    // Open forks are always joined, also on the early-return paths (FP8B_TRY):
     // under stream capture an unjoined fork would invalidate the capture, and run
     // eagerly the side-stream work would stay unordered with the caller's later
     // work.
@@ -86,7 +95,8 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
         bool fork() {
             if (!ss) return true;
             if (cudaEventRecord(ss->fork, st) != cudaSuccess ||
-                cudaStreamWaitEvent(ss->s, ss->fork, 0) != cudaSuccess)
+                cudaStreamWaitEvent(ss->s[0], ss->fork, 0) != cudaSuccess ||
+                cudaStreamWaitEvent(ss->s[1], ss->fork, 0) != cudaSuccess)
                 return false;
             open = true;
             return true;
@@ -94,58 +104,65 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
         bool join() {
             if (!ss || !open) return true;
             open = false;
-            return cudaEventRecord(ss->join, ss->s) == cudaSuccess &&
-                   cudaStreamWaitEvent(st, ss->join, 0) == cudaSuccess;
+            bool ok = true;
+            for (int i = 0; i < 2; ++i)
+                ok = (cudaEventRecord(ss->join[i], ss->s[i]) == cudaSuccess &&
+                      cudaStreamWaitEvent(st, ss->join[i], 0) == cudaSuccess) && ok;
+            return ok;
         }
         ~Branch() { join(); }
     } br{ss, st};
-    auto fork = [&]() { return br.fork(); };
-    auto join = [&]() { return br.join(); };
-    // ---- Q(E) on the side stream, beside the forward (it depends on nothing there)
-    if (!fork()) return FP8B_ECUDA;
-    FP8B_TRY(fp8b_quantize(s->e, s->qe, B * O, FP8B_E5M2, &rne, s->counters, side));
+    // ---- side 0: Q(E) (+ db), then bprop (nn.cpp:294-326)
+    if (!br.fork()) return FP8B_ECUDA;
+    FP8B_TRY(fp8b_quantize(s->e, s->qe, B * O, FP8B_E5M2, &rne, s->counters, side0));
     if (s->b_master) {
-        FP8B_TRY(fp8b_bias_grad(s->qe, FP8B_E5M2, B, O, s->db, side));
-        FP8B_TRY(fp8b_count_nonfinite(s->db, O, s->counters, side));
+        FP8B_TRY(fp8b_bias_grad(s->qe, FP8B_E5M2, B, O, s->db, side0));
+        FP8B_TRY(fp8b_count_nonfinite(s->db, O, s->counters, side0));
     }
-    // ---- forward (nn.cpp:187-203): qx = Q(x); y = qx . w_q (+ b); qy = Q(y)
-    if (s->b_master) FP8B_TRY(fp8b_dequantize(s->b_master, s->b_value, O, FP8B_FP16, stream));
-    FP8B_TRY(fp8b_quantize(s->x, s->qx, B * I, FP8B_E5M2, &rne, s->fwd_counters, stream));
+    if (ss && cudaEventRecord(ss->qe, ss->s[0]) != cudaSuccess) return FP8B_ECUDA;
     fp8b_gemm_args_t g{};
     g.engine = s->engine;
     g.cq_fmt = FP8B_E5M2;
     g.cq_mode = FP8B_RNE;
     g.cq_seed = 1;
     g.cq_saturate = s->saturate;
-    g.a_major = FP8B_K_MAJOR;
-    g.b_major = FP8B_MN_MAJOR;
-    g.c = s->y;
-    g.bias = s->b_master ? s->b_value : nullptr;
-    g.cq = s->qy;
-    g.cq_counters = s->fwd_counters;
-    FP8B_TRY(fp8b_gemm(s->qx, s->w_q, B, O, I, FP8B_E5M2, &g, stream));
-    // ---- backward (nn.cpp:294-326); Q(E) ran on the side stream
-    if (!join()) return FP8B_ECUDA;
-    // wgrad: dW[I,O] = qx^T . qe  (qx read M-major, qe N-major; no transpose pass)
-    g.a_major = FP8B_MN_MAJOR;
-    g.b_major = FP8B_MN_MAJOR;
-    g.c = nullptr;
-    g.bias = nullptr;
-    g.cq = s->qdw;
-    g.cq_counters = s->counters + 3;
-    // bprop: dX[B,I] = qe . w_q^T  (w_q [I,O] read as the K-major [N=I, K=O]
-    // operand) on the side stream, beside wgrad (both only read qx / qe / w_q)
     if (s->qdx) {
+        // bprop: dX[B,I] = qe . w_q^T  (w_q [I,O] read as the K-major [N=I, K=O] operand)
         fp8b_gemm_args_t gb = g;
         gb.a_major = FP8B_K_MAJOR;
         gb.b_major = FP8B_K_MAJOR;
         gb.cq = s->qdx;
         gb.cq_counters = s->counters;
-        if (!fork()) return FP8B_ECUDA;
-        FP8B_TRY(fp8b_gemm(s->qe, s->w_q, B, I, O, FP8B_E5M2, &gb, side));
+        FP8B_TRY(fp8b_gemm(s->qe, s->w_q, B, I, O, FP8B_E5M2, &gb, side0));
     }
-    FP8B_TRY(fp8b_gemm(s->qx, s->qe, I, O, B, FP8B_E5M2, &g, stream));
-    if (s->qdx && !join()) return FP8B_ECUDA;
+    // ---- main: forward (nn.cpp:187-203): qx = Q(x); y = qx . w_q (+ b); qy = Q(y)
+    if (s->b_master) FP8B_TRY(fp8b_dequantize(s->b_master, s->b_value, O, FP8B_FP16, stream));
+    FP8B_TRY(fp8b_quantize(s->x, s->qx, B * I, FP8B_E5M2, &rne, s->fwd_counters, stream));
+    if (ss && cudaEventRecord(ss->qx, st) != cudaSuccess) return FP8B_ECUDA;
+    {
+        fp8b_gemm_args_t gf = g;
+        gf.a_major = FP8B_K_MAJOR;
+        gf.b_major = FP8B_MN_MAJOR;
+        gf.c = s->y;
+        gf.bias = s->b_master ? s->b_value : nullptr;
+        gf.cq = s->qy;
+        gf.cq_counters = s->fwd_counters;
+        FP8B_TRY(fp8b_gemm(s->qx, s->w_q, B, O, I, FP8B_E5M2, &gf, stream));
+    }
+    // ---- side 1: wgrad dW[I,O] = qx^T . qe (qx read M-major, qe N-major; no
+    // transpose pass), once both Q nodes are done
+    if (ss && (cudaStreamWaitEvent(ss->s[1], ss->qx, 0) != cudaSuccess ||
+               cudaStreamWaitEvent(ss->s[1], ss->qe, 0) != cudaSuccess))
+        return FP8B_ECUDA;
+    {
+        fp8b_gemm_args_t gw = g;
+        gw.a_major = FP8B_MN_MAJOR;
+        gw.b_major = FP8B_MN_MAJOR;
+        gw.cq = s->qdw;
+        gw.cq_counters = s->counters + 3;
+        FP8B_TRY(fp8b_gemm(s->qx, s->qe, I, O, B, FP8B_E5M2, &gw, side1));
+    }
+    if (!br.join()) return FP8B_ECUDA;
     // grads_finite gate (nn.cpp:401-411): overflow of qe/qdw/qdx, NaN in qdw, non-finite db
     fp8b::merge_gate_kernel<<<1, 32, 0, st>>>(s->counters, s->gate);
     if (cudaGetLastError() != cudaSuccess) return FP8B_ECUDA;

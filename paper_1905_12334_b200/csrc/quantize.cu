@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(256) quant_lfsr_kernel(const float* __restrict
                                                          void* __restrict__ codes, int64_t n,
                                                          uint64_t seed, int saturate,
                                                          int64_t block_offset, LfsrTables tabs,
-                                                         int64_t* counters, int64_t block_begin) {
+                                                         int64_t* counters, int64_t block_begin,
+                                                         int vec) {
     __shared__ uint32_t smem_w[2][8];
     const bool sat = saturate != 0;
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
@@ -448,6 +449,11 @@ __global__ void __launch_bounds__(256) quant_lfsr_kernel(const float* __restrict
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
+            if (vec && base + kBlock <= n) {  // full block, aligned tensors: one 16-byte load
+                v[r] = *reinterpret_cast<const float4*>(x + i0);
+                valid[r] = 4;
+                continue;
+            }
             float f[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) f[k] = (i0 + k < n) ? x[i0 + k] : 0.0f;
@@ -472,6 +478,10 @@ __global__ void __launch_bounds__(256) quant_lfsr_kernel(const float* __restrict
                 c_unf += (a != 0u) && (a <= Fmt<MB>::maxbits) && ((c[k] & (Fmt<MB>::signbit - 1u)) == 0u);
             }
             const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
+            if (vec && base + kBlock <= n) {
+                store4<MB>(codes, i0, c);
+                continue;
+            }
             for (int k = 0; k < valid[r]; ++k) {
                 if (MB == 2) reinterpret_cast<uint8_t*>(codes)[i0 + k] = (uint8_t)c[k];
                 else reinterpret_cast<uint16_t*>(codes)[i0 + k] = (uint16_t)c[k];
@@ -612,7 +622,7 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
             auto fn = quant_lfsr_kernel<MB>;
             const int g = grid_for((const void*)fn, 256, nblocks - begin);
             fn<<<g, 256, 0, st>>>(x, codes, n, cfg.seed, cfg.saturate, cfg.block_offset, tabs,
-                                  counters, begin);
+                                  counters, begin, aligned ? 1 : 0);
         }
         return;
     }

@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(256) sgd_lfsr_kernel(const void* __restrict__ 
                                                        uint16_t* __restrict__ master,
                                                        float* __restrict__ mom, int64_t n,
                                                        UpdArgs a, int64_t block_offset,
-                                                       LfsrTables tabs, int64_t block_begin) {
+                                                       LfsrTables tabs, int64_t block_begin,
+                                                       int vec) {
     if (upd_skipped(a)) return;
     __shared__ uint32_t smem_w[2][8];
     const Unscale us(upd_scale(a));
@@ -353,10 +354,28 @@ __global__ void __launch_bounds__(256) sgd_lfsr_kernel(const void* __restrict__ 
         const int64_t base = b * kBlock;
         float w[4][4];
         uint32_t mask[4];
+        // full block, 16-byte aligned tensors: one vector access per tensor and round
+        const bool vfull = vec && base + kBlock <= n;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             mask[r] = 0;
             const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
+            if (vfull) {
+                float gr[4];
+                load_grad4<GFMT>(grad, i0 >> 2, gr);
+                const uint2 mw = *reinterpret_cast<const uint2*>(master + i0);
+                const float4 mv = *reinterpret_cast<const float4*>(mom + i0);
+                const uint32_t mc[4] = {mw.x & 0xFFFFu, mw.x >> 16, mw.y & 0xFFFFu, mw.y >> 16};
+                float m[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    w[r][k] = sgd_w32(gr[k], dec_f16(mc[k]), m[k], us, a);
+                    const uint32_t aa = __float_as_uint(w[r][k]) & 0x7FFFFFFFu;
+                    if (sr_inexact<10>(aa, __uint_as_float(aa))) mask[r] |= 1u << k;
+                }
+                *reinterpret_cast<float4*>(mom + i0) = make_float4(m[0], m[1], m[2], m[3]);
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int64_t i = i0 + k;
@@ -377,6 +396,19 @@ __global__ void __launch_bounds__(256) sgd_lfsr_kernel(const void* __restrict__ 
         for (int r = 0; r < 4; ++r) {
             uint32_t j = p0 + pre[r];
             const int64_t i0 = base + 1024 * r + 4 * threadIdx.x;
+            if (vfull) {
+                uint32_t c[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t take = (mask[r] >> k) & 1u;
+                    const uint32_t r16 = take ? (uint32_t)__ldg(tabs.tabx + j) : 0u;
+                    j += take;
+                    c[k] = sr_encode<10>(__float_as_uint(w[r][k]), r16, false, mb, mn, mu_);
+                }
+                *reinterpret_cast<uint2*>(master + i0) = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+                if (a.w8) *reinterpret_cast<uint32_t*>(a.w8 + i0) = w8_pack4(c, wsat, wb, wn, wu);
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const uint32_t take = (mask[r] >> k) & 1u;
@@ -484,7 +516,8 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
             int64_t g = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
             if (nb - begin < g) g = nb - begin;
             sgd_lfsr_kernel<GFMT><<<(int)g, 256, 0, st>>>(grad, master, mom, n, a,
-                                                          args.block_offset, tabs, begin);
+                                                          args.block_offset, tabs, begin,
+                                                          aligned ? 1 : 0);
         }
         return;
     }

@@ -231,6 +231,26 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    # what HBM delivers for each kernel's read : write mix with no arithmetic
+    # (fp8b_stream_probe, same access pattern): the practical ceiling beside the
+    # 1 : 1 copy figure the roofline fraction is quoted against
+    if rank == 0:
+        mix = {}
+        for name, ob, out in [("in4_out1", 1, c8a), ("in4_out2", 2, c16)]:
+            for _ in range(3):
+                F.stream_probe(x, out, ob)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(10):
+                F.stream_probe(x, out, ob)
+            b.record(stream)
+            torch.cuda.synchronize()
+            mix[name] = round(n * (4 + ob) * 10 / (a.elapsed_time(b) * 1e-3) / 1e9, 1)
+        dom_mix = mix["in4_out2" if BYTES_PER_ELEM[dom] == 6 else "in4_out1"]
+        result["roofline"]["access_mix_ceiling"] = {
+            "gbs": mix, "frac_of_mix_ceiling": round(kernel_gbs[dom] / dom_mix, 4),
+            "note": "no-arithmetic stream with the kernel's bytes in/out per element, measured live"}
     # counters sanity (all ranks identical data distribution): overflow fraction
     o, u, nn = cnt[0].values()
     result["counters_e5m2_rne_per_step"] = {"overflow": o // (args.steps + args.warmup),

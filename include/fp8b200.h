@@ -349,6 +349,13 @@ int64_t fp8b_launch_count(void);
 int fp8b_fill_synthetic(float *out, int64_t n, int32_t kind, uint64_t seed, double p,
                         double lo, double hi, void *stream);
 
+/* Measurement aid (bench.py; no reference counterpart): streams n FP32 values
+ * (n % 4 == 0, 16-byte aligned) with the quantizer's access pattern and writes
+ * out_bytes in {0, 1, 2, 4} bytes per element with no arithmetic -- what HBM
+ * delivers for that read : write mix, the practical ceiling of the quantize
+ * kernels beside the 1 : 1 copy figure. */
+int fp8b_stream_probe(const float *x, void *out, int64_t n, int32_t out_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,7 @@ from ._lib import LIB, check
 __all__ = [
     "QuantizedTensor", "ScaleEvent", "LossScaler", "quantize", "dequantize", "transpose",
     "gemm", "gemm_codes", "encode", "decode", "sgd_momentum_update", "bias_grad",
-    "count_nonfinite", "fill_synthetic", "Counters", "launch_count", "version",
+    "count_nonfinite", "fill_synthetic", "stream_probe", "Counters", "launch_count", "version",
     "conv2d", "conv2d_backward_data", "conv2d_backward_weights", "im2col", "conv_out_dim", "conv_tensor_supported", "conv_halo_supported",
     "conv2d_im2col",
 ]
@@ -628,6 +628,13 @@ def fill_synthetic(out: torch.Tensor, kind: str, seed: int, p: float = 0.01, lo:
     check(LIB.fp8b_fill_synthetic(out.data_ptr(), out.numel(), k, int(seed), float(p),
                                   float(lo), float(hi), _stream(stream)), "fill_synthetic")
     return out
+
+
+def stream_probe(x: torch.Tensor, out: Optional[torch.Tensor], out_bytes: int, stream=None) -> None:
+    """Measurement aid: stream x with the quantizer's access pattern, writing
+    out_bytes (0, 1, 2 or 4) bytes per element and doing no arithmetic."""
+    check(LIB.fp8b_stream_probe(x.data_ptr(), out.data_ptr() if out is not None else None,
+                                x.numel(), int(out_bytes), _stream(stream)), "stream_probe")
 
 
 class DenseLayer:

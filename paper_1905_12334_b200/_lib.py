@@ -106,6 +106,7 @@ SIGNATURES = {
     "fp8b_launch_count": (C.c_int64, []),
     "fp8b_fill_synthetic": (C.c_int, [_vp, _i64, _i32, _u64, C.c_double, C.c_double,
                                       C.c_double, _vp]),
+    "fp8b_stream_probe": (C.c_int, [_vp, _vp, _i64, _i32, _vp]),
 }
 
 

@@ -468,4 +468,14 @@ int fp8b_fill_synthetic(float* out, int64_t n, int32_t kind, uint64_t seed, doub
     return check_launch(1);
 }
 
+int fp8b_stream_probe(const float* x, void* out, int64_t n, int32_t out_bytes, void* stream) {
+    if (n < 0 || (n & 3) || (out_bytes != 0 && out_bytes != 1 && out_bytes != 2 && out_bytes != 4))
+        return fail(FP8B_EINVAL, "stream_probe: bad arguments");
+    if (n == 0) return FP8B_OK;
+    if (!x || (out_bytes && !out) || ((uintptr_t)x % 16) || ((uintptr_t)out % 16))
+        return fail(FP8B_EINVAL, "stream_probe: null or unaligned tensor");
+    fp8b::launch_stream_probe(x, out, n, out_bytes, S(stream));
+    return check_launch(1);
+}
+
 }  // extern "C"

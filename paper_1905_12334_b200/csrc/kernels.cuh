@@ -77,5 +77,6 @@ int64_t lfsr_cta_max_blocks();
 void note_launches(int n);
 void launch_fill_synthetic(float* out, int64_t n, int kind, uint64_t seed, double p, double lo,
                            double hi, cudaStream_t st);
+void launch_stream_probe(const float* x, void* out, int64_t n, int out_bytes, cudaStream_t st);
 
 }  // namespace fp8b

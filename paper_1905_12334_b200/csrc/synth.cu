@@ -43,4 +43,44 @@ void launch_fill_synthetic(float* out, int64_t n, int kind, uint64_t seed, doubl
     fill_synth_kernel<<<(int)blocks, 256, 0, st>>>(out, n, kind, seed, p, lo, hi);
 }
 
+// The quantizer's access pattern with no arithmetic (fp8b_stream_probe).
+template <int OUTB>
+__global__ void __launch_bounds__(256) stream_probe_kernel(const float4* __restrict__ x,
+                                                          void* __restrict__ out, int64_t ngroups) {
+    constexpr int UN = 2;
+    const int64_t stride = (int64_t)gridDim.x * 256 * UN;
+    float acc = 0.0f;
+    for (int64_t g0 = (int64_t)blockIdx.x * 256 * UN + threadIdx.x; g0 < ngroups; g0 += stride) {
+        float4 v[UN];
+#pragma unroll
+        for (int j = 0; j < UN; ++j)
+            if (g0 + j * 256 < ngroups) v[j] = __ldcs(x + g0 + j * 256);
+#pragma unroll
+        for (int j = 0; j < UN; ++j) {
+            const int64_t g = g0 + j * 256;
+            if (g >= ngroups) continue;
+            const uint32_t a = __float_as_uint(v[j].x), b = __float_as_uint(v[j].y),
+                           c = __float_as_uint(v[j].z), d = __float_as_uint(v[j].w);
+            if (OUTB == 0) acc += v[j].x + v[j].y + v[j].z + v[j].w;
+            if (OUTB == 1)
+                __stcs(reinterpret_cast<uint32_t*>(out) + g,
+                       (a >> 24) | ((b >> 24) << 8) | ((c >> 24) << 16) | (d & 0xFF000000u));
+            if (OUTB == 2)
+                __stcs(reinterpret_cast<uint2*>(out) + g,
+                       make_uint2((a >> 16) | (b & 0xFFFF0000u), (c >> 16) | (d & 0xFFFF0000u)));
+            if (OUTB == 4) __stcs(reinterpret_cast<float4*>(out) + g, v[j]);
+        }
+    }
+    if (OUTB == 0 && acc == 123.456f && out) *reinterpret_cast<float*>(out) = acc;
+}
+
+void launch_stream_probe(const float* x, void* out, int64_t n, int out_bytes, cudaStream_t st) {
+    const int grid = device_sm_count() * 8;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    if (out_bytes == 0) stream_probe_kernel<0><<<grid, 256, 0, st>>>(x4, out, n / 4);
+    else if (out_bytes == 1) stream_probe_kernel<1><<<grid, 256, 0, st>>>(x4, out, n / 4);
+    else if (out_bytes == 2) stream_probe_kernel<2><<<grid, 256, 0, st>>>(x4, out, n / 4);
+    else stream_probe_kernel<4><<<grid, 256, 0, st>>>(x4, out, n / 4);
+}
+
 }  // namespace fp8b

@@ -314,13 +314,16 @@ static int conv_common(int kind, const void* a, const void* b, float* out, int32
     g2.yq = nullptr;
     int nl = 0;
     int r = FP8B_ENOTSUP;
-    if (g->engine == FP8B_GEMM_TENSOR) r = fp8b::launch_conv_tc(kind, a, b, out, fmt, g2, st, &nl);
+    // wgrad: the Q(dW) node rides on the split-K sum where there is one (q_done)
+    int q_done = 0;
+    if (g->engine == FP8B_GEMM_TENSOR)
+        r = fp8b::launch_conv_tc(kind, a, b, out, fmt, kind == 2 ? *g : g2, st, &nl, &q_done);
     if (r == FP8B_ENOTSUP) {
         fp8b::launch_conv_seq(kind, a, b, out, fmt, g2, st);
         nl = 1;
         r = FP8B_OK;
     }
-    if (r == FP8B_OK && g->yq) {
+    if (r == FP8B_OK && g->yq && !q_done) {
         fp8b::LfsrTables tabs;
         r = get_tables(&tabs);
         if (r == FP8B_OK) {

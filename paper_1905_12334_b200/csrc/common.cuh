@@ -514,4 +514,28 @@ __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
     return r;
 }
 
+// An output Q node applied by a reduction kernel's last step (split-K sums of
+// the conv wgrads): the same integer rule and counter-bit stream as the
+// standalone quantize launch it replaces (element i draws counter_r16(seed, i)).
+struct QNode {
+    void* codes;       // null: no Q node
+    int fmt, mode;
+    uint64_t seed;
+    int sat;
+    int64_t* counters;
+};
+__device__ __forceinline__ void qnode_store(const QNode& q, int64_t i, float v, uint32_t& co,
+                                            uint32_t& cu, uint32_t& cn) {
+    const uint32_t r16 = q.mode == FP8B_SR ? counter_r16(q.seed, (uint64_t)i) : 0u;
+    int o, u, n;
+    if (q.fmt == FP8B_E5M2) {
+        const uint32_t c = encode_int<2>(__float_as_uint(v), q.mode, r16, q.sat != 0, o, u, n);
+        reinterpret_cast<uint8_t*>(q.codes)[i] = (uint8_t)c;
+    } else {
+        const uint32_t c = encode_int<10>(__float_as_uint(v), q.mode, r16, q.sat != 0, o, u, n);
+        reinterpret_cast<uint16_t*>(q.codes)[i] = (uint16_t)c;
+    }
+    co += o; cu += u; cn += n;
+}
+
 }  // namespace fp8b

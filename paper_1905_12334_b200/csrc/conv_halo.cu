@@ -690,17 +690,23 @@ __global__ void __launch_bounds__(192, 1)
     }
 }
 
-// dw [f, kh, kw, c] = sum over CTAs b (ascending) of ws[b][t][c][f]
-__global__ void conv_halo_wgrad_sum(const float* __restrict__ ws, float* __restrict__ dw, int nb, int C,
-                                   int F) {
+// dw [f, kh, kw, c] = sum over CTAs b (ascending) of ws[b][t][c][f], then the
+// layer's Q(dW) node when asked for (one launch fewer than sum + quantize).
+__global__ void __launch_bounds__(256) conv_halo_wgrad_sum(const float* __restrict__ ws,
+                                                           float* __restrict__ dw, int nb, int C,
+                                                           int F, QNode q) {
     const int total = 9 * C * F;
+    uint32_t co = 0, cu = 0, cn = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int f = i % F, tc = i / F;  // ws order: [t][c][f]
         float s = 0.f;
         for (int b = 0; b < nb; ++b) s = __fadd_rn(s, ws[(size_t)b * total + i]);
         const int t = tc / C, c = tc - t * C;
-        dw[((size_t)f * 9 + t) * C + c] = s;
+        const size_t o = ((size_t)f * 9 + t) * C + c;
+        dw[o] = s;
+        if (q.codes) qnode_store(q, (int64_t)o, s, co, cu, cn);
     }
+    if (q.codes && q.counters) flush_counters<256>(co, cu, cn, q.counters);
 }
 
 }  // namespace halo
@@ -793,7 +799,8 @@ bool conv_halo_wgrad_supported(int es, int64_t n, int64_t h, int64_t w, int64_t 
 
 // wgrad over NHWC x [n, h, w, c] and e [n, oh, ow, f] -> dw [f, 3, 3, c] (FP32).
 int launch_conv_halo_wgrad(const void* x, const void* e, float* dw, int es, int64_t n, int64_t h,
-                           int64_t w, int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl) {
+                           int64_t w, int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl,
+                           const fp8b_conv_t* gq) {
     using namespace tc::halo;
     if (!conv_halo_wgrad_supported(es, n, h, w, c, f, k, pad)) return FP8B_ENOTSUP;
     if ((uintptr_t)x % 16 || (uintptr_t)e % 16 || !dw) return FP8B_ENOTSUP;
@@ -837,7 +844,10 @@ int launch_conv_halo_wgrad(const void* x, const void* e, float* dw, int es, int6
     fn<<<grid, 192, smem, st>>>(tx, te, p, slab, stage, nstages);
     int b = (int)((part + 255) / 256);
     if (b > 4 * sms) b = 4 * sms;
-    conv_halo_wgrad_sum<<<b, 256, 0, st>>>(p.ws, dw, grid, (int)c, (int)f);
+    QNode q{};
+    if (gq && gq->yq)
+        q = QNode{gq->yq, gq->yq_fmt, gq->yq_mode, gq->yq_seed, gq->yq_saturate, gq->yq_counters};
+    conv_halo_wgrad_sum<<<b, 256, 0, st>>>(p.ws, dw, grid, (int)c, (int)f, q);
     cudaFreeAsync(p.ws, st);
     *nl = 2;
     return cudaGetLastError() == cudaSuccess ? FP8B_OK : FP8B_ECUDA;

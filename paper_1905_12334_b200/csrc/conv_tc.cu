@@ -329,15 +329,20 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
     }
 }
 
-// dw[i] = sum_s ws[s][i], s ascending (deterministic).
-__global__ void splitk_sum_kernel(const float* __restrict__ ws, float* __restrict__ out, int64_t mn,
-                                  int splits) {
+// dw[i] = sum_s ws[s][i], s ascending (deterministic), then the layer's Q(dW)
+// node when asked for (one launch fewer than sum + quantize).
+__global__ void __launch_bounds__(256) splitk_sum_kernel(const float* __restrict__ ws,
+                                                         float* __restrict__ out, int64_t mn,
+                                                         int splits, QNode q) {
+    uint32_t co = 0, cu = 0, cn = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mn;
          i += (int64_t)gridDim.x * blockDim.x) {
         float a = ws[i];
         for (int s = 1; s < splits; ++s) a = __fadd_rn(a, ws[s * mn + i]);
         out[i] = a;
+        if (q.codes) qnode_store(q, i, a, co, cu, cn);
     }
+    if (q.codes && q.counters) flush_counters<256>(co, cu, cn, q.counters);
 }
 
 // W'[c, kh, kw, f] = W[f, kH-1-kh, kW-1-kw, c]  (codes, ES bytes each)
@@ -444,9 +449,11 @@ static int fprop(const void* x, const void* w, float* y, int64_t n, int64_t h, i
 // wgrad: dw [f, k, k, c] from x [n, h, w, c] and e [n, oh, ow, f]
 template <int ES>
 static int wgrad(const void* x, const void* e, float* dw, int64_t n, int64_t h, int64_t wd,
-                 int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl) {
+                 int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl,
+                 const fp8b_conv_t& g, int* q_done) {
     {  // 3x3 with 64-byte channel and filter rows: the halo-slab wgrad
-        const int rc = launch_conv_halo_wgrad(x, e, dw, ES, n, h, wd, c, f, k, pad, st, nl);
+        const int rc = launch_conv_halo_wgrad(x, e, dw, ES, n, h, wd, c, f, k, pad, st, nl, &g);
+        if (rc == FP8B_OK && g.yq && q_done) *q_done = 1;
         if (rc != FP8B_ENOTSUP) return rc;
     }
     const int cb_bytes = (c * ES) % 128 == 0 ? 128 : ((c * ES) % 64 == 0 ? 64 : 0);
@@ -490,7 +497,12 @@ static int wgrad(const void* x, const void* e, float* dw, int64_t n, int64_t h, 
     if (splits > 1) {
         int64_t b = (mn + 255) / 256;
         if (b > 4 * num_sms()) b = 4 * num_sms();
-        splitk_sum_kernel<<<(int)b, 256, 0, st>>>(ws, dw, mn, splits);
+        QNode q{};
+        if (g.yq) {
+            q = QNode{g.yq, g.yq_fmt, g.yq_mode, g.yq_seed, g.yq_saturate, g.yq_counters};
+            if (q_done) *q_done = 1;
+        }
+        splitk_sum_kernel<<<(int)b, 256, 0, st>>>(ws, dw, mn, splits, q);
         cudaFreeAsync(ws, st);
         *nl = 2;
     }
@@ -536,8 +548,9 @@ int conv_tc_supported(int kind, int fmt, const fp8b_conv_t& g) {
 }
 
 int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
-                   const fp8b_conv_t& g, cudaStream_t st, int* nlaunch) {
+                   const fp8b_conv_t& g, cudaStream_t st, int* nlaunch, int* q_done) {
     *nlaunch = 0;
+    if (q_done) *q_done = 0;
     if (!conv_tc_supported(kind, fmt, g)) return FP8B_ENOTSUP;
     if (((uintptr_t)a % 16) || ((uintptr_t)b % 16)) return FP8B_ENOTSUP;
     const int k = (int)g.kh, pad = (int)g.pad;
@@ -576,8 +589,8 @@ int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
         rc = fmt == FP8B_E5M2 ? tc::cv::dgrad<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch, g)
                               : tc::cv::dgrad<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch, g);
     } else {
-        rc = fmt == FP8B_E5M2 ? tc::cv::wgrad<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch)
-                              : tc::cv::wgrad<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch);
+        rc = fmt == FP8B_E5M2 ? tc::cv::wgrad<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch, g, q_done)
+                              : tc::cv::wgrad<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, nlaunch, g, q_done);
     }
     return rc;
 }

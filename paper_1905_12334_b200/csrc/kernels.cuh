@@ -46,8 +46,10 @@ int launch_gemm_tc(const void* a, const void* b, int64_t m, int64_t n, int64_t k
 void launch_conv_seq(int kind, const void* a, const void* b, float* out, int fmt,
                      const fp8b_conv_t& g, cudaStream_t st);
 // Returns FP8B_ENOTSUP when the tensor engine does not cover the case.
+// wgrad (kind 2) with g.yq set: the Q node is fused into the split-K sum where
+// there is one, and *q_done says so (otherwise the caller quantizes `out`).
 int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
-                   const fp8b_conv_t& g, cudaStream_t st, int* nlaunch);
+                   const fp8b_conv_t& g, cudaStream_t st, int* nlaunch, int* q_done = nullptr);
 int conv_tc_supported(int kind, int fmt, const fp8b_conv_t& g);
 // Weight-stationary halo-slab fprop (conv_halo.cu) for C * bytes in {64, 128},
 // F <= 256; FP8B_ENOTSUP when the geometry is not covered.
@@ -60,7 +62,8 @@ int launch_conv_halo(const void* x, const void* wt, float* y, int es, int64_t n,
 bool conv_halo_wgrad_supported(int es, int64_t n, int64_t h, int64_t w, int64_t c, int64_t f, int k,
                                int pad);
 int launch_conv_halo_wgrad(const void* x, const void* e, float* dw, int es, int64_t n, int64_t h,
-                           int64_t w, int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl);
+                           int64_t w, int64_t c, int64_t f, int k, int pad, cudaStream_t st, int* nl,
+                           const fp8b_conv_t* gq = nullptr);
 void launch_im2col(const void* x, void* cols, int fmt, const fp8b_conv_t& g, cudaStream_t st);
 // Per-device setup (several GPUs per process are allowed): SM count of the
 // current device, and the >48 KB dynamic shared memory opt-in of a kernel on

@@ -590,8 +590,7 @@ def bench_conv(F, args, reps=5, only=None):
             cur.wait_stream(side2)
             F.sgd_momentum_update(qdw.codes, "fp8", master, mom, lr=0.1, mu=0.9, scaler=scaler,
                                   skip_counters=bwd, master_mode="stochastic", seed=5,
-                                  w_e5m2=W.codes)
-            scaler.step_async(True, 0, counters=bwd)
+                                  w_e5m2=W.codes, step_scaler_iteration=0)
         sms = _graph_ms(step, reps)
         tot_step += sms
         res[name] = {"passes_f32": row,
@@ -606,7 +605,7 @@ def bench_conv(F, args, reps=5, only=None):
                               "layers": nl}
     res["config"] = {"batch": nb, "layout": "NHWC", "dtype": "e5m2 x e5m2 -> f32 / e5m2",
                      "timing": "CUDA-graph replays (device time incl. dgrad's weight flip, "
-                               "wgrad's split-K sum, Q(dW), update and scaler); in the step, "
+                               "wgrad's split-K sum + Q(dW), update + scaler step); in the step, "
                                "fprop, dgrad and wgrad run as parallel graph branches"}
     return res
 

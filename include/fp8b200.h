@@ -160,6 +160,10 @@ typedef struct {
     int32_t last_action;
     int32_t last_grads_finite;
     double last_scale_after;
+    /* device-internal: arrival ticket of a fused update + step (see
+     * fp8b_sgd_args_t.step_scaler); zero outside a running update */
+    uint32_t step_ticket;
+    uint32_t reserved;
 } fp8b_loss_scaler_t;
 
 int fp8b_loss_scaler_init(fp8b_loss_scaler_t *dev_state, const fp8b_loss_scaler_t *host_opts,
@@ -190,8 +194,15 @@ typedef struct {
     uint8_t *w_e5m2;            /* optional fused Q_RNE(decode(master_new)) for the next
                                    fprop (nn.cpp:192-193), E5M2 codes */
     int32_t w_saturate;
-    int32_t reserved;
+    int32_t step_scaler;        /* 1: once the whole update has read the scale, run
+                                   LossScaler::step(grads_finite(skip_counters),
+                                   step_iteration) on `scaler` from the update's last
+                                   CTA -- the fp8b_loss_scaler_step that follows the
+                                   iteration's last update (nn.cpp:546-547) without its
+                                   own launch. At most one such update per scaler in
+                                   flight. */
     int64_t *w_counters;        /* device int64[3] or NULL */
+    int64_t step_iteration;     /* for step_scaler */
 } fp8b_sgd_args_t;
 
 /* update_tensor (nn.cpp:417-432) as driven by Network::apply_update

@@ -583,11 +583,15 @@ def sgd_momentum_update(grad: torch.Tensor, grad_fmt: str, master: torch.Tensor,
                         block_offset: int = 0, rbits: Optional[torch.Tensor] = None,
                         master_counters: Optional[Counters] = None,
                         w_e5m2: Optional[torch.Tensor] = None, w_saturate: bool = False,
-                        w_counters: Optional[Counters] = None, stream=None) -> None:
+                        w_counters: Optional[Counters] = None,
+                        step_scaler_iteration: Optional[int] = None, stream=None) -> None:
     """update_tensor (nn.cpp:417-432) for one parameter tensor, in place.
 
     grad: device codes (grad_fmt "fp8"/"fp16") or FP32 values (grad_fmt "f32");
-    master: FP16 codes (int16 tensor); momentum: FP32."""
+    master: FP16 codes (int16 tensor); momentum: FP32.
+    step_scaler_iteration: when given (the iteration's last update), the update
+    also runs LossScaler::step(grads_finite(skip_counters), iteration) on
+    `scaler` once every CTA has read the scale -- no separate step launch."""
     gf = {"fp8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16, "f32": _lib.F32}.get(grad_fmt)
     if gf is None:
         raise ValueError(f"unknown gradient format: {grad_fmt}")
@@ -599,8 +603,10 @@ def sgd_momentum_update(grad: torch.Tensor, grad_fmt: str, master: torch.Tensor,
                         skip_counters.ptr if skip_counters is not None else None,
                         _mode(master_mode), _BITS[bits], int(seed), int(block_offset),
                         _ptr(rbits), master_counters.ptr if master_counters else None,
-                        _ptr(w_e5m2), int(bool(w_saturate)), 0,
-                        w_counters.ptr if w_counters else None)
+                        _ptr(w_e5m2), int(bool(w_saturate)),
+                        0 if step_scaler_iteration is None else 1,
+                        w_counters.ptr if w_counters else None,
+                        0 if step_scaler_iteration is None else int(step_scaler_iteration))
     check(LIB.fp8b_sgd_momentum_update(grad.data_ptr(), gf, master.data_ptr(),
                                        momentum.data_ptr(), n, args, _stream(stream)),
           "sgd_momentum_update")

@@ -47,7 +47,8 @@ class LossScalerState(C.Structure):
                 ("growth_interval", _i64), ("steps_since_overflow", _i64),
                 ("sched_iter", _i64 * MAX_SCHEDULE), ("sched_scale", C.c_double * MAX_SCHEDULE),
                 ("last_iteration", _i64), ("last_action", _i32), ("last_grads_finite", _i32),
-                ("last_scale_after", C.c_double)]
+                ("last_scale_after", C.c_double), ("step_ticket", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 class SgdArgs(C.Structure):
@@ -55,7 +56,8 @@ class SgdArgs(C.Structure):
                 ("scale", C.c_float), ("scaler", _vp), ("skip_counters", _vp),
                 ("master_mode", _i32), ("bits", _i32), ("seed", _u64), ("block_offset", _i64),
                 ("rbits", _vp), ("master_counters", _vp), ("w_e5m2", _vp),
-                ("w_saturate", _i32), ("reserved", _i32), ("w_counters", _vp)]
+                ("w_saturate", _i32), ("step_scaler", _i32), ("w_counters", _vp),
+                ("step_iteration", _i64)]
 
 
 class DenseStep(C.Structure):

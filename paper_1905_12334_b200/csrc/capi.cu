@@ -409,6 +409,8 @@ int fp8b_loss_scaler_init(fp8b_loss_scaler_t* dev_state, const fp8b_loss_scaler_
     h.last_action = FP8B_ACT_NONE;
     h.last_grads_finite = 1;
     h.last_scale_after = o->scale;
+    h.step_ticket = 0;
+    h.reserved = 0;
     if (cudaMemcpyAsync(dev_state, &h, sizeof(h), cudaMemcpyHostToDevice, S(stream)) != cudaSuccess ||
         cudaStreamSynchronize(S(stream)) != cudaSuccess) {
         cudaGetLastError();
@@ -451,7 +453,16 @@ int fp8b_sgd_momentum_update(const void* grad, int32_t grad_fmt, uint16_t* maste
     }
     if (!args->scaler && !(args->scale > 0.0f))
         return fail(FP8B_EINVAL, "loss scale must be finite and positive");
-    if (n == 0) return FP8B_OK;
+    if (args->step_scaler && !args->scaler)
+        return fail(FP8B_EINVAL, "sgd: step_scaler needs a device scaler");
+    if (n == 0) {
+        if (args->step_scaler) {  // nothing to update: the step alone
+            fp8b::launch_scaler_step(const_cast<fp8b_loss_scaler_t*>(args->scaler),
+                                     args->skip_counters, 1, args->step_iteration, S(stream));
+            return check_launch(1);
+        }
+        return FP8B_OK;
+    }
     if (!grad || !master || !momentum) return fail(FP8B_EINVAL, "sgd: null tensor");
     fp8b::LfsrTables tabs{nullptr, nullptr};
     if (args->master_mode == FP8B_SR && args->bits == FP8B_BITS_LFSR) {

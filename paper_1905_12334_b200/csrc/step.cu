@@ -180,17 +180,20 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     u.seed = s->seed ? s->seed : 1;
     u.w_e5m2 = s->w_q;
     u.w_saturate = s->saturate;
+    // LossScaler::step(grads_finite, iteration) (nn.cpp:547) rides on the step's
+    // last update kernel (its last CTA, after every CTA has read the scale)
+    u.step_iteration = s->iteration;
+    u.step_scaler = s->b_master ? 0 : 1;
     FP8B_TRY(fp8b_sgd_momentum_update(s->qdw, FP8B_E5M2, s->w_master, s->w_momentum, I * O, &u,
                                       stream));
     if (s->b_master) {
         u.two_lambda = 0.0f;  // biases are not regularised (nn.cpp:445, 452)
         u.seed = s->seed + 1 ? s->seed + 1 : 1;
         u.w_e5m2 = nullptr;
+        u.step_scaler = 1;
         FP8B_TRY(fp8b_sgd_momentum_update(s->db, FP8B_F32, s->b_master, s->b_momentum, O, &u,
                                           stream));
     }
-    // ---- LossScaler::step(grads_finite, iteration) (nn.cpp:547)
-    FP8B_TRY(fp8b_loss_scaler_step(s->scaler, s->gate, 1, s->iteration, stream));
 #undef FP8B_TRY
     return FP8B_OK;
 }

@@ -25,7 +25,68 @@ struct UpdArgs {
     uint8_t* w8;
     int w_sat;
     int64_t* wcnt;
+    int step_scaler;     // run the scaler step from the kernel's last CTA
+    int64_t iteration;
 };
+
+// ---------------------------------------------------------- loss scaler
+// loss_scaling.cpp:40-47
+__device__ double scaler_min_threshold(const fp8b_loss_scaler_t& s, int64_t it) {
+    double thr = 1.0;
+    for (int i = 0; i < s.n_schedule; ++i) {
+        if (s.sched_iter[i] > it) break;
+        thr = s.sched_scale[i];
+    }
+    return thr;
+}
+
+// loss_scaling.cpp:49-83
+__device__ void scaler_step_dev(fp8b_loss_scaler_t* s, const int64_t* counters, int finite_in,
+                                int64_t iteration) {
+    const bool finite = counters ? (counters[0] + counters[2]) == 0 : finite_in != 0;
+    int action = FP8B_ACT_NONE;
+    if (s->kind == FP8B_SCALER_DYNAMIC_BACKOFF) {
+        const double thr = scaler_min_threshold(*s, iteration);
+        if (!finite) {
+            const double cand = s->scale * s->backoff_factor;
+            if (cand < thr) { s->scale = thr; action = FP8B_ACT_CLAMPED_TO_MIN; }
+            else { s->scale = cand; action = FP8B_ACT_BACKOFF; }
+            s->steps_since_overflow = 0;
+        } else {
+            ++s->steps_since_overflow;
+            if (s->steps_since_overflow >= s->growth_interval) {
+                s->scale *= s->growth_factor;
+                s->steps_since_overflow = 0;
+                action = FP8B_ACT_GROWTH;
+            }
+            if (s->scale < thr) { s->scale = thr; action = FP8B_ACT_CLAMPED_TO_MIN; }
+        }
+    }
+    s->last_iteration = iteration;
+    s->last_action = action;
+    s->last_grads_finite = finite ? 1 : 0;
+    s->last_scale_after = s->scale;
+}
+
+__global__ void scaler_step_kernel(fp8b_loss_scaler_t* s, const int64_t* counters, int finite_in,
+                                   int64_t iteration) {
+    scaler_step_dev(s, counters, finite_in, iteration);
+}
+
+// Fused LossScaler::step (fp8b_sgd_args_t.step_scaler): every CTA reads the scale
+// before it gets here, so the CTA that draws the last ticket may advance it.
+__device__ __forceinline__ void upd_tail(const UpdArgs& a) {
+    if (!a.step_scaler) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fp8b_loss_scaler_t* sc = const_cast<fp8b_loss_scaler_t*>(a.scaler);
+        __threadfence();
+        if (atomicAdd(&sc->step_ticket, 1u) == gridDim.x - 1) {
+            sc->step_ticket = 0;
+            scaler_step_dev(sc, a.skip, 1, a.iteration);
+        }
+    }
+}
 
 __device__ __forceinline__ bool upd_skipped(const UpdArgs& a) {
     return a.skip && (a.skip[0] + a.skip[2]) != 0;
@@ -129,7 +190,7 @@ __global__ void __launch_bounds__(NT, MINB) sgd_elem_kernel(const void* __restri
                                                             uint16_t* __restrict__ master,
                                                             float* __restrict__ mom, int64_t n,
                                                             UpdArgs a, int aligned) {
-    if (upd_skipped(a)) return;
+    if (upd_skipped(a)) { upd_tail(a); return; }
     const Unscale us(upd_scale(a));
     const bool wsat = a.w_sat != 0;
     uint32_t mb = 0, mn = 0, mu_ = 0, wb = 0, wn = 0, wu = 0;
@@ -189,6 +250,7 @@ __global__ void __launch_bounds__(NT, MINB) sgd_elem_kernel(const void* __restri
     // counters are dead code (and compiled out) unless the caller asked for them
     if (CNT && a.mcnt) flush_counters<NT>(mb - mn, mu_, mn, a.mcnt);
     if (CNT && a.wcnt) flush_counters<NT>(wb - wn, wu, wn, a.wcnt);
+    upd_tail(a);
 }
 
 // Reference-stream SR master: quantize(Tensor(w32), kFp16, {Stochastic, seed})
@@ -216,7 +278,7 @@ __global__ void __launch_bounds__(kWarpUpdThreads, 1)
                          LfsrTables tabs) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t tab_bar;
-    if (upd_skipped(a)) return;
+    if (upd_skipped(a)) { upd_tail(a); return; }
     const Unscale us(upd_scale(a));
     const bool wsat = a.w_sat != 0;
     uint32_t mb = 0, mn = 0, mu_ = 0, wb = 0, wn = 0, wu = 0;
@@ -333,6 +395,7 @@ __global__ void __launch_bounds__(kWarpUpdThreads, 1)
     }
     if (CNT && a.mcnt) flush_counters<kWarpUpdThreads>(mb - mn, mu_, mn, a.mcnt);
     if (CNT && a.wcnt) flush_counters<kWarpUpdThreads>(wb - wn, wu, wn, a.wcnt);
+    upd_tail(a);
 }
 
 // Tail / unaligned variant: blocks [block_begin, nblocks) with scalar accesses.
@@ -343,7 +406,7 @@ __global__ void __launch_bounds__(256) sgd_lfsr_kernel(const void* __restrict__ 
                                                        UpdArgs a, int64_t block_offset,
                                                        LfsrTables tabs, int64_t block_begin,
                                                        int vec) {
-    if (upd_skipped(a)) return;
+    if (upd_skipped(a)) { upd_tail(a); return; }
     __shared__ uint32_t smem_w[2][8];
     const Unscale us(upd_scale(a));
     const bool wsat = a.w_sat != 0;
@@ -425,45 +488,7 @@ __global__ void __launch_bounds__(256) sgd_lfsr_kernel(const void* __restrict__ 
     }
     if (a.mcnt) flush_counters<256>(mb - mn, mu_, mn, a.mcnt);
     if (a.wcnt) flush_counters<256>(wb - wn, wu, wn, a.wcnt);
-}
-
-// ---------------------------------------------------------- loss scaler
-// loss_scaling.cpp:40-47
-__device__ double scaler_min_threshold(const fp8b_loss_scaler_t& s, int64_t it) {
-    double thr = 1.0;
-    for (int i = 0; i < s.n_schedule; ++i) {
-        if (s.sched_iter[i] > it) break;
-        thr = s.sched_scale[i];
-    }
-    return thr;
-}
-
-// loss_scaling.cpp:49-83
-__global__ void scaler_step_kernel(fp8b_loss_scaler_t* s, const int64_t* counters, int finite_in,
-                                   int64_t iteration) {
-    const bool finite = counters ? (counters[0] + counters[2]) == 0 : finite_in != 0;
-    int action = FP8B_ACT_NONE;
-    if (s->kind == FP8B_SCALER_DYNAMIC_BACKOFF) {
-        const double thr = scaler_min_threshold(*s, iteration);
-        if (!finite) {
-            const double cand = s->scale * s->backoff_factor;
-            if (cand < thr) { s->scale = thr; action = FP8B_ACT_CLAMPED_TO_MIN; }
-            else { s->scale = cand; action = FP8B_ACT_BACKOFF; }
-            s->steps_since_overflow = 0;
-        } else {
-            ++s->steps_since_overflow;
-            if (s->steps_since_overflow >= s->growth_interval) {
-                s->scale *= s->growth_factor;
-                s->steps_since_overflow = 0;
-                action = FP8B_ACT_GROWTH;
-            }
-            if (s->scale < thr) { s->scale = thr; action = FP8B_ACT_CLAMPED_TO_MIN; }
-        }
-    }
-    s->last_iteration = iteration;
-    s->last_action = action;
-    s->last_grads_finite = finite ? 1 : 0;
-    s->last_scale_after = s->scale;
+    upd_tail(a);
 }
 
 // loss_scaling.cpp:89-92
@@ -486,6 +511,9 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     a.elem_offset = args.block_offset * kBlock; a.rbits = args.rbits;
     a.mcnt = args.master_counters; a.w8 = args.w_e5m2; a.w_sat = args.w_saturate;
     a.wcnt = args.w_counters;
+    a.step_scaler = 0;  // set on the call's last kernel only
+    a.iteration = args.step_iteration;
+    const int want_step = args.step_scaler && args.scaler;
     constexpr int NT = 256;
     const bool cnt = a.mcnt != nullptr || a.wcnt != nullptr;
     const bool aligned = ((uintptr_t)grad % 16 == 0) && ((uintptr_t)master % 16 == 0) &&
@@ -506,6 +534,7 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
             if (wpc > kWarpUpdThreads / 32) wpc = kWarpUpdThreads / 32;
             const int64_t need = (nfull + wpc - 1) / wpc;
             if (need < g) g = need;
+            a.step_scaler = want_step && nfull == nb;  // no tail kernel follows
             fn<<<(int)g, (int)(32 * wpc), smem, st>>>(grad, master, mom, nfull, a, args.block_offset,
                                                       tabs);
             begin = nfull;
@@ -515,6 +544,7 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sgd_lfsr_kernel<GFMT>, 256, 0);
             int64_t g = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
             if (nb - begin < g) g = nb - begin;
+            a.step_scaler = want_step;
             sgd_lfsr_kernel<GFMT><<<(int)g, 256, 0, st>>>(grad, master, mom, n, a,
                                                           args.block_offset, tabs, begin,
                                                           aligned ? 1 : 0);
@@ -525,6 +555,7 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     const int64_t need = ((aligned ? n / 16 : n) + NT - 1) / NT;
     if (need < g) g = need < 1 ? 1 : need;
     const int al = aligned ? 1 : 0;
+    a.step_scaler = want_step;
     // 4 groups x 4 parameters per thread, <= 64 registers (4 CTAs of 256 per SM):
     // measured over 2^28 parameters against 2 groups at 72 registers, 4x6, 4x5,
     // 8x2, 8x3 (scripts/upd_time.py): RNE 0.718 -> 0.580 ms, counter SR + E5M2 W

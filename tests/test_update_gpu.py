@@ -171,3 +171,44 @@ def test_unscale_true_division(fp8):
     s = fp8.LossScaler("constant", 4096.0)
     u = s.unscale(np.array([4096.0, -8192.0, np.inf, np.nan], np.float32)).cpu().numpy()
     assert u[0] == 1.0 and u[1] == -2.0 and np.isinf(u[2]) and np.isnan(u[3])
+
+
+@pytest.mark.parametrize("n", [5000, 3 * 4096, 1 << 20, 512 * 4096, 700 * 4096 + 33])
+@pytest.mark.parametrize("mode,bits", [("nearest-even", "lfsr"), ("stochastic", "lfsr"),
+                                       ("stochastic", "counter")])
+@pytest.mark.parametrize("overflow", [False, True])
+def test_fused_scaler_step_equals_update_then_step(fp8, n, mode, bits, overflow):
+    """step_scaler: the update's last CTA runs LossScaler::step after every CTA
+    has read the scale. Masters, momentum, E5M2 W and the whole scaler state
+    equal the separate update + fp8b_loss_scaler_step, over several iterations
+    (growth, backoff and floor clamps), with the update skipped on overflow."""
+    import torch
+    rng = np.random.default_rng(n % 1000 + len(mode))
+    m0 = O.quantize(rng.normal(0, 1 / 32, n).astype(np.float32), "fp16")[0].view(np.int16)
+    g0 = O.quantize(rng.normal(0, 1.0, n).astype(np.float32), "fp8")[0].astype(np.uint8)
+    out = []
+    for fused in (False, True):
+        master, mom, grad = _dev(m0.copy()), _dev(np.zeros(n, np.float32)), _dev(g0)
+        w8 = torch.empty(n, dtype=torch.uint8, device="cuda")
+        sc = fp8.LossScaler("dynamic-backoff", 65536.0, growth_interval=2,
+                            min_threshold_schedule=[(0, 8192.0), (3, 32768.0)])
+        gate = fp8.Counters()
+        trace = []
+        for it in range(6):
+            gate.zero_()
+            if overflow and it in (1, 4):
+                gate.t[0] = 3  # an overflow count: update skipped, scale backs off
+            kw = dict(lr=0.05, mu=0.9, scaler=sc, skip_counters=gate, master_mode=mode, bits=bits,
+                      seed=9 + it, w_e5m2=w8)
+            if fused:
+                fp8.sgd_momentum_update(grad, "fp8", master, mom, step_scaler_iteration=it, **kw)
+            else:
+                fp8.sgd_momentum_update(grad, "fp8", master, mom, **kw)
+                sc.step_async(True, it, counters=gate)
+            trace.append(sc.state.cpu().numpy().tobytes())
+        out.append((master.cpu().numpy(), mom.cpu().numpy().view(np.uint32), w8.cpu().numpy(), trace))
+    a, b = out
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+    np.testing.assert_array_equal(a[2], b[2])
+    assert a[3] == b[3]

@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
             if (warp == 2 && lane == 0) HTRACE(5, (tile - blockIdx.x) / gridDim.x);
             if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
         }
-        if (lane == 0) bulk_wait_all();
+        if (lane == 0) bulk_wait_read0();
     }
     if (p.ep.cq_counters) flush_counters<THREADS_MAX>(co, cu, cn, p.ep.cq_counters);
     fence_before();

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
             if (++acc == 2) { acc = 0; accphase ^= 1; }
         }
     }
-    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
+    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_read0();  // smem read out; the writes land by grid completion
     if (MODE == 0 && p.ep.cq_counters) flush_counters<threads_of<EW>()>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     __syncthreads();

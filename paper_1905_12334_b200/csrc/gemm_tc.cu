@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (++acc == 2) { acc = 0; accphase ^= 1; }
         }
     }
-    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
+    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_read0();  // smem read out; the writes land by grid completion
     if (p.ep.cq_counters) flush_counters<NUM_THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     __syncthreads();
@@ -1023,7 +1023,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
             if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
         }
     }
-    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_all();
+    if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_read0();  // smem read out; the writes land by grid completion
     if (p.ep.cq_counters) flush_counters<G::THREADS>(co, cu, cn, p.ep.cq_counters);
     fence_before();
     cluster_sync_all();

@@ -203,6 +203,11 @@ typedef struct {
                                    flight. */
     int64_t *w_counters;        /* device int64[3] or NULL */
     int64_t step_iteration;     /* for step_scaler */
+    const int64_t *skip_counters2; /* optional second int64[3]: the gate is the element-wise
+                                      sum skip_counters + skip_counters2 (the step's two
+                                      counter sets, nn.cpp:401-411, with no merge launch) */
+    int64_t *gate_out;          /* with step_scaler: the merged int64[3] gate is stored
+                                   here by the update's last CTA (may alias neither input) */
 } fp8b_sgd_args_t;
 
 /* update_tensor (nn.cpp:417-432) as driven by Network::apply_update

@@ -584,14 +584,18 @@ def sgd_momentum_update(grad: torch.Tensor, grad_fmt: str, master: torch.Tensor,
                         master_counters: Optional[Counters] = None,
                         w_e5m2: Optional[torch.Tensor] = None, w_saturate: bool = False,
                         w_counters: Optional[Counters] = None,
-                        step_scaler_iteration: Optional[int] = None, stream=None) -> None:
+                        step_scaler_iteration: Optional[int] = None,
+                        skip_counters2: Optional[Counters] = None,
+                        gate_out: Optional[Counters] = None, stream=None) -> None:
     """update_tensor (nn.cpp:417-432) for one parameter tensor, in place.
 
     grad: device codes (grad_fmt "fp8"/"fp16") or FP32 values (grad_fmt "f32");
     master: FP16 codes (int16 tensor); momentum: FP32.
     step_scaler_iteration: when given (the iteration's last update), the update
     also runs LossScaler::step(grads_finite(skip_counters), iteration) on
-    `scaler` once every CTA has read the scale -- no separate step launch."""
+    `scaler` once every CTA has read the scale -- no separate step launch.
+    skip_counters2 / gate_out: the gate is skip_counters + skip_counters2, and
+    (with step_scaler_iteration) the merged counts are stored in gate_out."""
     gf = {"fp8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16, "f32": _lib.F32}.get(grad_fmt)
     if gf is None:
         raise ValueError(f"unknown gradient format: {grad_fmt}")
@@ -606,7 +610,9 @@ def sgd_momentum_update(grad: torch.Tensor, grad_fmt: str, master: torch.Tensor,
                         _ptr(w_e5m2), int(bool(w_saturate)),
                         0 if step_scaler_iteration is None else 1,
                         w_counters.ptr if w_counters else None,
-                        0 if step_scaler_iteration is None else int(step_scaler_iteration))
+                        0 if step_scaler_iteration is None else int(step_scaler_iteration),
+                        skip_counters2.ptr if skip_counters2 is not None else None,
+                        gate_out.ptr if gate_out is not None else None)
     check(LIB.fp8b_sgd_momentum_update(grad.data_ptr(), gf, master.data_ptr(),
                                        momentum.data_ptr(), n, args, _stream(stream)),
           "sgd_momentum_update")

@@ -57,7 +57,7 @@ class SgdArgs(C.Structure):
                 ("master_mode", _i32), ("bits", _i32), ("seed", _u64), ("block_offset", _i64),
                 ("rbits", _vp), ("master_counters", _vp), ("w_e5m2", _vp),
                 ("w_saturate", _i32), ("step_scaler", _i32), ("w_counters", _vp),
-                ("step_iteration", _i64)]
+                ("step_iteration", _i64), ("skip_counters2", _vp), ("gate_out", _vp)]
 
 
 class DenseStep(C.Structure):

@@ -455,7 +455,13 @@ int fp8b_sgd_momentum_update(const void* grad, int32_t grad_fmt, uint16_t* maste
         return fail(FP8B_EINVAL, "loss scale must be finite and positive");
     if (args->step_scaler && !args->scaler)
         return fail(FP8B_EINVAL, "sgd: step_scaler needs a device scaler");
+    if (args->gate_out && !args->step_scaler)
+        return fail(FP8B_EINVAL, "sgd: gate_out is written by the fused scaler step (step_scaler)");
+    if (args->gate_out && (args->gate_out == args->skip_counters || args->gate_out == args->skip_counters2))
+        return fail(FP8B_EINVAL, "sgd: gate_out must not alias the gate's inputs");
     if (n == 0) {
+        if (args->step_scaler && args->skip_counters2)
+            return fail(FP8B_EINVAL, "sgd: an empty update cannot merge the gate");
         if (args->step_scaler) {  // nothing to update: the step alone
             fp8b::launch_scaler_step(const_cast<fp8b_loss_scaler_t*>(args->scaler),
                                      args->skip_counters, 1, args->step_iteration, S(stream));

@@ -6,18 +6,15 @@
 // LossScaler::step, with a full FP32 tensor materialised between each. Here the
 // output Q nodes are fused into the GEMM epilogues, the finiteness check is the
 // Q kernels' own counters, the update skips itself on device and also emits the
-// next step's E5M2 weights, and the scaler state never leaves HBM: 8-10 kernel
-// launches, no host synchronisation, CUDA-graph capturable.
+// next step's E5M2 weights, the gate merge and the scaler step ride on the last
+// update kernel, and the scaler state never leaves HBM: 6 kernel launches (8 with
+// a bias), no host synchronisation, CUDA-graph capturable.
 #include <cstring>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace fp8b {
-__global__ void merge_gate_kernel(const int64_t* c, int64_t* gate) {
-    if (threadIdx.x < 3) gate[threadIdx.x] = c[threadIdx.x] + c[3 + threadIdx.x];
-}
-
 // Side streams for the step's independent branches. Given Q(X) and Q(E), the
 // three GEMMs of the layer are independent (fprop reads qx and w_q, bprop qe and
 // w_q, wgrad qx and qe) and together need 64 of the 148 SMs at config-1 size, so
@@ -163,10 +160,9 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
         FP8B_TRY(fp8b_gemm(s->qx, s->qe, I, O, B, FP8B_E5M2, &gw, side1));
     }
     if (!br.join()) return FP8B_ECUDA;
-    // grads_finite gate (nn.cpp:401-411): overflow of qe/qdw/qdx, NaN in qdw, non-finite db
-    fp8b::merge_gate_kernel<<<1, 32, 0, st>>>(s->counters, s->gate);
-    if (cudaGetLastError() != cudaSuccess) return FP8B_ECUDA;
-    fp8b::note_launches(1);
+    // grads_finite gate (nn.cpp:401-411): overflow of qe/qdw/qdx, NaN in qdw,
+    // non-finite db = the sum of the step's two counter sets. The update kernels
+    // read both; the last one stores the merged gate (no merge launch).
     // ---- apply_update (nn.cpp:436-458), skipped on device when the gate is set
     fp8b_sgd_args_t u{};
     u.lr = s->lr;
@@ -174,7 +170,8 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     u.two_lambda = s->two_lambda;
     u.scale = 1.0f;
     u.scaler = s->scaler;
-    u.skip_counters = s->gate;
+    u.skip_counters = s->counters;
+    u.skip_counters2 = s->counters + 3;
     u.master_mode = s->master_mode;
     u.bits = s->bits;
     u.seed = s->seed ? s->seed : 1;
@@ -184,6 +181,7 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
     // last update kernel (its last CTA, after every CTA has read the scale)
     u.step_iteration = s->iteration;
     u.step_scaler = s->b_master ? 0 : 1;
+    u.gate_out = s->b_master ? nullptr : s->gate;
     FP8B_TRY(fp8b_sgd_momentum_update(s->qdw, FP8B_E5M2, s->w_master, s->w_momentum, I * O, &u,
                                       stream));
     if (s->b_master) {
@@ -191,6 +189,7 @@ int fp8b_dense_step(const fp8b_dense_step_t* s, void* stream) {
         u.seed = s->seed + 1 ? s->seed + 1 : 1;
         u.w_e5m2 = nullptr;
         u.step_scaler = 1;
+        u.gate_out = s->gate;
         FP8B_TRY(fp8b_sgd_momentum_update(s->db, FP8B_F32, s->b_master, s->b_momentum, O, &u,
                                           stream));
     }

@@ -27,6 +27,8 @@ struct UpdArgs {
     int64_t* wcnt;
     int step_scaler;     // run the scaler step from the kernel's last CTA
     int64_t iteration;
+    const int64_t* skip2;  // optional second counter set of the gate
+    int64_t* gate_out;     // merged gate, stored by the last CTA (with step_scaler)
 };
 
 // ---------------------------------------------------------- loss scaler
@@ -83,13 +85,25 @@ __device__ __forceinline__ void upd_tail(const UpdArgs& a) {
         __threadfence();
         if (atomicAdd(&sc->step_ticket, 1u) == gridDim.x - 1) {
             sc->step_ticket = 0;
-            scaler_step_dev(sc, a.skip, 1, a.iteration);
+            if (a.skip && a.skip2) {  // merged gate (nn.cpp:401-411)
+                int64_t g[3];
+                for (int i = 0; i < 3; ++i) g[i] = a.skip[i] + a.skip2[i];
+                if (a.gate_out)
+                    for (int i = 0; i < 3; ++i) a.gate_out[i] = g[i];
+                scaler_step_dev(sc, nullptr, (g[0] + g[2]) == 0, a.iteration);
+            } else {
+                if (a.skip && a.gate_out)
+                    for (int i = 0; i < 3; ++i) a.gate_out[i] = a.skip[i];
+                scaler_step_dev(sc, a.skip, 1, a.iteration);
+            }
         }
     }
 }
 
 __device__ __forceinline__ bool upd_skipped(const UpdArgs& a) {
-    return a.skip && (a.skip[0] + a.skip[2]) != 0;
+    int64_t bad = a.skip ? a.skip[0] + a.skip[2] : 0;
+    if (a.skip2) bad += a.skip2[0] + a.skip2[2];
+    return bad != 0;
 }
 __device__ __forceinline__ float upd_scale(const UpdArgs& a) {
     return a.scaler ? __double2float_rn(a.scaler->scale) : a.scale;
@@ -513,6 +527,8 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     a.wcnt = args.w_counters;
     a.step_scaler = 0;  // set on the call's last kernel only
     a.iteration = args.step_iteration;
+    a.skip2 = args.skip_counters2;
+    a.gate_out = args.gate_out;
     const int want_step = args.step_scaler && args.scaler;
     constexpr int NT = 256;
     const bool cnt = a.mcnt != nullptr || a.wcnt != nullptr;

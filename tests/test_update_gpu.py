@@ -212,3 +212,37 @@ def test_fused_scaler_step_equals_update_then_step(fp8, n, mode, bits, overflow)
     np.testing.assert_array_equal(a[1], b[1])
     np.testing.assert_array_equal(a[2], b[2])
     assert a[3] == b[3]
+
+
+@pytest.mark.parametrize("n", [3 * 4096 + 5, 512 * 4096])
+def test_merged_gate_two_counter_sets(fp8, n):
+    """skip_counters2 / gate_out: the update is gated on the sum of two counter
+    sets (the step's forward-side and wgrad-side Q nodes), and its last CTA stores
+    the merged gate and steps the scaler on it -- equal to a merge, an update and
+    a step done separately."""
+    import torch
+    rng = np.random.default_rng(n % 977)
+    m0 = O.quantize(rng.normal(0, 1 / 32, n).astype(np.float32), "fp16")[0].view(np.int16)
+    g0 = O.quantize(rng.normal(0, 1.0, n).astype(np.float32), "fp8")[0].astype(np.uint8)
+    for c1, c2 in [((0, 4, 0), (0, 1, 0)), ((0, 0, 0), (2, 0, 0)), ((0, 0, 1), (0, 0, 0))]:
+        res = []
+        for fused in (False, True):
+            master, mom, grad = _dev(m0.copy()), _dev(np.zeros(n, np.float32)), _dev(g0)
+            sc = fp8.LossScaler("dynamic-backoff", 65536.0, growth_interval=1,
+                                min_threshold_schedule=[(0, 8192.0)])
+            a, b, gate = fp8.Counters(), fp8.Counters(), fp8.Counters()
+            a.t.copy_(torch.tensor(c1)); b.t.copy_(torch.tensor(c2))
+            kw = dict(lr=0.05, mu=0.9, scaler=sc, master_mode="stochastic", seed=3)
+            if fused:
+                fp8.sgd_momentum_update(grad, "fp8", master, mom, skip_counters=a, skip_counters2=b,
+                                        gate_out=gate, step_scaler_iteration=7, **kw)
+            else:
+                gate.t.copy_(a.t + b.t)
+                fp8.sgd_momentum_update(grad, "fp8", master, mom, skip_counters=gate, **kw)
+                sc.step_async(True, 7, counters=gate)
+            res.append((master.cpu().numpy(), mom.cpu().numpy().view(np.uint32), gate.values(),
+                        sc.state.cpu().numpy().tobytes()))
+        assert res[0][2] == res[1][2] == tuple(x + y for x, y in zip(c1, c2))
+        np.testing.assert_array_equal(res[0][0], res[1][0])
+        np.testing.assert_array_equal(res[0][1], res[1][1])
+        assert res[0][3] == res[1][3]

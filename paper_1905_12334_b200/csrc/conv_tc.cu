@@ -581,6 +581,23 @@ int launch_conv_tc(int kind, const void* a, const void* b, float* out, int fmt,
         if (rc != FP8B_ENOTSUP) return rc;
         *nlaunch = 0;
     }
+    // 1x1 wgrad dW[F, C] = e^T . x is the GEMM with A = e [K = P, M = F] (MN-major)
+    // and B = x [K = P, N = C] (N-major). Through the pair-tile GEMM's split-K it
+    // wins only for few pixels (measured as graph replays: P = 12544, 2048 x 512:
+    // 24.8 vs 34.7 us; P = 50176, 256 x 1024: 40.8 vs 31.6 us; 56 x 56 far slower).
+    // FP8B_CONV_1X1_WGRAD_PIX overrides the pixel limit (diagnostic; 0 disables).
+    if (kind == 2 && k == 1 && pad == 0 && g.stride == 1 && out) {
+        const char* e3 = getenv("FP8B_CONV_1X1_WGRAD_PIX");
+        const int64_t lim = e3 && e3[0] ? atoll(e3) : 16384;
+        const int64_t P = g.n * g.h * g.w;
+        if (P <= lim && g.f >= 256 && g.c >= 256) {
+            const EpiArgs ep{out, nullptr, g.yq, g.yq_fmt, g.yq_mode, g.yq_seed, g.yq_saturate, g.yq_counters};
+            rc = launch_gemm_tc(b, a, g.f, g.c, P, fmt, 1, 1, ep, st, nlaunch);
+            if (rc == FP8B_OK && g.yq && q_done) *q_done = 1;
+            if (rc != FP8B_ENOTSUP) return rc;
+            *nlaunch = 0;
+        }
+    }
     if (kind == 0) {
         rc = fmt == FP8B_E5M2 ? tc::cv::fprop<1>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, g)
                               : tc::cv::fprop<2>(a, b, out, g.n, g.h, g.w, g.c, g.f, k, pad, st, g);

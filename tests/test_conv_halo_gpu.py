@@ -195,3 +195,40 @@ def test_halo_wgrad_exact_grid(fp8, env, shape):
                                       err_msg=f"halo={halo}")
         np.testing.assert_array_equal(q.codes.cpu().numpy(), codes.astype(np.uint8))
         assert cq.values() == tuple(int(v) for v in cnt), halo
+
+
+@pytest.mark.parametrize("shape", [(4, 256, 7, 7, 512), (2, 512, 5, 6, 256), (3, 320, 4, 4, 384)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("out_mode", ["nearest-even", "stochastic", "truncate"])
+def test_1x1_wgrad_gemm_route_exact(fp8, shape, out_mode):
+    """1x1 wgrad with few pixels routed to the pair-tile GEMM engine (dW = e^T . x,
+    A = e MN-major, B = x N-major, split-K) equals the im2col wgrad and the exact
+    result bit for bit on an exact operand grid; the fused Q(dW) node (RNE / TRUNC
+    / SR with counter bits) equals the standalone quantize of dW, counters included."""
+    n, c, h, w, f = shape
+    rng = np.random.default_rng(c + f + 1)
+    xc = _grid(rng, n * h * w * c, "fp8", 0.5).reshape(n, h, w, c)
+    ec = _grid(rng, n * h * w * f, "fp8", 0.25).reshape(n, h, w, f)
+    dec = lambda a: O.dequantize(a.reshape(-1), "fp8").astype(np.float64).reshape(a.shape)
+    dw_ex = np.einsum("nhwf,nhwc->fc", dec(ec), dec(xc)).astype(np.float32)
+    X, E = _qt(fp8, xc, xc.shape, "fp8"), _qt(fp8, ec, ec.shape, "fp8")
+    old = os.environ.get("FP8B_CONV_1X1_WGRAD_PIX")
+    try:
+        got = []
+        for lim in ("1000000", "0"):
+            os.environ["FP8B_CONV_1X1_WGRAD_PIX"] = lim
+            cnt = fp8.Counters()
+            dw, q = fp8.conv2d_backward_weights(X, E, 1, 1, 1, 0, layout="nhwc", engine="tensor",
+                                                out_fmt="fp8", out_mode=out_mode, out_seed=5,
+                                                out_counters=cnt)
+            np.testing.assert_array_equal(dw.cpu().numpy().reshape(-1), dw_ex.reshape(-1), err_msg=lim)
+            ref = fp8.quantize(dw.reshape(-1), "fp8", out_mode, 5, bits="counter")
+            assert (q.codes == ref.codes).all(), lim
+            assert cnt.values() == ref.counters.values(), lim
+            got.append(q.codes.cpu().numpy())
+        np.testing.assert_array_equal(got[0], got[1])
+    finally:
+        if old is None:
+            os.environ.pop("FP8B_CONV_1X1_WGRAD_PIX", None)
+        else:
+            os.environ["FP8B_CONV_1X1_WGRAD_PIX"] = old

@@ -97,30 +97,39 @@ __device__ __forceinline__ void tma_im2col_4d(const CUtensorMap* tm, void* dst, 
         : "memory");
 }
 
-// Compile-time geometry of one kernel instance.
-template <int ES, int MODE, int BN, int CB, int EW>
+// Compile-time geometry of one kernel instance. wgrad (MODE 1) tiles may hold
+// MH x NH blocks of 128 x BN: the operand stream, not the MMAs, bounds the
+// 128 x 128 tile (ncu: tensor pipe 37 % active, 32 KB of TMA rows per 271 MMA
+// cycles), and a 256 x 256 tile moves half the bytes per MAC.
+template <int ES, int MODE, int BN, int CB, int EW, int MH = 1, int NH = 1>
 struct Geo {
     static constexpr uint32_t EPI_BYTES = (uint32_t)EW * 8192;  // 2 x 4 KB per epilogue warp
     static constexpr int KPIX = 128 / ES;            // wgrad: pixels per K block
-    static constexpr uint32_t A_BYTES = MODE == 0 ? 128u * CB : 128u * 128u;
-    static constexpr uint32_t B_BYTES = MODE == 0 ? (uint32_t)BN * CB : (uint32_t)KPIX * CB;
+    static constexpr uint32_t A_HALF = 128u * 128u;  // wgrad: one 128-row block of E
+    static constexpr uint32_t B_HALF = (uint32_t)KPIX * CB;  // wgrad: one BN-wide block of X
+    static constexpr uint32_t A_BYTES = MODE == 0 ? 128u * CB : MH * A_HALF;
+    static constexpr uint32_t B_BYTES = MODE == 0 ? (uint32_t)BN * CB : NH * B_HALF;
     static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
     static constexpr int BUDGET = 232448 - (int)EPI_BYTES - 1280;
     static constexpr int STAGES = (BUDGET / (int)STAGE) > 16 ? 16 : (BUDGET / (int)STAGE);
     static constexpr uint32_t SMEM = STAGES * STAGE + EPI_BYTES + 1024 + 256;
-    static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int ACC_COLS = MH * NH * BN;    // one accumulator set
+    static constexpr int NACC = 2 * ACC_COLS <= 512 ? 2 : 1;
+    static constexpr uint32_t TMEM_COLS = NACC * ACC_COLS < 32 ? 32 : NACC * ACC_COLS;
     static constexpr uint32_t SWZ_LAYOUT = CB == 128 ? 2u : 4u;  // UMMA layout code
     static constexpr uint32_t SBO = 8u * CB;                     // 8 rows of one swizzle atom
+    static_assert(MODE == 1 || (MH == 1 && NH == 1), "block tiles are a wgrad feature");
+    static_assert(STAGES >= 2, "ring too shallow");
 };
 
 // MODE 0: fprop (A = im2col X, K-major; B = W [F, taps*C], K-major).
 // MODE 1: wgrad (A = E [P, F], MN-major; B = im2col X, MN-major), split-K.
-template <int ES, int MODE, int BN, int CB, int EW>
+template <int ES, int MODE, int BN, int CB, int EW, int MH = 1, int NH = 1>
 __global__ void __launch_bounds__(threads_of<EW>(), 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
                    const CParams p) {
-    using G = Geo<ES, MODE, BN, CB, EW>;
+    using G = Geo<ES, MODE, BN, CB, EW, MH, NH>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -201,19 +210,23 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
                         tma_load_2d(&tmB, sB, full_bar + stage, t * p.C + cb * CBE, tn * BN);
                     } else {
                         const int64_t P0 = (int64_t)kb * G::KPIX;
-                        const int f0 = tm * 128;
+                        const int f0 = tm * 128 * MH;
 #pragma unroll
-                        for (int j = 0; j < ES; ++j)  // 128 rows of F in 128-byte chunks
-                            tma_load_2d(&tmA, sA + j * (G::KPIX * 128), full_bar + stage,
-                                        f0 + j * (128 / ES), (int32_t)P0);
-                        const int col = tn * BN;  // = t * C + c0
+                        for (int mh = 0; mh < MH; ++mh)
+#pragma unroll
+                            for (int j = 0; j < ES; ++j)  // 128 rows of F in 128-byte chunks
+                                tma_load_2d(&tmA, sA + mh * G::A_HALF + j * (G::KPIX * 128),
+                                            full_bar + stage, f0 + mh * 128 + j * (128 / ES), (int32_t)P0);
+                        const int col = tn * (NH * BN);  // = t * C + c0 (a tile never straddles taps)
                         const int t = col / p.C, c0 = col - t * p.C;
                         const int kh = t / p.KW, kw = t - kh * p.KW;
                         const int n = (int)(P0 / pix_img);
                         const int r = (int)(P0 - (int64_t)n * pix_img);
                         const int oh = r / p.OW, ow = r - oh * p.OW;
-                        tma_im2col_4d(&tmB, sB, full_bar + stage, c0, ow - p.pad, oh - p.pad, n,
-                                      (uint16_t)kw, (uint16_t)kh);
+#pragma unroll
+                        for (int nh = 0; nh < NH; ++nh)
+                            tma_im2col_4d(&tmB, sB + nh * G::B_HALF, full_bar + stage, c0 + nh * BN,
+                                          ow - p.pad, oh - p.pad, n, (uint16_t)kw, (uint16_t)kh);
                     }
                     if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -225,7 +238,7 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
             uint32_t idesc = (1u << 4);
             if (ES == 1) idesc |= (1u << 7) | (1u << 10);
             if (MODE == 1) idesc |= (1u << 15) | (1u << 16);  // A and B MN-major
-            idesc |= (uint32_t)(BN >> 3) << 17;
+            idesc |= (uint32_t)((NH * BN) >> 3) << 17;
             idesc |= (uint32_t)(128 >> 4) << 24;
             int stage = 0;
             uint32_t phase = 0;
@@ -236,7 +249,7 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
                 item_of(item, tm, tn, s, kb0, kb1);
                 mbar_wait(tempty_bar + acc, accphase ^ 1);
                 fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * G::ACC_COLS);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(full_bar + stage, phase);
                     fence_after();
@@ -252,23 +265,29 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
                     } else {
 #pragma unroll
                         for (int k = 0; k < G::KPIX / UK; ++k) {
-                            const uint64_t ad = umma_desc(a_base + k * UK * 128, G::KPIX * 128, 1024);
-                            const uint64_t bd = umma_desc(b_base + k * UK * CB, G::KPIX * CB, G::SBO,
+                            // B: NH blocks of BN columns, one swizzle atom each, LBO apart
+                            const uint64_t bd = umma_desc(b_base + k * UK * CB, G::B_HALF, G::SBO,
                                                           G::SWZ_LAYOUT);
-                            mma_p<ES>(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u, leader);
+#pragma unroll
+                            for (int mh = 0; mh < MH; ++mh) {
+                                const uint64_t ad = umma_desc(a_base + mh * G::A_HALF + k * UK * 128,
+                                                              G::KPIX * 128, 1024);
+                                mma_p<ES>(d_tmem + (uint32_t)(mh * NH * BN), ad, bd, idesc,
+                                          (kb > kb0 || k) ? 1u : 0u, leader);
+                            }
                         }
                     }
                     umma_commit_p(empty_bar + stage, leader);
                     if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
                 }
                 umma_commit_p(tfull_bar + acc, leader);
-                if (++acc == 2) { acc = 0; accphase ^= 1; }
+                if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
             }
         }
     } else {
         const int quarter = warp & 3;             // TMEM lanes 32*quarter .. +31
         const int ew = warp - 2;                   // epilogue warp index
-        constexpr int NC = BN / 32;                // 32-column chunks per tile
+        constexpr int NC = NH * BN / 32;           // 32-column chunks per 128-row block
         constexpr int PER = NC / (EW / 4);         // chunks per warp (column halves when EW = 8)
         const int c_lo = (ew / 4) * PER;
         uint8_t* sbuf = smem + G::STAGES * G::STAGE + ew * 8192;
@@ -278,44 +297,48 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
             int tm, tn, s, kb0, kb1;
             item_of(item, tm, tn, s, kb0, kb1);
-            const int64_t row = (int64_t)tm * 128 + quarter * 32 + lane;
             mbar_wait(tfull_bar + acc, accphase);
             fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
-            EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
-                      (int64_t)tm * 128 + quarter * 32, lane, -1, p.qg, 0, nullptr};
 #pragma unroll 1
-            for (int c = c_lo; c < c_lo + PER; ++c) {
-                uint32_t v[32];
-                tmem_ld32(taddr + c * 32, v);
-                const int64_t col0 = (int64_t)tn * BN + c * 32;
-                if (col0 >= p.N) continue;
-                const int64_t row0 = (int64_t)tm * 128 + quarter * 32;
-                if (p.c_tma || p.q_tma) {
-                    if (MODE == 0) {
-                        const bool last = c == c_lo + PER - 1 || col0 + 32 >= p.N;
-                        epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
-                    } else {
-                        stage_store_f32(&tmC, sbuf, nst, v, lane, (int32_t)col0, (int32_t)row0, s);
+            for (int mh = 0; mh < MH; ++mh) {
+                const int64_t row0 = ((int64_t)tm * MH + mh) * 128 + quarter * 32;
+                const int64_t row = row0 + lane;
+                const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                                       (uint32_t)(acc * G::ACC_COLS + mh * NH * BN);
+                EpiTma et{p.c_tma ? &tmC : nullptr, p.q_tma ? &tmQ : nullptr, sbuf, &nst,
+                          row0, lane, -1, p.qg, 0, nullptr};
+#pragma unroll 1
+                for (int c = c_lo; c < c_lo + PER; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(taddr + c * 32, v);
+                    const int64_t col0 = (int64_t)tn * (NH * BN) + c * 32;
+                    if (col0 >= p.N) continue;
+                    if (p.c_tma || p.q_tma) {
+                        if (MODE == 0) {
+                            const bool last = c == c_lo + PER - 1 || col0 + 32 >= p.N;
+                            epilogue_chunk(p, row, col0, v, co, cu, cn, &et, last);
+                        } else {
+                            stage_store_f32(&tmC, sbuf, nst, v, lane, (int32_t)col0, (int32_t)row0, s);
+                        }
+                        continue;
                     }
-                    continue;
-                }
-                if (row >= p.M) continue;
-                if (MODE == 0) {
-                    epilogue_chunk(p, row, col0, v, co, cu, cn);
-                } else {
-                    float* dst = p.ws + ((int64_t)s * p.M + row) * p.N + col0;
-                    float4* d4 = reinterpret_cast<float4*>(dst);
+                    if (row >= p.M) continue;
+                    if (MODE == 0) {
+                        epilogue_chunk(p, row, col0, v, co, cu, cn);
+                    } else {
+                        float* dst = p.ws + ((int64_t)s * p.M + row) * p.N + col0;
+                        float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                        for (int j = 0; j < 8; ++j)
+                            d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                    }
                 }
             }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar + acc);
-            if (++acc == 2) { acc = 0; accphase ^= 1; }
+            if (++acc == G::NACC) { acc = 0; accphase ^= 1; }
         }
     }
     if ((p.c_tma || p.q_tma) && warp >= 2 && lane == 0) bulk_wait_read0();  // smem read out; the writes land by grid completion
@@ -381,14 +404,14 @@ static bool make_ws_map(CUtensorMap* tm, float* ws, int splits, int64_t m, int64
 
 static int num_sms() { return device_sm_count(); }
 
-template <int ES, int MODE, int BN, int CB, int EW = 4>
+template <int ES, int MODE, int BN, int CB, int EW = 4, int MH = 1, int NH = 1>
 static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm,
                const CUtensorMap& tqm, const CParams& p, cudaStream_t st) {
-    using G = Geo<ES, MODE, BN, CB, EW>;
-    ensure_smem_attr((const void*)conv_tc_kernel<ES, MODE, BN, CB, EW>, G::SMEM);
+    using G = Geo<ES, MODE, BN, CB, EW, MH, NH>;
+    ensure_smem_attr((const void*)conv_tc_kernel<ES, MODE, BN, CB, EW, MH, NH>, G::SMEM);
     const int items = p.tiles_m * p.tiles_n * p.splits;
     const int grid = items < num_sms() ? items : num_sms();
-    conv_tc_kernel<ES, MODE, BN, CB, EW><<<grid, threads_of<EW>(), G::SMEM, st>>>(ta, tb, tcm, tqm, p);
+    conv_tc_kernel<ES, MODE, BN, CB, EW, MH, NH><<<grid, threads_of<EW>(), G::SMEM, st>>>(ta, tb, tcm, tqm, p);
     return FP8B_OK;
 }
 
@@ -466,10 +489,25 @@ static int wgrad(const void* x, const void* e, float* dw, int64_t n, int64_t h, 
     CUtensorMap ta, tb;
     if (!make_map(&ta, e, ES, (uint64_t)f, (uint64_t)P, 128 / ES, KPIX)) return FP8B_ENOTSUP;
     if (!make_im2col(&tb, x, ES, n, h, wd, c, k, pad, bn, KPIX, swz)) return FP8B_ENOTSUP;
+    // block tiles (MH x 128 rows of F, NH x bn channels): FP8B_CONV_WGRAD_BLOCK=0 disables
+    const char* eb = getenv("FP8B_CONV_WGRAD_BLOCK");
+    const int blk = eb && eb[0] ? atoi(eb) : -1;  // -1 auto, 0 off, 1 = 2 x 2, 2 = 2 x 1
+    const bool can_m = f % 256 == 0, can_n = cb_bytes == 128 && c % (2 * bn) == 0;
+    int mh = 1, nh = 1;
+    if (blk == 1 || blk == 2) {
+        mh = can_m ? 2 : 1;
+        nh = blk == 1 && mh == 2 && can_n ? 2 : 1;
+    } else if (blk < 0 && k > 1 && can_m) {
+        // measured (config-4 layers, graph replays): 2 x 1 blocks take 3x3 256 @14
+        // 52 -> 39.5 us and 3x3 512 @7 48.7 -> 47.6 us (2 x 2: 41.8 / 49.1 -- the wider
+        // tile forces more split-K partials of a large dW); 1x1 layers are DRAM-bound
+        // and lose 2-5 us to the extra partials, so they keep the 128 x 128 tile
+        mh = 2;
+    }
     CParams p{};
     p.M = f; p.N = (int64_t)k * k * c;
-    p.tiles_m = (int)((f + 127) / 128);
-    p.tiles_n = (int)(p.N / bn);
+    p.tiles_m = (int)((f + 128 * mh - 1) / (128 * mh));
+    p.tiles_n = (int)(p.N / (nh * bn));
     p.num_kb = (int)((P + KPIX - 1) / KPIX);
     const int tiles = p.tiles_m * p.tiles_n;
     int splits = tiles >= num_sms() ? 1 : num_sms() / tiles;
@@ -491,8 +529,14 @@ static int wgrad(const void* x, const void* e, float* dw, int64_t n, int64_t h, 
     memset(&tqm, 0, sizeof(tqm));
     p.q_tma = 0;
     int rc;
-    if (cb_bytes == 128) rc = run<ES, 1, 128 / ES, 128>(ta, tb, tcm, tqm, p, st);
-    else rc = run<ES, 1, 64 / ES, 64>(ta, tb, tcm, tqm, p, st);
+    if (cb_bytes == 128) {
+        if (nh == 2) rc = run<ES, 1, 128 / ES, 128, 4, 2, 2>(ta, tb, tcm, tqm, p, st);
+        else if (mh == 2) rc = run<ES, 1, 128 / ES, 128, 4, 2, 1>(ta, tb, tcm, tqm, p, st);
+        else rc = run<ES, 1, 128 / ES, 128>(ta, tb, tcm, tqm, p, st);
+    } else {
+        if (mh == 2) rc = run<ES, 1, 64 / ES, 64, 4, 2, 1>(ta, tb, tcm, tqm, p, st);
+        else rc = run<ES, 1, 64 / ES, 64>(ta, tb, tcm, tqm, p, st);
+    }
     *nl = 1;
     if (splits > 1) {
         int64_t b = (mn + 255) / 256;

@@ -25,12 +25,14 @@ def fp8():
 
 @pytest.fixture
 def env():
-    old = os.environ.get("FP8B_CONV_HALO")
+    keys = ("FP8B_CONV_HALO", "FP8B_CONV_WGRAD_BLOCK", "FP8B_CONV_1X1_WGRAD_PIX")
+    old = {k: os.environ.get(k) for k in keys}
     yield os.environ
-    if old is None:
-        os.environ.pop("FP8B_CONV_HALO", None)
-    else:
-        os.environ["FP8B_CONV_HALO"] = old
+    for k, v in old.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
 
 
 def _qt(F, codes, shape, fmt):
@@ -232,3 +234,37 @@ def test_1x1_wgrad_gemm_route_exact(fp8, shape, out_mode):
             os.environ.pop("FP8B_CONV_1X1_WGRAD_PIX", None)
         else:
             os.environ["FP8B_CONV_1X1_WGRAD_PIX"] = old
+
+
+@pytest.mark.parametrize("shape", [(2, 256, 6, 6, 256, 3, 1, "fp8"), (3, 512, 5, 7, 256, 1, 0, "fp8"),
+                                   (2, 128, 9, 8, 256, 3, 1, "fp8"), (2, 64, 12, 10, 512, 1, 0, "fp8"),
+                                   (2, 128, 6, 6, 256, 3, 1, "fp16"), (2, 64, 5, 9, 256, 1, 0, "fp16"),
+                                   (2, 192, 6, 5, 256, 3, 1, "fp8")],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_wgrad_block_tiles_exact_grid(fp8, env, shape):
+    """im2col wgrad with block tiles (2 x 128 filter rows, 1 or 2 channel blocks
+    per CTA: half the operand bytes per MAC) == the 128 x 128 tiles == the exact
+    result, bit for bit, on an exact operand grid; Q(dW) codes and counters too."""
+    n, c, h, w, f, k, pad, fmt = shape
+    oh, ow = h + 2 * pad - k + 1, w + 2 * pad - k + 1
+    rng = np.random.default_rng(c + f + k)
+    xc = _grid(rng, n * h * w * c, fmt, 0.5).reshape(n, h, w, c)
+    ec = _grid(rng, n * oh * ow * f, fmt, 0.25).reshape(n, oh, ow, f)
+    dec = lambda a: O.dequantize(a.reshape(-1), fmt).astype(np.float64).reshape(a.shape)
+    from numpy.lib.stride_tricks import sliding_window_view as swv
+    xp = np.pad(dec(xc), ((0, 0), (pad, pad), (pad, pad), (0, 0)))
+    win = swv(xp, (k, k), axis=(1, 2))
+    dw_ex = np.einsum("nhwf,nhwcij->fijc", dec(ec), win, optimize=True).astype(np.float32)
+    X, E = _qt(fp8, xc, xc.shape, fmt), _qt(fp8, ec, ec.shape, fmt)
+    codes, cnt = O.quantize(dw_ex.reshape(-1), "fp8", "nearest-even")
+    env["FP8B_CONV_1X1_WGRAD_PIX"] = "0"   # keep 1x1 shapes on the im2col kernel
+    env["FP8B_CONV_HALO"] = "0"
+    for blk in ("1", "0"):
+        env["FP8B_CONV_WGRAD_BLOCK"] = blk
+        cq = fp8.Counters()
+        dw, q = fp8.conv2d_backward_weights(X, E, k, k, 1, pad, layout="nhwc", engine="tensor",
+                                            out_fmt="fp8", out_counters=cq)
+        np.testing.assert_array_equal(dw.cpu().numpy().reshape(-1), dw_ex.reshape(-1),
+                                      err_msg=f"block={blk}")
+        np.testing.assert_array_equal(q.codes.cpu().numpy(), codes.astype(np.uint8))
+        assert cq.values() == tuple(int(v) for v in cnt), blk

@@ -365,6 +365,30 @@ int64_t fp8b_launch_count(void);
 int fp8b_fill_synthetic(float *out, int64_t n, int32_t kind, uint64_t seed, double p,
                         double lo, double hi, void *stream);
 
+/* ------------------------------------------------- peer memory (multi-GPU) ---- */
+/* The data-parallel exchange of SURVEY 8e over NVLink / NVSwitch peer memory
+ * (no reference counterpart: the reference is single-process). Buffers that
+ * other processes of the node map: */
+#define FP8B_PEER_HANDLE_BYTES 64
+#define FP8B_MAX_PEERS 16
+int fp8b_peer_alloc(void **ptr, int64_t bytes, unsigned char handle[FP8B_PEER_HANDLE_BYTES]);
+int fp8b_peer_free(void *ptr);
+/* Map / unmap a buffer another PROCESS allocated with fp8b_peer_alloc. */
+int fp8b_peer_open(const unsigned char handle[FP8B_PEER_HANDLE_BYTES], void **ptr);
+int fp8b_peer_close(void *ptr);
+/* Fused reduce-scatter + Q node: for i in [0, n): s = peers[0][i0 + i] + peers[1][i0 + i]
+ * + ... in rank order (binary32, the same order on every rank), codes[i] =
+ * Q(s) with `cfg` (RNE, TRUNC, or SR with counter bits; cfg->block_offset * 4096 +
+ * i is the element's index in the unsharded tensor), counters as fp8b_quantize,
+ * and optionally sum_out[i] = s. `peers`: HOST array of `world` device pointers
+ * (this rank's own buffer and the fp8b_peer_open mappings), 16-byte aligned;
+ * i0 and n multiples of 4. The caller orders the step: every rank's partial
+ * must be complete before any rank launches this, and no rank may overwrite
+ * its partial until every reader is done. */
+int fp8b_peer_reduce_quantize(const float *const *peers, int32_t world, int64_t i0, int64_t n,
+                              float *sum_out, void *codes, int32_t fmt,
+                              const fp8b_quant_config_t *cfg, int64_t *counters, void *stream);
+
 /* Measurement aid (bench.py; no reference counterpart): streams n FP32 values
  * (n % 4 == 0, 16-byte aligned) with the quantizer's access pattern and writes
  * out_bytes in {0, 1, 2, 4} bytes per element with no arithmetic -- what HBM

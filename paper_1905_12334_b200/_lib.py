@@ -109,6 +109,12 @@ SIGNATURES = {
     "fp8b_fill_synthetic": (C.c_int, [_vp, _i64, _i32, _u64, C.c_double, C.c_double,
                                       C.c_double, _vp]),
     "fp8b_stream_probe": (C.c_int, [_vp, _vp, _i64, _i32, _vp]),
+    "fp8b_peer_alloc": (C.c_int, [C.POINTER(_vp), _i64, C.c_char_p]),
+    "fp8b_peer_free": (C.c_int, [_vp]),
+    "fp8b_peer_open": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "fp8b_peer_close": (C.c_int, [_vp]),
+    "fp8b_peer_reduce_quantize": (C.c_int, [C.POINTER(_vp), _i32, _i64, _i64, _vp, _vp, _i32,
+                                            C.POINTER(QuantConfig), _vp, _vp]),
 }
 
 

@@ -488,6 +488,77 @@ int fp8b_fill_synthetic(float* out, int64_t n, int32_t kind, uint64_t seed, doub
     return check_launch(1);
 }
 
+int fp8b_peer_alloc(void** ptr, int64_t bytes, unsigned char handle[FP8B_PEER_HANDLE_BYTES]) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == FP8B_PEER_HANDLE_BYTES, "handle size");
+    if (!ptr || bytes <= 0) return fail(FP8B_EINVAL, "peer_alloc: bad arguments");
+    void* p = nullptr;
+    if (cudaMalloc(&p, (size_t)bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FP8B_ECUDA, "peer_alloc: cudaMalloc failed");
+    }
+    if (handle) {
+        cudaIpcMemHandle_t h;
+        if (cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(p);
+            return fail(FP8B_ECUDA, "peer_alloc: cudaIpcGetMemHandle failed");
+        }
+        memcpy(handle, &h, sizeof(h));
+    }
+    *ptr = p;
+    return FP8B_OK;
+}
+int fp8b_peer_free(void* ptr) {
+    if (ptr && cudaFree(ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FP8B_ECUDA, "peer_free: cudaFree failed");
+    }
+    return FP8B_OK;
+}
+int fp8b_peer_open(const unsigned char handle[FP8B_PEER_HANDLE_BYTES], void** ptr) {
+    if (!handle || !ptr) return fail(FP8B_EINVAL, "peer_open: null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FP8B_ECUDA, "peer_open: cudaIpcOpenMemHandle failed");
+    }
+    *ptr = p;
+    return FP8B_OK;
+}
+int fp8b_peer_close(void* ptr) {
+    if (ptr && cudaIpcCloseMemHandle(ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FP8B_ECUDA, "peer_close: cudaIpcCloseMemHandle failed");
+    }
+    return FP8B_OK;
+}
+int fp8b_peer_reduce_quantize(const float* const* peers, int32_t world, int64_t i0, int64_t n,
+                              float* sum_out, void* codes, int32_t fmt,
+                              const fp8b_quant_config_t* cfg, int64_t* counters, void* stream) {
+    if (!cfg || !peers) return fail(FP8B_EINVAL, "peer_reduce_quantize: null argument");
+    if (world < 1 || world > FP8B_MAX_PEERS) return fail(FP8B_EINVAL, "peer_reduce_quantize: bad world size");
+    if (cfg->seed == 0) return fail(FP8B_EINVAL, "QuantConfig.seed must be nonzero");
+    if (!valid_fmt(fmt)) return fail(FP8B_EINVAL, "peer_reduce_quantize: unknown float format");
+    if (!valid_mode(cfg->mode)) return fail(FP8B_EINVAL, "unknown rounding mode");
+    if (cfg->mode == FP8B_SR && cfg->bits != FP8B_BITS_COUNTER)
+        return fail(FP8B_EINVAL, "peer_reduce_quantize: SR takes counter bits");
+    if (i0 < 0 || n < 0 || (i0 & 3) || (n & 3) || cfg->block_offset < 0)
+        return fail(FP8B_EINVAL, "peer_reduce_quantize: i0 and n must be non-negative multiples of 4");
+    if (n == 0) return FP8B_OK;
+    if (!codes) return fail(FP8B_EINVAL, "peer_reduce_quantize: null tensor");
+    for (int r = 0; r < world; ++r)
+        if (!peers[r] || ((uintptr_t)peers[r] % 16))
+            return fail(FP8B_EINVAL, "peer_reduce_quantize: null or unaligned peer buffer");
+    if (((uintptr_t)codes % 8) || (sum_out && ((uintptr_t)sum_out % 16)))
+        return fail(FP8B_EINVAL, "peer_reduce_quantize: unaligned output");
+    const int rc = fp8b::launch_peer_reduce_quantize(peers, world, i0, n, sum_out, codes, fmt, *cfg,
+                                                     counters, S(stream));
+    if (rc) return rc;
+    return check_launch(1);
+}
+
 int fp8b_stream_probe(const float* x, void* out, int64_t n, int32_t out_bytes, void* stream) {
     if (n < 0 || (n & 3) || (out_bytes != 0 && out_bytes != 1 && out_bytes != 2 && out_bytes != 4))
         return fail(FP8B_EINVAL, "stream_probe: bad arguments");

@@ -80,6 +80,11 @@ int64_t lfsr_cta_max_blocks();
 void note_launches(int n);
 void launch_fill_synthetic(float* out, int64_t n, int kind, uint64_t seed, double p, double lo,
                            double hi, cudaStream_t st);
+// peer.cu: fused rank-order sum of the ranks' FP32 partials + Q node over peer memory
+int launch_peer_reduce_quantize(const float* const* peers, int world, int64_t i0, int64_t n,
+                                float* sum_out, void* codes, int fmt,
+                                const fp8b_quant_config_t& cfg, int64_t* counters,
+                                cudaStream_t st);
 void launch_stream_probe(const float* x, void* out, int64_t n, int out_bytes, cudaStream_t st);
 
 }  // namespace fp8b

@@ -146,7 +146,18 @@ class ZeroDataParallelDense:
 
     def __init__(self, w_master_full, w_q, *, batch_per_rank: int, lr: float, mu: float,
                  two_lambda: float = 0.0, scaler=None, ops=None, group=None,
-                 master_mode: str = "nearest-even", seed: int = 1):
+                 master_mode: str = "nearest-even", seed: int = 1,
+                 transport: str = "collective"):
+        """transport "collective": reduce-scatter / all-gather through the process
+        group (NCCL on GPUs). "peer": one node, NVLink / NVSwitch peer memory --
+        every rank's FP32 dW lives in a buffer its peers map, the shard owner's
+        fused kernel sums the ranks' partials in rank order and applies Q(dW) in
+        the same pass (peer.py, csrc/peer.cu), and the E5M2 weight shards are
+        pulled from the owners' buffers; the two transports give identical bits
+        when the FP32 sums are order-independent."""
+        if transport not in ("collective", "peer"):
+            raise ValueError(f"unknown transport: {transport}")
+        self.transport = transport
         self.ops = ops or GpuOps()
         self.group = group
         distributed = dist.is_initialized()
@@ -166,9 +177,65 @@ class ZeroDataParallelDense:
         self.lr, self.mu, self.two_lambda = lr, mu, two_lambda
         self.scaler = scaler
         self.master_mode, self.seed = master_mode, seed
-        self._wq_pad = torch.zeros(self.per * self.world, dtype=w_q.dtype, device=dev)
+        if transport == "peer":
+            from .peer import PeerBuffer
+            if n % 4:
+                raise ValueError("peer transport needs a parameter count that is a multiple of 4")
+            self._dw_peer = PeerBuffer(4 * self.per * self.world, group)
+            self._wq_peer = PeerBuffer(self.per * self.world, group)
+            self._dw_full = self._dw_peer.view().view(torch.float32)
+            self._dw_full.zero_()
+            self._wq_pad = self._wq_peer.view()
+            self._wq_pad.zero_()
+        else:
+            self._wq_pad = torch.zeros(self.per * self.world, dtype=w_q.dtype, device=dev)
+
+    def _step_peer(self, x_local, e_local, iteration: int):
+        """The step over peer memory (transport="peer")."""
+        from .peer import fence, reduce_quantize
+        B, I, O = self.bpr, self.in_f, self.out_f
+        ops = self.ops
+        fwd, bwd = ops.counters(), ops.counters()
+        qx = ops.quantize(x_local.reshape(-1), counters=fwd)
+        qy = ops.gemm_q(qx, self.w_q, B, O, I, "k", "n", counters=fwd)
+        qe = ops.quantize(e_local.reshape(-1), counters=bwd)
+        # this rank's FP32 partial dW, written where its peers can read it
+        ops.gemm_f32(qx, qe, I, O, B, "m", "n", out=self._dw_full[: self.n])
+        qdx = ops.gemm_q(qe, self.w_q, B, I, O, "k", "k", counters=bwd)
+        fence(self.group)          # every rank's partial is complete
+        ns = self.end - self.start
+        qdw = torch.empty(ns, dtype=torch.uint8, device=self.w_q.device)
+        if ns:
+            reduce_quantize(self._dw_peer.ptrs, self.start, ns, qdw, counters=bwd,
+                            block_offset=self.block_offset)
+        gate = ops.ctensor(bwd)
+        if self.world > 1:
+            dist.all_reduce(gate, op=dist.ReduceOp.SUM, group=self.group)
+        lo = self.rank * self.per
+        if ns:
+            self._wq_pad[lo: lo + ns].copy_(self.w_q.reshape(-1)[self.start:self.end])
+            ops.update(qdw, self.w_master, self.momentum, lr=self.lr, mu=self.mu,
+                       two_lambda=self.two_lambda, scaler=self.scaler, skip_counters=bwd,
+                       master_mode=self.master_mode, seed=self.seed,
+                       w_e5m2=self._wq_pad[lo: lo + ns], block_offset=self.block_offset)
+        fence(self.group)          # every owner's new E5M2 shard is in its buffer
+        for r in range(self.world):  # pull the other owners' shards over NVLink
+            if r != self.rank:
+                s0, s1, _ = block_shard(self.n, self.world, r)
+                if s1 > s0:
+                    self._wq_pad[r * self.per: r * self.per + (s1 - s0)].copy_(
+                        self._wq_peer.view(r)[r * self.per: r * self.per + (s1 - s0)])
+        wflat = self.w_q.reshape(-1)
+        for r in range(self.world):
+            s0, s1, _ = block_shard(self.n, self.world, r)
+            wflat[s0:s1].copy_(self._wq_pad[r * self.per: r * self.per + (s1 - s0)])
+        if self.scaler is not None and hasattr(self.scaler, "step_async"):
+            self.scaler.step_async(True, iteration, counters=bwd)
+        return qy, qdx, gate
 
     def step(self, x_local, e_local, iteration: int):
+        if self.transport == "peer":
+            return self._step_peer(x_local, e_local, iteration)
         B, I, O = self.bpr, self.in_f, self.out_f
         ops = self.ops
         fwd, bwd = ops.counters(), ops.counters()

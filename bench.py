@@ -258,6 +258,7 @@ def run_ours(args):
     result["e2e"] = e2e_ours(F, args, x, stream)
     if rank == 0 and not args.no_extras:
         result["update"] = bench_update(F, args)
+        result["peer_reduce_quantize"] = bench_peer_reduce(F, args)
         result["gemm"] = bench_gemm(F, args, bf16_peak)
         result["dense_step"] = bench_dense_step(F, args)
         result["conv"] = bench_conv(F, args)
@@ -424,6 +425,37 @@ def bench_update(F, args):
                      "bytes_per_param": bpe}
     out["params"] = n
     return out
+
+
+def bench_peer_reduce(F, args):
+    """The fused rank-order sum + Q(dW) kernel of the peer-memory exchange
+    (fp8b_peer_reduce_quantize) on VIRTUAL peers: four buffers of this one GPU,
+    so the bytes come from HBM, not NVLink (one GPU here; the kernel only sees
+    pointers). GB/s of (4 x world + 1) bytes per element."""
+    import torch
+    from paper_1905_12334_b200.peer import PeerBuffer, reduce_quantize
+    n, world = 1 << 26, 4
+    bufs = [PeerBuffer(4 * n) for _ in range(world)]
+    for r, b in enumerate(bufs):
+        F.fill_synthetic(b.view().view(torch.float32), "normal", 40 + r, 1.0)
+    codes = torch.empty(n, dtype=torch.uint8, device="cuda")
+    cnt = F.Counters()
+    ptrs = [b.ptrs[0] for b in bufs]
+    for _ in range(3):
+        reduce_quantize(ptrs, 0, n, codes, counters=cnt)
+    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(10):
+        reduce_quantize(ptrs, 0, n, codes, counters=cnt)
+    b_.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b_) / 10
+    for bb in bufs:
+        bb.close()
+    return {"ms": round(ms, 4), "gbs": round(n * (4 * world + 1) / (ms * 1e-3) / 1e9, 1),
+            "elements": n, "virtual_peers": world,
+            "note": "peers are buffers of this GPU (HBM-bound stand-in); NVLink unmeasured"}
 
 
 def bench_gemm(F, args, bf16_peak):

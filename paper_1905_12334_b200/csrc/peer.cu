@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "quant_group.cuh"
 
 namespace fp8b {
 
@@ -25,7 +26,9 @@ struct PeerPtrs {
     const float* p[kMaxPeers];
 };
 
-// s[i] = peers[0][i0 + i] + peers[1][i0 + i] + ... (rank order), then the Q node.
+// s[i] = peers[0][i0 + i] + peers[1][i0 + i] + ... (rank order), then the Q node
+// of the elementwise quantize kernels (quant_group.cuh: the same code words,
+// counters and counter-bit stream as fp8b_quantize on the sum).
 template <int MB, int MODE>  // MODE 0 RNE, 1 SR counter bits, 3 TRUNC
 __global__ void __launch_bounds__(256) peer_reduce_quant_kernel(PeerPtrs peers, int world,
                                                                 int64_t i0, int64_t n,
@@ -34,35 +37,40 @@ __global__ void __launch_bounds__(256) peer_reduce_quant_kernel(PeerPtrs peers, 
                                                                 uint64_t seed, int saturate,
                                                                 int64_t elem_offset,
                                                                 int64_t* counters) {
+    constexpr int UN = 2;
     const bool sat = saturate != 0;
-    uint32_t co = 0, cu = 0, cn = 0;
+    uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int64_t ngroups = n >> 2;
-    const int mode = MODE == 0 ? FP8B_RNE : (MODE == 3 ? FP8B_TRUNC : FP8B_SR);
-    for (int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x; g < ngroups;
-         g += (int64_t)gridDim.x * 256) {
-        float4 s = __ldcs(reinterpret_cast<const float4*>(peers.p[0] + i0) + g);
-        for (int r = 1; r < world; ++r) {
-            const float4 v = __ldcs(reinterpret_cast<const float4*>(peers.p[r] + i0) + g);
-            s.x = __fadd_rn(s.x, v.x); s.y = __fadd_rn(s.y, v.y);
-            s.z = __fadd_rn(s.z, v.z); s.w = __fadd_rn(s.w, v.w);
-        }
-        if (sum_out) reinterpret_cast<float4*>(sum_out)[g] = s;
-        const float f[4] = {s.x, s.y, s.z, s.w};
-        uint32_t c[4];
+    const int64_t stride = (int64_t)gridDim.x * 256 * UN;
+    const uint32_t rb[4] = {0u, 0u, 0u, 0u};
+    for (int64_t g0 = (int64_t)blockIdx.x * 256 * UN + threadIdx.x; g0 < ngroups; g0 += stride) {
+        float4 s[UN];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int64_t i = 4 * g + k;
-            const uint32_t r16 = MODE == 1 ? counter_r16(seed, (uint64_t)(elem_offset + i)) : 0u;
-            int o, u, na;
-            c[k] = encode_int<MB>(__float_as_uint(f[k]), mode, r16, sat, o, u, na);
-            co += o; cu += u; cn += na;
+        for (int j = 0; j < UN; ++j) {
+            const int64_t g = g0 + j * 256;
+            if (g < ngroups) s[j] = __ldcs(reinterpret_cast<const float4*>(peers.p[0] + i0) + g);
         }
-        if (MB == 2)
-            reinterpret_cast<uint32_t*>(codes)[g] = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-        else
-            reinterpret_cast<uint2*>(codes)[g] = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+        for (int r = 1; r < world; ++r) {
+            const float4* pr = reinterpret_cast<const float4*>(peers.p[r] + i0);
+#pragma unroll
+            for (int j = 0; j < UN; ++j) {
+                const int64_t g = g0 + j * 256;
+                if (g >= ngroups) continue;
+                const float4 v = __ldcs(pr + g);
+                s[j].x = __fadd_rn(s[j].x, v.x); s[j].y = __fadd_rn(s[j].y, v.y);
+                s[j].z = __fadd_rn(s[j].z, v.z); s[j].w = __fadd_rn(s[j].w, v.w);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < UN; ++j) {
+            const int64_t g = g0 + j * 256;
+            if (g >= ngroups) continue;
+            if (sum_out) reinterpret_cast<float4*>(sum_out)[g] = s[j];
+            quant_group<MB, MODE>(s[j], rb, g, codes, seed, sat, elem_offset, c_big, c_nan, c_unf);
+        }
     }
-    if (counters) flush_counters<256>(co, cu, cn, counters);
+    if (counters)
+        flush_counters<256>(quant_group_overflow<MB, MODE>(c_big, c_nan), c_unf, c_nan, counters);
 }
 
 int launch_peer_reduce_quantize(const float* const* peers, int world, int64_t i0, int64_t n,
@@ -72,7 +80,7 @@ int launch_peer_reduce_quantize(const float* const* peers, int world, int64_t i0
     PeerPtrs pp;
     memset(&pp, 0, sizeof(pp));
     for (int r = 0; r < world; ++r) pp.p[r] = peers[r];
-    int64_t g = (n / 4 + 255) / 256;
+    int64_t g = (n / 4 + 511) / 512;
     const int64_t cap = (int64_t)device_sm_count() * 8;
     if (g > cap) g = cap;
     if (g < 1) g = 1;

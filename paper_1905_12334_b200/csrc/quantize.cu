@@ -204,6 +204,8 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
     if (lane == 0 && wid < nfull)
         p0_next = __ldg(tabs.pos + lfsr_split(seed, (uint64_t)(block_offset + wid)));
     mbar_wait(&tab_bar, 0);
+    float4 va[FP8B_LFSR_EPL / 4], vb[FP8B_LFSR_EPL / 4];
+    bool va_ready = false;
     for (int64_t b = wid; b < nfull; b += wstride) {
         const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, p0_next, 0);
         if (lane == 0 && b + wstride < nfull)
@@ -295,10 +297,13 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
             }
         };
         // two register sets in ping-pong, each chunk's loads issued one chunk
-        // ahead (no register copies between chunks)
-        float4 va[NV], vb[NV];
+        // ahead (no register copies between chunks), across block boundaries:
+        // the next block's first chunk is requested before this block's last
+        // chunk is processed (va_ready)
+        if (!va_ready) {
 #pragma unroll
-        for (int q = 0; q < NV; ++q) va[q] = __ldcs(xb + q);
+            for (int q = 0; q < NV; ++q) va[q] = __ldcs(xb + q);
+        }
 #pragma unroll 1
         for (int c = 0; c < kBlock / CH; c += 2) {
 #pragma unroll
@@ -307,6 +312,13 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
             if (c + 2 < kBlock / CH) {
 #pragma unroll
                 for (int q = 0; q < NV; ++q) va[q] = __ldcs(xb + (CH / 4) * (c + 2) + q);
+            } else if (b + wstride < nfull) {
+                const float4* xn = reinterpret_cast<const float4*>(x + (b + wstride) * kBlock) + NV * lane;
+#pragma unroll
+                for (int q = 0; q < NV; ++q) va[q] = __ldcs(xn + q);
+                va_ready = true;
+            } else {
+                va_ready = false;
             }
             chunk(vb, c + 1);
         }

@@ -170,7 +170,10 @@ __device__ __forceinline__ void codes_chunk(const P& p, const float (&y)[32], in
 // one box = one epilogue warp's 32 TMEM lanes for one column chunk.
 // KS: the kernel size when known at compile time (3: the tap loop fully
 // unrolled, every descriptor a constant offset), 0: any k at run time.
-template <int ES, int CB, int BN, int KS>
+// LEAN: compiled for the layer step's output only -- fused E5M2 RNE codes, no
+// FP32 y, no bias, no diagnostics -- so the epilogue warps issue far fewer
+// instructions beside the MMA-issuing warp they share an SM sub-partition with.
+template <int ES, int CB, int BN, int KS, int LEAN = 0>
 __global__ void __launch_bounds__(THREADS_MAX, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmQ,
@@ -367,13 +370,31 @@ __global__ void __launch_bounds__(THREADS_MAX, 1)
             int qpos = 0;
             uint8_t* qbuf = nullptr;
 #pragma unroll 1
-            for (int c = c_lo; any && !(p.dbg & 4) && c < c_lo + CPW && c * 32 < p.N; ++c) {
+            for (int c = c_lo; any && (LEAN || !(p.dbg & 4)) && c < c_lo + CPW && c * 32 < p.N; ++c) {
                 uint32_t v[32];
-                if (p.dbg & 256) {
+                if (!LEAN && (p.dbg & 256)) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = (uint32_t)(j * lane);
                 } else {
                     tmem_ld32(taddr + c * 32, v);
+                }
+                if (LEAN) {
+                    const int col0 = c * 32;
+                    const int nvalid = p.N - col0 < 32 ? (int)(p.N - col0) : 32;
+                    float y[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]);
+                    uint32_t w[8];
+                    lean_e5m2_codes(y, w, p.ep.cq_sat != 0, live, nvalid, co, cu, cn);
+                    if (qpos == 0) qbuf = acquire(qbase, nst_q, p.q_nbuf, qbox);
+                    if (p.qg == 4) stage_write<128, 8>(qbuf, qpos * 32, w, lane);
+                    else if (p.qg == 2) stage_write<64, 8>(qbuf, qpos * 32, w, lane);
+                    else stage_write<32, 8>(qbuf, qpos * 32, w, lane);
+                    if (++qpos == p.qg || c == c_lo + CPW - 1 || col0 + 32 >= p.N) {
+                        tma_store_4d(&tmQ, qbuf, lane, col0 - 32 * (qpos - 1), ow0, oh0 + r0, n);
+                        qpos = 0;
+                    }
+                    continue;
                 }
                 if (warp == 2 && lane == 0 && c == c_lo) HTRACE(6, (tile - blockIdx.x) / gridDim.x);
                 const int col0 = c * 32;
@@ -541,6 +562,13 @@ template <int ES, int CB, int BN>
 static int run(const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty, const CUtensorMap& tq,
                const HParams& p, const Plan& pl, cudaStream_t st) {
     auto fn = p.k == 3 ? conv_halo_kernel<ES, CB, BN, 3> : conv_halo_kernel<ES, CB, BN, 0>;
+    if constexpr (ES == 1) {
+        // the layer step's case: E5M2 RNE codes only (FP8B_CONV_HALO_LEAN=0 disables)
+        const char* el = getenv("FP8B_CONV_HALO_LEAN");
+        if (p.k == 3 && p.q_tma && !p.c_tma && !p.ep.c && !p.ep.bias && p.ep.cq_fmt == FP8B_E5M2 &&
+            p.ep.cq_mode == FP8B_RNE && p.dbg == 0 && !(el && el[0] == '0'))
+            fn = conv_halo_kernel<ES, CB, BN, 3, 1>;
+    }
     ensure_smem_attr((const void*)fn, (int)pl.smem);
     const int sms = device_sm_count();
     const int grid = p.ntiles < sms ? p.ntiles : sms;

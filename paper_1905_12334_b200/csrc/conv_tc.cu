@@ -124,7 +124,10 @@ struct Geo {
 
 // MODE 0: fprop (A = im2col X, K-major; B = W [F, taps*C], K-major).
 // MODE 1: wgrad (A = E [P, F], MN-major; B = im2col X, MN-major), split-K.
-template <int ES, int MODE, int BN, int CB, int EW, int MH = 1, int NH = 1>
+// LEAN (fprop): compiled for fused E5M2 RNE codes only (no FP32 y, no bias),
+// the layer step's output -- the generic epilogue's run-time cases cost ~200
+// instructions per 32-column chunk on the short-K passes it paces.
+template <int ES, int MODE, int BN, int CB, int EW, int MH = 1, int NH = 1, int LEAN = 0>
 __global__ void __launch_bounds__(threads_of<EW>(), 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmQ,
@@ -313,6 +316,17 @@ __global__ void __launch_bounds__(threads_of<EW>(), 1)
                     tmem_ld32(taddr + c * 32, v);
                     const int64_t col0 = (int64_t)tn * (NH * BN) + c * 32;
                     if (col0 >= p.N) continue;
+                    if (LEAN) {
+                        const bool last = c == c_lo + PER - 1 || col0 + 32 >= p.N;
+                        float y[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]);
+                        uint32_t w[8];
+                        const int nvalid = col0 + 32 <= p.N ? 32 : (int)(p.N - col0);
+                        lean_e5m2_codes(y, w, p.ep.cq_sat != 0, row < p.M, nvalid, co, cu, cn);
+                        stage_codes<1>(&et, w, col0, last);
+                        continue;
+                    }
                     if (p.c_tma || p.q_tma) {
                         if (MODE == 0) {
                             const bool last = c == c_lo + PER - 1 || col0 + 32 >= p.N;
@@ -408,9 +422,19 @@ template <int ES, int MODE, int BN, int CB, int EW = 4, int MH = 1, int NH = 1>
 static int run(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm,
                const CUtensorMap& tqm, const CParams& p, cudaStream_t st) {
     using G = Geo<ES, MODE, BN, CB, EW, MH, NH>;
-    ensure_smem_attr((const void*)conv_tc_kernel<ES, MODE, BN, CB, EW, MH, NH>, G::SMEM);
     const int items = p.tiles_m * p.tiles_n * p.splits;
     const int grid = items < num_sms() ? items : num_sms();
+    if constexpr (ES == 1 && MODE == 0) {
+        // the layer step's output (FP8B_CONV_LEAN=0 disables)
+        const char* el = getenv("FP8B_CONV_LEAN");
+        if (p.q_tma && !p.c_tma && !p.ep.c && !p.ep.bias && p.ep.cq_fmt == FP8B_E5M2 &&
+            p.ep.cq_mode == FP8B_RNE && !(el && el[0] == '0')) {
+            ensure_smem_attr((const void*)conv_tc_kernel<ES, MODE, BN, CB, EW, 1, 1, 1>, G::SMEM);
+            conv_tc_kernel<ES, MODE, BN, CB, EW, 1, 1, 1><<<grid, threads_of<EW>(), G::SMEM, st>>>(ta, tb, tcm, tqm, p);
+            return FP8B_OK;
+        }
+    }
+    ensure_smem_attr((const void*)conv_tc_kernel<ES, MODE, BN, CB, EW, MH, NH>, G::SMEM);
     conv_tc_kernel<ES, MODE, BN, CB, EW, MH, NH><<<grid, threads_of<EW>(), G::SMEM, st>>>(ta, tb, tcm, tqm, p);
     return FP8B_OK;
 }

@@ -285,8 +285,8 @@ __global__ void __launch_bounds__(NT, MINB) sgd_elem_kernel(const void* __restri
 #endif
 constexpr int kWarpUpdThreads = FP8B_UPD_THREADS;
 constexpr int kUpdTabBytes = ((kLfsrPeriod + kBlock) * 2 + 15) & ~15;
-template <int GFMT, bool CNT>
-__global__ void __launch_bounds__(kWarpUpdThreads, 1)
+template <int GFMT, bool CNT, int NT = kWarpUpdThreads>
+__global__ void __launch_bounds__(NT, 1)
     sgd_lfsr_warp_kernel(const void* __restrict__ grad, uint16_t* __restrict__ master,
                          float* __restrict__ mom, int64_t nfull, UpdArgs a, int64_t block_offset,
                          LfsrTables tabs) {
@@ -407,8 +407,8 @@ __global__ void __launch_bounds__(kWarpUpdThreads, 1)
             }
         }
     }
-    if (CNT && a.mcnt) flush_counters<kWarpUpdThreads>(mb - mn, mu_, mn, a.mcnt);
-    if (CNT && a.wcnt) flush_counters<kWarpUpdThreads>(wb - wn, wu, wn, a.wcnt);
+    if (CNT && a.mcnt) flush_counters<NT>(mb - mn, mu_, mn, a.mcnt);
+    if (CNT && a.wcnt) flush_counters<NT>(wb - wn, wu, wn, a.wcnt);
     upd_tail(a);
 }
 
@@ -541,13 +541,39 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
         if (aligned && n / kBlock > lfsr_cta_max_blocks()) {
             const int64_t nfull = n / kBlock;
             constexpr int smem = kUpdTabBytes;
-            auto fn = cnt ? sgd_lfsr_warp_kernel<GFMT, true> : sgd_lfsr_warp_kernel<GFMT, false>;
-            ensure_smem_attr((const void*)fn, smem);
             // one warp per 4096-block: a small tensor (config 1: 256 blocks)
             // spreads its warps over every SM instead of filling a few CTAs
             int64_t g = sm_count();
-            int64_t wpc = (nfull + g - 1) / g;
-            if (wpc > kWarpUpdThreads / 32) wpc = kWarpUpdThreads / 32;
+            // A warp walks a block as a serial chain of 16 chunks whose pace is
+            // ~max(1.1 us, 0.082 us x warps per SM) (latency floor, then HBM), and
+            // a partly filled last round of blocks costs a whole round: time ~
+            // rounds(w) x pace(w). Pick the warps per CTA that minimise it
+            // (measured: 2^24 parameters = 4096 blocks, 24 warps: 2 rounds, 63 us;
+            // 28-32 warps: 1 round, 39 us; 2^26: 24 warps 160 us, 32 warps 170 us).
+            // More than 24 warps take the 1024-thread instantiation (64 registers,
+            // a few spills). FP8B_UPD_WARPS forces a count (diagnostic).
+            static const int force = [] { const char* e = getenv("FP8B_UPD_WARPS"); return e ? atoi(e) : 0; }();
+            constexpr int kW = kWarpUpdThreads / 32;
+            int wbest = kW;
+            if (nfull <= g * kW) {
+                wbest = (int)((nfull + g - 1) / g);  // one round, spread over every SM
+            } else {
+                auto cost = [&](int w) {
+                    const double rounds = (double)((nfull + g * w - 1) / (g * w));
+                    double pace = 0.082 * w > 1.1 ? 0.082 * w : 1.1;
+                    if (w > kW) pace *= 1.05;
+                    return rounds * pace;
+                };
+                double cbest = cost(kW);
+                for (int w = 16; w <= 32; ++w)  // leave the default only for a clear (3 %) gain
+                    if (cost(w) < cbest * 0.97) { cbest = cost(w); wbest = w; }
+            }
+            if (force >= 1 && force <= 32) wbest = force;
+            const bool big = wbest > kWarpUpdThreads / 32;
+            auto fn = big ? (cnt ? sgd_lfsr_warp_kernel<GFMT, true, 1024> : sgd_lfsr_warp_kernel<GFMT, false, 1024>)
+                          : (cnt ? sgd_lfsr_warp_kernel<GFMT, true> : sgd_lfsr_warp_kernel<GFMT, false>);
+            ensure_smem_attr((const void*)fn, smem);
+            int64_t wpc = wbest;
             const int64_t need = (nfull + wpc - 1) / wpc;
             if (need < g) g = need;
             a.step_scaler = want_step && nfull == nb;  // no tail kernel follows

@@ -538,7 +538,16 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     if (args.master_mode == FP8B_SR && args.bits == FP8B_BITS_LFSR) {
         const int64_t nb = (n + kBlock - 1) / kBlock;
         int64_t begin = 0;
-        if (aligned && n / kBlock > lfsr_cta_max_blocks()) {
+        // up to one resident wave of CTA-per-block CTAs (4 per SM at 64 registers)
+        // the CTA kernel wins: its 256 threads take a block at once, while a warp
+        // walks it as 16 dependent chunks (2.36M parameters = 576 blocks: 17 -> 9 us)
+        int64_t cta_max = lfsr_cta_max_blocks();
+        if (!getenv("FP8B_LFSR_CTA_MAX")) {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sgd_lfsr_kernel<GFMT>, 256, 0);
+            if ((int64_t)per_sm * sm_count() > cta_max) cta_max = (int64_t)per_sm * sm_count();
+        }
+        if (aligned && n / kBlock > cta_max) {
             const int64_t nfull = n / kBlock;
             constexpr int smem = kUpdTabBytes;
             // one warp per 4096-block: a small tensor (config 1: 256 blocks)

@@ -254,3 +254,11 @@ def test_zero1_overflow_on_one_rank_skips_all_shards():
         assert gate[0] > 0
         np.testing.assert_array_equal(wm.reshape(-1).view(np.uint16), m0)
         np.testing.assert_array_equal(wq.reshape(-1), qw0)
+
+
+def test_zero1_rejects_unknown_transport():
+    import pytest
+    w = torch.zeros(8, 8, dtype=torch.int16)
+    with pytest.raises(ValueError):
+        ZeroDataParallelDense(w, w.to(torch.uint8), batch_per_rank=2, lr=0.1, mu=0.9,
+                              ops=CpuOps(), transport="carrier-pigeon")

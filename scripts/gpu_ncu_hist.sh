@@ -8,4 +8,5 @@ timeout 600 $NCU --set full --clock-control none --import-source on -k regex:$k 
     -o gpurun_out/prof_$name -f "$@" > gpurun_out/ncu_$name.log 2>&1
 $NCU -i gpurun_out/prof_$name.ncu-rep --page source --csv --print-source sass > gpurun_out/src_$name.csv 2>/dev/null
 python scripts/src_hist.py gpurun_out/src_$name.csv ${WANT:-}
+[ -n "$LIST" ] && python scripts/src_list.py gpurun_out/src_$name.csv $LIST > gpurun_out/list_$name.txt
 rm -f gpurun_out/prof_$name.ncu-rep gpurun_out/src_$name.csv

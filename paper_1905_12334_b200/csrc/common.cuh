@@ -538,4 +538,17 @@ __device__ __forceinline__ void qnode_store(const QNode& q, int64_t i, float v, 
     co += o; cu += u; cn += n;
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// A kernel launched with programmatic stream serialization (tc_common.cuh
+// launch_pdl: the tcgen05 GEMM) may have its CTAs scheduled, and run its
+// prologue, while the previous kernel of the stream is still running, once every
+// CTA of that kernel has executed pdl_trigger (or exited). The dependent blocks
+// in pdl_wait -- before its first global-memory access -- until the previous
+// kernel has completed and its writes are visible, so nothing observable
+// changes; what is hidden is the ~2.8 us dependent-node latency plus the GEMM's
+// prologue behind a short producer (the Q node before a layer's GEMM). Both are
+// no-ops for plain launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace fp8b

@@ -514,6 +514,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo2<NB, EW, NBUF, A
     cluster_sync_all();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: from here on the previous kernel of the stream is complete (the
+    // stream-K variant draws its ticket from global memory above and is
+    // launched the plain way)
+    pdl_wait();
     // (32-bit unit arithmetic: the host keeps sk_units * nclusters < 2^31)
     int ticket = 0;
     uint32_t sk_u0 = 0, sk_u1 = 0;
@@ -1220,7 +1224,7 @@ static int launch_2sm_ast(const CUtensorMap& tA2, const CUtensorMap& tB2, const 
     int grid2 = 2 * p2.tiles_m;
     const int maxg = num_sms & ~1;
     if (grid2 > maxg) grid2 = maxg;
-    gemm_tc2_kernel<ES, 1, EW, NBUF, LEAN, AST><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tq2, p2);
+    launch_pdl(gemm_tc2_kernel<ES, 1, EW, NBUF, LEAN, AST>, grid2, G::THREADS, G::SMEM, st, tA2, tB2, tmC, tq2, p2);
     return FP8B_OK;
 }
 
@@ -1296,7 +1300,7 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
         pk.ep = EpiArgs{ws, nullptr, nullptr, 0, 0, 0, 0, nullptr};
         int grid2 = 2 * ntiles2 * splits;
         if (grid2 > maxg) grid2 = maxg;
-        gemm_tc2_kernel<ES, NB, EW, NBUF, 0><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmW, tmQ, pk);
+        launch_pdl(gemm_tc2_kernel<ES, NB, EW, NBUF, 0>, grid2, G::THREADS, G::SMEM, st, tA2, tB2, tmW, tmQ, pk);
         Params pf = p2;
         pf.splits = splits;
         const int64_t nch = m * ((n + 31) / 32);
@@ -1313,7 +1317,7 @@ static int launch_2sm(const CUtensorMap& tA2, const CUtensorMap& tB2, const CUte
     const int dp_tiles = choose_sk(ntiles2, maxg / 2, p.num_kb, NB);
     if (p.dbg == 0 && dp_tiles >= 0 && (int64_t)ntiles2 * p.num_kb * (maxg / 2) < (1ll << 31))
         return launch_2sm_sk<ES, NB>(tA2, tB2, tmC, tmQ, p, m, n, dp_tiles, maxg, st);
-    gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN><<<grid2, G::THREADS, G::SMEM, st>>>(tA2, tB2, tmC, tq2, p2);
+    launch_pdl(gemm_tc2_kernel<ES, NB, EW, NBUF, LEAN>, grid2, G::THREADS, G::SMEM, st, tA2, tB2, tmC, tq2, p2);
     return FP8B_OK;
 }
 

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(NT, (UN == 2 && NT == 256 && PF == 0) ? 8 : 1)
                                                         int64_t elem_offset,
                                                         const uint32_t* __restrict__ rbits,
                                                         int64_t* counters) {
+    pdl_trigger();  // a PDL-launched consumer (the layer's GEMM) may start its prologue
     const bool sat = saturate != 0;
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int64_t ngroups = n >> 2;  // float4 groups

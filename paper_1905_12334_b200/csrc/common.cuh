@@ -6,6 +6,8 @@
 // inputs (checked on the B200 by tests/test_quantize_gpu.py::test_exhaustive).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -550,5 +552,28 @@ __device__ __forceinline__ void qnode_store(const QNode& q, int64_t i, float v, 
 // no-ops for plain launches.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Launch with programmatic stream serialization (see pdl_wait above).
+// FP8B_PDL=0 launches the plain way.
+inline bool pdl_enabled() {
+    static const bool on = [] { const char* e = getenv("FP8B_PDL"); return !(e && e[0] == '0'); }();
+    return on;
+}
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, KArgs(args)...);
+}
+
 
 }  // namespace fp8b

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(NT, (UN == 2 && NT == 256 && PF == 0) ? 8 : 1)
                                                         const uint32_t* __restrict__ rbits,
                                                         int64_t* counters) {
     pdl_trigger();  // a PDL-launched consumer (the layer's GEMM) may start its prologue
+    pdl_wait();     // and this kernel, launched the same way, waits for its predecessor here
     const bool sat = saturate != 0;
     uint32_t c_big = 0, c_nan = 0, c_unf = 0;
     const int64_t ngroups = n >> 2;  // float4 groups
@@ -198,7 +199,11 @@ __global__ void __launch_bounds__(kWarpLfsrThreads, 1)
             bulk_g2s(smem + off, reinterpret_cast<const uint8_t*>(tabs.tabx) + off, len, &tab_bar);
         }
     }
+    pdl_trigger();
     __syncthreads();
+    // PDL: the jump-table copy above (constant data) overlaps the previous
+    // kernel's tail; the tensors are touched only after it has completed
+    pdl_wait();
     const uint32_t stab_addr = smem_addr(smem);
     // lane 0 derives LfsrStream::split(seed, block) one block ahead
     uint32_t p0_next = 0;
@@ -511,8 +516,8 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
                 if (wpc > kWarpLfsrThreads / 32) wpc = kWarpLfsrThreads / 32;
                 const int64_t need = (nfull + wpc - 1) / wpc;
                 if (need < g) g = need;
-                fn<<<(int)g, (int)(32 * wpc), smem, st>>>(x, codes, nfull, cfg.seed, cfg.saturate,
-                                                          cfg.block_offset, tabs, counters);
+                launch_pdl(fn, (unsigned)g, (unsigned)(32 * wpc), (size_t)smem, st, x, codes, nfull, cfg.seed,
+                           cfg.saturate, cfg.block_offset, tabs, counters);
                 begin = nfull;
             }
         }
@@ -545,7 +550,8 @@ static void launch_quant(const float* x, void* codes, int64_t n, const fp8b_quan
         auto fn = quant_elem_kernel<MB, MODE, TN, UN, PF>;                                     \
         const int64_t items = (n / 4 + TN * UN - 1) / (TN * UN);                               \
         const int g = grid_for((const void*)fn, TN, items);                                    \
-        fn<<<g, TN, 0, st>>>(x, codes, n, cfg.seed, cfg.saturate, eoff, cfg.rbits, counters);  \
+        launch_pdl(fn, (unsigned)g, (unsigned)TN, 0, st, x, codes, n, cfg.seed, cfg.saturate, eoff, \
+                   cfg.rbits, counters);                                                       \
     }
 #define FP8B_LAUNCH_ELEM(MODE)                                                  \
     {                                                                           \

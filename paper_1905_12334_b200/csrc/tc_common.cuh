@@ -89,27 +89,7 @@ __device__ __forceinline__ void fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 
-// Launch with programmatic stream serialization (see common.cuh pdl_wait).
-// FP8B_PDL=0 launches the plain way.
-inline bool pdl_enabled() {
-    static const bool on = [] { const char* e = getenv("FP8B_PDL"); return !(e && e[0] == '0'); }();
-    return on;
-}
-template <class... KArgs, class... Args>
-inline cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
-                              cudaStream_t st, Args&&... args) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, KArgs(args)...);
-}
+using fp8b::launch_pdl;  // common.cuh
 
 // UMMA shared-memory matrix descriptor, version 1 (sm_100); layout 2 =
 // SWIZZLE_128B (default), 4 = SWIZZLE_64B.

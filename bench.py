@@ -638,7 +638,7 @@ def bench_conv(F, args, reps=5, only=None):
         side2 = torch.cuda.Stream()
 
         def step():
-            bwd.zero_()
+            # (no zeroing launch: the update's fused tail hands bwd back cleared)
             # fprop, dgrad and wgrad only read X, W and E: three parallel branches
             # of the captured graph (each kernel fills the GPU, so what overlaps
             # is launch latency and the tails), joined before the update
@@ -656,7 +656,7 @@ def bench_conv(F, args, reps=5, only=None):
             cur.wait_stream(side2)
             F.sgd_momentum_update(qdw.codes, "fp8", master, mom, lr=0.1, mu=0.9, scaler=scaler,
                                   skip_counters=bwd, master_mode="stochastic", seed=5,
-                                  w_e5m2=W.codes, step_scaler_iteration=0)
+                                  w_e5m2=W.codes, step_scaler_iteration=0, clear_skip_counters=True)
         sms = _graph_ms(step, reps)
         tot_step += sms
         res[name] = {"passes_f32": row,

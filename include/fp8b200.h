@@ -200,7 +200,9 @@ typedef struct {
                                    CTA -- the fp8b_loss_scaler_step that follows the
                                    iteration's last update (nn.cpp:546-547) without its
                                    own launch. At most one such update per scaler in
-                                   flight. */
+                                   flight. 2: the same, and the gate's input counters
+                                   (skip_counters, skip_counters2) are then cleared for the
+                                   next step, so a step needs no zeroing launch. */
     int64_t *w_counters;        /* device int64[3] or NULL */
     int64_t step_iteration;     /* for step_scaler */
     const int64_t *skip_counters2; /* optional second int64[3]: the gate is the element-wise

@@ -586,7 +586,8 @@ def sgd_momentum_update(grad: torch.Tensor, grad_fmt: str, master: torch.Tensor,
                         w_counters: Optional[Counters] = None,
                         step_scaler_iteration: Optional[int] = None,
                         skip_counters2: Optional[Counters] = None,
-                        gate_out: Optional[Counters] = None, stream=None) -> None:
+                        gate_out: Optional[Counters] = None,
+                        clear_skip_counters: bool = False, stream=None) -> None:
     """update_tensor (nn.cpp:417-432) for one parameter tensor, in place.
 
     grad: device codes (grad_fmt "fp8"/"fp16") or FP32 values (grad_fmt "f32");
@@ -595,7 +596,8 @@ def sgd_momentum_update(grad: torch.Tensor, grad_fmt: str, master: torch.Tensor,
     also runs LossScaler::step(grads_finite(skip_counters), iteration) on
     `scaler` once every CTA has read the scale -- no separate step launch.
     skip_counters2 / gate_out: the gate is skip_counters + skip_counters2, and
-    (with step_scaler_iteration) the merged counts are stored in gate_out."""
+    (with step_scaler_iteration) the merged counts are stored in gate_out;
+    clear_skip_counters then also zeroes the gate's inputs for the next step."""
     gf = {"fp8": _lib.E5M2, "e5m2": _lib.E5M2, "fp16": _lib.FP16, "f32": _lib.F32}.get(grad_fmt)
     if gf is None:
         raise ValueError(f"unknown gradient format: {grad_fmt}")
@@ -608,7 +610,7 @@ def sgd_momentum_update(grad: torch.Tensor, grad_fmt: str, master: torch.Tensor,
                         _mode(master_mode), _BITS[bits], int(seed), int(block_offset),
                         _ptr(rbits), master_counters.ptr if master_counters else None,
                         _ptr(w_e5m2), int(bool(w_saturate)),
-                        0 if step_scaler_iteration is None else 1,
+                        0 if step_scaler_iteration is None else (2 if clear_skip_counters else 1),
                         w_counters.ptr if w_counters else None,
                         0 if step_scaler_iteration is None else int(step_scaler_iteration),
                         skip_counters2.ptr if skip_counters2 is not None else None,

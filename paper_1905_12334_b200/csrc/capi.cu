@@ -453,6 +453,8 @@ int fp8b_sgd_momentum_update(const void* grad, int32_t grad_fmt, uint16_t* maste
     }
     if (!args->scaler && !(args->scale > 0.0f))
         return fail(FP8B_EINVAL, "loss scale must be finite and positive");
+    if (args->step_scaler < 0 || args->step_scaler > 2)
+        return fail(FP8B_EINVAL, "sgd: step_scaler must be 0, 1 or 2");
     if (args->step_scaler && !args->scaler)
         return fail(FP8B_EINVAL, "sgd: step_scaler needs a device scaler");
     if (args->gate_out && !args->step_scaler)

@@ -96,6 +96,12 @@ __device__ __forceinline__ void upd_tail(const UpdArgs& a) {
                     for (int i = 0; i < 3; ++i) a.gate_out[i] = a.skip[i];
                 scaler_step_dev(sc, a.skip, 1, a.iteration);
             }
+            if (a.step_scaler == 2) {  // hand the gate's inputs back cleared (no zeroing launch next step)
+                for (int i = 0; i < 3; ++i) {
+                    if (a.skip) const_cast<int64_t*>(a.skip)[i] = 0;
+                    if (a.skip2) const_cast<int64_t*>(a.skip2)[i] = 0;
+                }
+            }
         }
     }
 }
@@ -529,7 +535,7 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
     a.iteration = args.step_iteration;
     a.skip2 = args.skip_counters2;
     a.gate_out = args.gate_out;
-    const int want_step = args.step_scaler && args.scaler;
+    const int want_step = args.scaler ? args.step_scaler : 0;
     constexpr int NT = 256;
     const bool cnt = a.mcnt != nullptr || a.wcnt != nullptr;
     const bool aligned = ((uintptr_t)grad % 16 == 0) && ((uintptr_t)master % 16 == 0) &&
@@ -585,7 +591,7 @@ static void launch_sgd_fmt(const void* grad, uint16_t* master, float* mom, int64
             int64_t wpc = wbest;
             const int64_t need = (nfull + wpc - 1) / wpc;
             if (need < g) g = need;
-            a.step_scaler = want_step && nfull == nb;  // no tail kernel follows
+            a.step_scaler = nfull == nb ? want_step : 0;  // no tail kernel follows
             fn<<<(int)g, (int)(32 * wpc), smem, st>>>(grad, master, mom, nfull, a, args.block_offset,
                                                       tabs);
             begin = nfull;

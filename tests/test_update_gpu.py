@@ -246,3 +246,37 @@ def test_merged_gate_two_counter_sets(fp8, n):
         np.testing.assert_array_equal(res[0][0], res[1][0])
         np.testing.assert_array_equal(res[0][1], res[1][1])
         assert res[0][3] == res[1][3]
+
+
+@pytest.mark.parametrize("n", [5000, 700 * 4096 + 33])
+def test_fused_step_clears_gate_inputs(fp8, n):
+    """clear_skip_counters (step_scaler = 2): after the update and the fused
+    scaler step the gate's input counters are zero again, the merged gate is in
+    gate_out, and masters / momentum / scaler state equal the non-clearing run."""
+    import torch
+    rng = np.random.default_rng(n % 911)
+    m0 = O.quantize(rng.normal(0, 1 / 32, n).astype(np.float32), "fp16")[0].view(np.int16)
+    g0 = O.quantize(rng.normal(0, 1.0, n).astype(np.float32), "fp8")[0].astype(np.uint8)
+    res = []
+    for clear in (False, True):
+        master, mom, grad = _dev(m0.copy()), _dev(np.zeros(n, np.float32)), _dev(g0)
+        sc = fp8.LossScaler("dynamic-backoff", 65536.0, growth_interval=2,
+                            min_threshold_schedule=[(0, 8192.0)])
+        a, b, gate = fp8.Counters(), fp8.Counters(), fp8.Counters()
+        for it, (c1, c2) in enumerate([((0, 3, 0), (0, 1, 0)), ((1, 0, 0), (0, 0, 0)),
+                                       ((0, 0, 0), (0, 2, 0))]):
+            a.t.copy_(torch.tensor(c1)); b.t.copy_(torch.tensor(c2))
+            fp8.sgd_momentum_update(grad, "fp8", master, mom, lr=0.05, mu=0.9, scaler=sc,
+                                    skip_counters=a, skip_counters2=b, gate_out=gate,
+                                    master_mode="stochastic", seed=3 + it,
+                                    step_scaler_iteration=it, clear_skip_counters=clear)
+            assert gate.values() == tuple(x + y for x, y in zip(c1, c2))
+            if clear:
+                assert a.values() == (0, 0, 0) and b.values() == (0, 0, 0)
+            else:
+                assert a.values() == c1 and b.values() == c2
+        res.append((master.cpu().numpy(), mom.cpu().numpy().view(np.uint32),
+                    sc.state.cpu().numpy().tobytes()))
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    np.testing.assert_array_equal(res[0][1], res[1][1])
+    assert res[0][2] == res[1][2]
